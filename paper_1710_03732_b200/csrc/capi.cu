@@ -1,0 +1,514 @@
+// capi.cu — the C-ABI (include/qapb200.h) over the device engine.
+//
+// Exceptions never cross the boundary: each entry point maps the C++
+// exception type the reference would throw (SURVEY.md §8b "Errors") onto a
+// status code and a thread-local message.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/qapb200.h"
+#include "engine.h"
+#include "kernels.h"
+
+using qapb::CudaError;
+using qapb::Engine;
+
+struct qapb_engine {
+  std::unique_ptr<Engine> e;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+qapb_status guard(F&& f) {
+  try {
+    f();
+    return QAPB_OK;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return QAPB_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return QAPB_EINVAL;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return QAPB_ELOGIC;
+  } catch (const std::bad_alloc& e) {
+    g_err = "out of host memory";
+    return QAPB_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return QAPB_ERUNTIME;
+  }
+}
+
+void need(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+// ---- host-side store helpers (reference API, not on the hot path) -------
+struct HIdx {  // StoreIndex, rlt2.hpp:25-69
+  int m, lpairs, esz;
+  explicit HIdx(int m_) : m(m_), lpairs(m_ * (m_ - 1)), esz((m_ - 2) * (m_ - 2)) {}
+  int fpair(int i, int j) const { return i * m - i * (i + 1) / 2 + (j - i - 1); }
+  int lpair(int p, int q) const { return p * (m - 1) + q - (q > p); }
+  int tile(int i, int j, int p, int q) const { return fpair(i, j) * lpairs + lpair(p, q); }
+  int cell(int i, int j, int p, int q, int k, int r) const {
+    const int kl = k - (k > i) - (k > j);
+    const int lo = p < q ? p : q, hi = p < q ? q : p;
+    return kl * (m - 2) + (r - (r > lo) - (r > hi));
+  }
+  void uncell(int i, int j, int p, int q, int c, int* k, int* r) const {
+    int kk = c / (m - 2), rr = c % (m - 2);
+    if (kk >= i) ++kk;
+    if (kk >= j) ++kk;
+    const int lo = p < q ? p : q, hi = p < q ? q : p;
+    if (rr >= lo) ++rr;
+    if (rr >= hi) ++rr;
+    *k = kk;
+    *r = rr;
+  }
+  size_t cidx(int i, int p, int j, int q) const {
+    return ((size_t)i * m + p) * (m - 1) * (m - 1) + (size_t)(j - (j > i)) * (m - 1) +
+           (q - (q > p));
+  }
+  int tiles() const { return (m * (m - 1) / 2) * lpairs; }
+};
+
+size_t nb_of(int m) { return (size_t)m * m; }
+size_t nc_of(int m) { return (size_t)m * m * (m - 1) * (m - 1); }
+size_t nd_of(int m) { return m >= 3 ? (size_t)HIdx(m).tiles() * (m - 2) * (m - 2) : 0; }
+}  // namespace
+
+extern "C" {
+
+QAPB_API const char* qapb_last_error(void) { return g_err.c_str(); }
+QAPB_API int qapb_abi_version(void) { return 1; }
+
+QAPB_API void qapb_config_init(qapb_config* c) {  // rlt2.hpp:98-121
+  std::memset(c, 0, sizeof *c);
+  c->variant = QAPB_F1;
+  c->sa_enabled = 0;
+  c->iter_limit = 100;
+  c->min_gap = 0.0;
+  c->kappa_z_upper = 2.0 / 3.0;
+  c->phi_split = 0.5;
+  c->kappa_y = 1.0;
+  c->kappa_x = 1.0;
+  c->varphi = 0.5;
+  c->sa_t0_fraction = 0.04;
+  c->sa_kappa_lb_cap = 0.25;
+  c->sa_cool_factor = 0.99;
+  c->sa_cool_period = 100;
+  c->workers = 1;
+  c->seed = 0;
+  c->upper_bound = std::numeric_limits<double>::infinity();
+  c->fathom_threshold = std::numeric_limits<double>::infinity();
+  c->early_stop_window = 0;
+  c->early_stop_delta = 0.0002;
+  c->record_history = 1;
+  c->device = 0;
+}
+
+QAPB_API qapb_status qapb_device_count(int* count) {
+  return guard([&] { qapb::cuda_check(cudaGetDeviceCount(count), "cudaGetDeviceCount"); });
+}
+
+QAPB_API const char* qapb_variant_name(int v) {  // rlt2.cpp:24-32
+  switch (v) {
+    case QAPB_F1: return "F1";
+    case QAPB_F2: return "F2";
+    case QAPB_S1: return "S1";
+    case QAPB_S2: return "S2";
+  }
+  return "?";
+}
+
+QAPB_API qapb_status qapb_parse_variant(const char* s, int* variant) {  // rlt2.cpp:34-42
+  return guard([&] {
+    std::string t;
+    for (const char* p = s; *p; ++p) t += (char)std::toupper((unsigned char)*p);
+    if (t == "F1") *variant = QAPB_F1;
+    else if (t == "F2") *variant = QAPB_F2;
+    else if (t == "S1") *variant = QAPB_S1;
+    else if (t == "S2") *variant = QAPB_S2;
+    else throw std::invalid_argument("unknown variant: " + std::string(s));
+  });
+}
+
+// ---- LAP ---------------------------------------------------------------
+QAPB_API qapb_status qapb_lap_solve_batch_device(const double* costs, int m, int count,
+                                                 double* values, int* r2c, int* c2r, double* u,
+                                                 double* v, void* stream) {
+  return guard([&] {
+    need(m > 0, "lap: m must be positive");  // lap.cpp:26
+    need(m <= qapb::lap_max_m(), "lap: m exceeds the device solver limit");
+    need(count >= 0, "lap: count must be non-negative");
+    if (count == 0) return;
+    int* counter = nullptr;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    qapb::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(int), st),
+                     "cudaMallocAsync");
+    qapb::cuda_check(cudaMemsetAsync(counter, 0, sizeof(int), st), "memset");
+    qapb::BatchLapParams p{};
+    p.costs = costs;
+    p.m = m;
+    p.count = count;
+    p.counter = counter;
+    p.values = values;
+    p.r2c = r2c;
+    p.c2r = c2r;
+    p.u = u;
+    p.v = v;
+    qapb::cuda_check(qapb::launch_lap_batch(p, st), "lap batch");
+    qapb::cuda_check(cudaFreeAsync(counter, st), "cudaFreeAsync");
+  });
+}
+
+QAPB_API qapb_status qapb_lap_solve_batch(const double* costs, int m, int count, double* values,
+                                          int* r2c, int* c2r, double* u, double* v) {
+  return guard([&] {
+    need(m > 0, "lap: m must be positive");
+    need(count >= 0, "lap: count must be non-negative");
+    if (count == 0) return;
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t nc = (size_t)count * m * m, nv = (size_t)count * m;
+    double *dc = nullptr, *dval = nullptr, *du = nullptr, *dv = nullptr;
+    int *dr = nullptr, *dcr = nullptr;
+    auto al = [&](void** p, size_t bytes) {
+      qapb::cuda_check(cudaMallocAsync(p, bytes, st), "cudaMallocAsync");
+    };
+    al((void**)&dc, nc * 8);
+    if (values) al((void**)&dval, count * 8);
+    if (u) al((void**)&du, nv * 8);
+    if (v) al((void**)&dv, nv * 8);
+    if (r2c) al((void**)&dr, nv * 4);
+    if (c2r) al((void**)&dcr, nv * 4);
+    qapb::cuda_check(cudaMemcpyAsync(dc, costs, nc * 8, cudaMemcpyHostToDevice, st), "H2D");
+    const qapb_status rc = qapb_lap_solve_batch_device(dc, m, count, dval, dr, dcr, du, dv, st);
+    if (rc) throw std::invalid_argument(g_err);
+    if (values) cudaMemcpyAsync(values, dval, count * 8, cudaMemcpyDeviceToHost, st);
+    if (u) cudaMemcpyAsync(u, du, nv * 8, cudaMemcpyDeviceToHost, st);
+    if (v) cudaMemcpyAsync(v, dv, nv * 8, cudaMemcpyDeviceToHost, st);
+    if (r2c) cudaMemcpyAsync(r2c, dr, nv * 4, cudaMemcpyDeviceToHost, st);
+    if (c2r) cudaMemcpyAsync(c2r, dcr, nv * 4, cudaMemcpyDeviceToHost, st);
+    for (void* p : {(void*)dc, (void*)dval, (void*)du, (void*)dv, (void*)dr, (void*)dcr})
+      if (p) cudaFreeAsync(p, st);
+    qapb::cuda_check(cudaStreamSynchronize(st), "lap batch");
+  });
+}
+
+QAPB_API qapb_status qapb_lap_solve(const double* cost, int m, int* r2c, int* c2r, double* u,
+                                    double* v, double* value) {
+  return qapb_lap_solve_batch(cost, m, 1, value, r2c, c2r, u, v);
+}
+
+// ---- store helpers -------------------------------------------------------
+QAPB_API qapb_status qapb_init_coefficients(int n, const double* flow, const double* dist,
+                                            const double* linear, double* b, double* c,
+                                            double* d) {
+  return guard([&] {
+    need(n >= 3, "init_coefficients: n >= 3 required by RLT2");  // rlt2.cpp:67-68
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t nn = (size_t)n * n;
+    double *df, *dd, *dl = nullptr, *db, *dc;
+    qapb::cuda_check(cudaMallocAsync((void**)&df, nn * 8, st), "alloc");
+    qapb::cuda_check(cudaMallocAsync((void**)&dd, nn * 8, st), "alloc");
+    if (linear) qapb::cuda_check(cudaMallocAsync((void**)&dl, nn * 8, st), "alloc");
+    qapb::cuda_check(cudaMallocAsync((void**)&db, nb_of(n) * 8, st), "alloc");
+    qapb::cuda_check(cudaMallocAsync((void**)&dc, nc_of(n) * 8, st), "alloc");
+    cudaMemcpyAsync(df, flow, nn * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dd, dist, nn * 8, cudaMemcpyHostToDevice, st);
+    if (linear) cudaMemcpyAsync(dl, linear, nn * 8, cudaMemcpyHostToDevice, st);
+    qapb::cuda_check(qapb::launch_init_store(n, df, dd, dl, db, dc, st), "init_store");
+    cudaMemcpyAsync(b, db, nb_of(n) * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(c, dc, nc_of(n) * 8, cudaMemcpyDeviceToHost, st);
+    for (void* p : {(void*)df, (void*)dd, (void*)dl, (void*)db, (void*)dc})
+      if (p) cudaFreeAsync(p, st);
+    qapb::cuda_check(cudaStreamSynchronize(st), "init_coefficients");
+    if (d) std::memset(d, 0, nd_of(n) * sizeof(double));
+  });
+}
+
+// store_evaluate, rlt2.cpp:91-107 (host, O(n^3): an exactness oracle of the API)
+QAPB_API qapb_status qapb_store_evaluate(int m, const double* b, const double* c,
+                                         const double* d, double offset, const int* perm,
+                                         double* value) {
+  return guard([&] {
+    need(m >= 3, "store_evaluate: m >= 3 required");
+    HIdx ix(m);
+    double v = offset;
+    for (int i = 0; i < m; ++i) v += b[(size_t)i * m + perm[i]];
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j)
+        if (j != i) v += c[ix.cidx(i, perm[i], j, perm[j])];
+    for (int i = 0; i < m; ++i)
+      for (int j = i + 1; j < m; ++j) {
+        const double* tl = d + (size_t)ix.tile(i, j, perm[i], perm[j]) * ix.esz;
+        for (int k = 0; k < m; ++k)
+          if (k != i && k != j) v += tl[ix.cell(i, j, perm[i], perm[j], k, perm[k])];
+      }
+    *value = v;
+  });
+}
+
+// collapse_store, rlt2.cpp:109-182 (host; the device version is SURVEY §8f #1)
+QAPB_API qapb_status qapb_collapse_store(int m, const double* b, const double* c,
+                                         const double* d, double offset, int fac, int loc,
+                                         double* ob, double* oc, double* od, double* ooffset) {
+  return guard([&] {
+    const int mc = m - 1;
+    need(mc >= 2, "collapse_store: store too small");
+    HIdx ix(m), ox(mc);
+    *ooffset = offset + b[(size_t)fac * m + loc];
+    auto fm = [&](int i) { return i - (i > fac); };
+    auto lm = [&](int p) { return p - (p > loc); };
+    for (int i = 0; i < m; ++i) {
+      if (i == fac) continue;
+      for (int p = 0; p < m; ++p) {
+        if (p == loc) continue;
+        ob[(size_t)fm(i) * mc + lm(p)] =
+            b[(size_t)i * m + p] + c[ix.cidx(i, p, fac, loc)] + c[ix.cidx(fac, loc, i, p)];
+      }
+    }
+    std::memset(oc, 0, nc_of(mc) * sizeof(double));
+    for (int i = 0; i < m; ++i) {
+      if (i == fac) continue;
+      for (int p = 0; p < m; ++p) {
+        if (p == loc) continue;
+        for (int j = 0; j < m; ++j) {
+          if (j == i || j == fac) continue;
+          for (int q = 0; q < m; ++q) {
+            if (q == p || q == loc) continue;
+            oc[ox.cidx(fm(i), lm(p), fm(j), lm(q))] = c[ix.cidx(i, p, j, q)];
+          }
+        }
+      }
+    }
+    if (mc >= 3 && od) std::memset(od, 0, nd_of(mc) * sizeof(double));
+    if (m < 3) return;
+    const int tiles = ix.tiles();
+    for (int t = 0; t < tiles; ++t) {
+      const int fp = t / ix.lpairs, lp = t % ix.lpairs;
+      int i = 0, j = 0;
+      for (int a = 0, acc = 0; a < m; ++a) {
+        if (fp < acc + (m - 1 - a)) {
+          i = a;
+          j = a + 1 + (fp - acc);
+          break;
+        }
+        acc += m - 1 - a;
+      }
+      const int p = lp / (m - 1), qq = lp % (m - 1), q = qq + (qq >= p);
+      const double* tl = d + (size_t)t * ix.esz;
+      if (i == fac || j == fac) {
+        const bool first = (i == fac);
+        if ((first ? p : q) != loc) continue;
+        const int oi = first ? j : i, op = first ? q : p;
+        for (int cc = 0; cc < ix.esz; ++cc) {
+          if (tl[cc] == 0) continue;
+          int k, r;
+          ix.uncell(i, j, p, q, cc, &k, &r);
+          if (r == loc) continue;
+          oc[ox.cidx(fm(oi), lm(op), fm(k), lm(r))] += tl[cc];
+        }
+        continue;
+      }
+      if (p == loc || q == loc) continue;
+      for (int cc = 0; cc < ix.esz; ++cc) {
+        const double v = tl[cc];
+        int k, r;
+        ix.uncell(i, j, p, q, cc, &k, &r);
+        if (k == fac) {
+          if (r == loc) oc[ox.cidx(fm(i), lm(p), fm(j), lm(q))] += v;
+          continue;
+        }
+        if (r == loc) continue;
+        if (v == 0) continue;
+        if (od)
+          od[(size_t)ox.tile(fm(i), fm(j), lm(p), lm(q)) * ox.esz +
+             ox.cell(fm(i), fm(j), lm(p), lm(q), fm(k), lm(r))] += v;
+      }
+    }
+  });
+}
+
+// redistribute_family, rlt2.cpp:184-205
+QAPB_API qapb_status qapb_redistribute_family(const double pi[3], double add[3],
+                                              int virtual_slots, double tol, int* ok) {
+  return guard([&] {
+    int nb = virtual_slots;
+    double total = 0;
+    for (int s = 0; s < 3; ++s) {
+      if (pi[s] > tol)
+        total += pi[s];
+      else
+        ++nb;
+    }
+    if (total <= 0) {
+      add[0] = add[1] = add[2] = 0;
+      *ok = 1;
+      return;
+    }
+    if (nb == 0) {
+      add[0] = add[1] = add[2] = 0;
+      *ok = 0;
+      return;
+    }
+    const double share = total / nb;
+    for (int s = 0; s < 3; ++s) add[s] = (pi[s] > tol) ? -pi[s] : share;
+    *ok = 1;
+  });
+}
+
+// ---- engine ------------------------------------------------------------
+QAPB_API qapb_status qapb_engine_create(int m, const double* b, const double* c, const double* d,
+                                        double offset, const qapb_config* cfg,
+                                        qapb_engine** out) {
+  return guard([&] {
+    qapb_config c0;
+    qapb_config_init(&c0);
+    auto h = std::make_unique<qapb_engine>();
+    h->e = std::make_unique<Engine>(m, b, c, d, offset, cfg ? *cfg : c0);
+    *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_engine_create_instance(int n, const double* flow, const double* dist,
+                                                 const double* linear, const qapb_config* cfg,
+                                                 qapb_engine** out) {
+  return guard([&] {
+    qapb_config c0;
+    qapb_config_init(&c0);
+    auto h = std::make_unique<qapb_engine>();
+    h->e = std::make_unique<Engine>(n, flow, dist, linear, cfg ? *cfg : c0);
+    *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_engine_destroy(qapb_engine* e) {
+  return guard([&] { delete e; });
+}
+
+QAPB_API qapb_status qapb_engine_iterate(qapb_engine* e, double* bound) {
+  return guard([&] {
+    const double b = e->e->iterate();
+    if (bound) *bound = b;
+  });
+}
+
+QAPB_API qapb_status qapb_engine_run(qapb_engine* e, qapb_report* rep, qapb_record* records,
+                                     int max_records, int* certificate) {
+  return guard([&] {
+    std::vector<qapb_record> recs;
+    std::vector<int> cert;
+    qapb_report r{};
+    e->e->run(&r, records ? &recs : nullptr, &cert);
+    int k = 0;
+    if (records) {
+      k = std::min<int>(max_records, (int)recs.size());
+      std::copy(recs.begin(), recs.begin() + k, records);
+    }
+    r.n_records = k;
+    if (certificate && !cert.empty()) std::copy(cert.begin(), cert.end(), certificate);
+    if (rep) *rep = r;
+  });
+}
+
+QAPB_API qapb_status qapb_engine_best_bound(qapb_engine* e, double* v) {
+  *v = e->e->best_bound();
+  return QAPB_OK;
+}
+QAPB_API qapb_status qapb_engine_gap(qapb_engine* e, double* v) {
+  *v = e->e->gap();
+  return QAPB_OK;
+}
+QAPB_API qapb_status qapb_engine_iteration(qapb_engine* e, int* v) {
+  *v = e->e->iteration();
+  return QAPB_OK;
+}
+QAPB_API qapb_status qapb_engine_last_record(qapb_engine* e, qapb_record* r) {
+  *r = e->e->last_record();
+  return QAPB_OK;
+}
+QAPB_API qapb_status qapb_engine_certificate(qapb_engine* e, int* has, int* perm,
+                                             double* value) {
+  return guard([&] {
+    *has = e->e->has_certificate();
+    if (*has && perm) {
+      auto c = e->e->certificate();
+      std::copy(c.begin(), c.end(), perm);
+    }
+    if (value) *value = e->e->certificate_value();
+  });
+}
+QAPB_API qapb_status qapb_engine_x_assignment(qapb_engine* e, int* xrow) {
+  return guard([&] {
+    auto x = e->e->x_assignment();
+    std::copy(x.begin(), x.end(), xrow);
+  });
+}
+QAPB_API qapb_status qapb_engine_array_size(qapb_engine* e, int which, size_t* count) {
+  return guard([&] { *count = e->e->array_size(which); });
+}
+QAPB_API qapb_status qapb_engine_get_array(qapb_engine* e, int which, double* dst,
+                                           size_t count) {
+  return guard([&] { e->e->get_array(which, dst, count); });
+}
+QAPB_API qapb_status qapb_engine_store_offset(qapb_engine* e, double* offset) {
+  *offset = e->e->offset();
+  return QAPB_OK;
+}
+QAPB_API qapb_status qapb_engine_snapshot(qapb_engine* e, double* b, double* c, double* d,
+                                          double* offset) {
+  return guard([&] {
+    if (e->e->is_fast())  // rlt2.cpp:537-541
+      throw std::logic_error("warm-start snapshots are only offered from S variants");
+    e->e->get_array(QAPB_ARR_STORE_B, b, e->e->array_size(QAPB_ARR_STORE_B));
+    e->e->get_array(QAPB_ARR_STORE_C, c, e->e->array_size(QAPB_ARR_STORE_C));
+    e->e->get_array(QAPB_ARR_STORE_D, d, e->e->array_size(QAPB_ARR_STORE_D));
+    *offset = e->e->offset();
+  });
+}
+QAPB_API qapb_status qapb_engine_launch_count(qapb_engine* e, long long* n) {
+  *n = e->e->launches();
+  return QAPB_OK;
+}
+
+QAPB_API qapb_status qapb_run_ascent(int n, const double* flow, const double* dist,
+                                     const double* linear, const qapb_config* cfg,
+                                     qapb_report* rep, qapb_record* records, int max_records,
+                                     int* certificate) {
+  return guard([&] {
+    qapb_config c0;
+    qapb_config_init(&c0);
+    Engine eng(n, flow, dist, linear, cfg ? *cfg : c0);
+    std::vector<qapb_record> recs;
+    std::vector<int> cert;
+    qapb_report r{};
+    eng.run(&r, records ? &recs : nullptr, &cert);
+    int k = 0;
+    if (records) {
+      k = std::min<int>(max_records, (int)recs.size());
+      std::copy(recs.begin(), recs.begin() + k, records);
+    }
+    r.n_records = k;
+    if (!cert.empty()) {  // run_ascent re-evaluates on the instance, rlt2.cpp:594-595
+      double v = 0;
+      for (int i = 0; i < n; ++i) {
+        v += linear ? linear[(size_t)i * n + cert[i]] : 0.0;
+        for (int j = 0; j < n; ++j) v += flow[(size_t)i * n + j] * dist[(size_t)cert[i] * n + cert[j]];
+      }
+      r.certificate_value = v;
+      if (certificate) std::copy(cert.begin(), cert.end(), certificate);
+    }
+    if (rep) *rep = r;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// common.cuh — device helpers shared by the RLT2 kernels (sm_100a).
+//
+// Arithmetic contract: every floating-point operation on the path is a
+// separately rounded IEEE fp64 op in the reference's evaluation order
+// (SURVEY.md Appendix A).  The explicit __d*_rn intrinsics are never fused
+// into FMAs by nvcc; the library is additionally compiled with --fmad=false.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define QAPB_FULL 0xffffffffu
+
+namespace qapb {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// StoreIndex (rlt2.hpp:25-69) on the device.  m = problem size.
+struct DIdx {
+  int m, lpairs, esz;
+  __host__ __device__ DIdx() : m(0), lpairs(0), esz(0) {}
+  __host__ __device__ explicit DIdx(int m_)
+      : m(m_), lpairs(m_ * (m_ - 1)), esz((m_ - 2) * (m_ - 2)) {}
+  __device__ __forceinline__ int fpair(int i, int j) const {  // rlt2.hpp:37-39
+    return i * m - i * (i + 1) / 2 + (j - i - 1);
+  }
+  __device__ __forceinline__ int lpair(int p, int q) const {  // rlt2.hpp:40-42
+    return p * (m - 1) + q - (q > p);
+  }
+  __device__ __forceinline__ int tile(int i, int j, int p, int q) const {  // :43-45
+    return fpair(i, j) * lpairs + lpair(p, q);
+  }
+  __device__ __forceinline__ int cell(int i, int j, int p, int q, int k, int r) const {
+    const int kl = k - (k > i) - (k > j);  // rlt2.hpp:47-52
+    const int lo = p < q ? p : q, hi = p < q ? q : p;
+    const int rl = r - (r > lo) - (r > hi);
+    return kl * (m - 2) + rl;
+  }
+  __device__ __forceinline__ size_t cidx(int i, int p, int j, int q) const {  // :65-68
+    return ((size_t)i * m + p) * (m - 1) * (m - 1) + (size_t)(j - (j > i)) * (m - 1) +
+           (q - (q > p));
+  }
+  // lpair id -> (p, q), inverse of lpair()
+  __device__ __forceinline__ void unlpair(int lp, int* p, int* q) const {
+    const int pp = lp / (m - 1), qq = lp - pp * (m - 1);
+    *p = pp;
+    *q = qq + (qq >= pp);
+  }
+};
+
+// r-th free index of {0..n-1} \ {lo, hi} (lo < hi): uncell's column rule.
+__device__ __forceinline__ int skip2(int r, int lo, int hi) {
+  if (r >= lo) ++r;
+  if (r >= hi) ++r;
+  return r;
+}
+
+// ---- async copy / mbarrier primitives (TMA bulk path) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// One TMA bulk copy global -> shared, completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "QAPB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra QAPB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+}  // namespace qapb

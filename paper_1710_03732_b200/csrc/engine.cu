@@ -1,0 +1,529 @@
+// engine.cu — host side of the device-resident RLT2 dual-ascent engine.
+#include "engine.h"
+
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+
+namespace qapb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+template <class T>
+void dalloc(T** p, size_t n) {
+  cuda_check(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)),
+             "cudaMalloc");
+}
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+bool env_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v && std::strcmp(v, "0") != 0;
+}
+}  // namespace
+
+Engine::Engine(int m, const double* b, const double* c, const double* d, double offset,
+               const qapb_config& cfg)
+    : m_(m), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
+  if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");  // rlt2.cpp:209
+  if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
+  alloc();
+  init_state();
+  cuda_check(cudaMemcpyAsync(b_, b, nb_ * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D b");
+  cuda_check(cudaMemcpyAsync(c_, c, nc_ * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D c");
+  if (d)
+    cuda_check(cudaMemcpyAsync(d_, d, nd_ * sizeof(double), cudaMemcpyHostToDevice, st_),
+               "H2D d");
+  else
+    cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
+  hS_.offset = offset;
+  push_scalars();
+  cuda_check(cudaStreamSynchronize(st_), "engine create");
+}
+
+Engine::Engine(int n, const double* flow, const double* dist, const double* linear,
+               const qapb_config& cfg)
+    : m_(n), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
+  if (n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
+  if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
+  alloc();
+  init_state();
+  double *df = nullptr, *dd = nullptr, *dl = nullptr;
+  const size_t nn = (size_t)n * n;
+  dalloc(&df, nn);
+  dalloc(&dd, nn);
+  if (linear) dalloc(&dl, nn);
+  cuda_check(cudaMemcpyAsync(df, flow, nn * 8, cudaMemcpyHostToDevice, st_), "H2D flow");
+  cuda_check(cudaMemcpyAsync(dd, dist, nn * 8, cudaMemcpyHostToDevice, st_), "H2D dist");
+  if (linear)
+    cuda_check(cudaMemcpyAsync(dl, linear, nn * 8, cudaMemcpyHostToDevice, st_), "H2D lin");
+  cuda_check(launch_init_store(n, df, dd, dl, b_, c_, st_), "init_store");
+  ++launches_;
+  cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
+  hS_.offset = 0.0;
+  push_scalars();
+  cuda_check(cudaStreamSynchronize(st_), "engine create");
+  cudaFree(df);
+  cudaFree(dd);
+  if (dl) cudaFree(dl);
+}
+
+void Engine::alloc() {
+  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  const int m = m_;
+  fpairs_ = m * (m - 1) / 2;
+  lpairs_ = m * (m - 1);
+  tiles_ = fpairs_ * lpairs_;
+  esz_ = (m - 2) * (m - 2);
+  nb_ = (size_t)m * m;
+  nc_ = (size_t)m * m * (m - 1) * (m - 1);
+  nd_ = (size_t)tiles_ * esz_;
+  ntriples_ = m * (m - 1) * (m - 2) / 6;
+  chunk_ = fold_chunk(m);
+  nchunks_ = (m + chunk_ - 1) / chunk_;
+  dalloc(&b_, nb_);
+  dalloc(&c_, nc_);
+  dalloc(&d_, nd_);
+  dalloc(&piz_, nd_);
+  if (is_fast()) dalloc(&incz_, nd_);
+  dalloc(&piy_, nc_);
+  dalloc(&pix_, nb_);
+  dalloc(&theta_, tiles_);
+  if (is_two_phase()) dalloc(&theta1_, tiles_);
+  dalloc(&delta_, nb_);
+  dalloc(&ybar_, tiles_);
+  dalloc(&dx_, nb_);
+  dalloc(&push_, tiles_);
+  dalloc(&sa_fac_, m);
+  dalloc(&sa_loc_, m);
+  dalloc(&xrow_, m);
+  dalloc(&xcol_, m);
+  dalloc(&cert_, m);
+  dalloc(&triples_, 3 * (size_t)ntriples_);
+  dalloc(&fpair_ij_, fpairs_);
+  dalloc(&counter_, 4);
+  dalloc(&S_, 1);
+  cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hSpin_), sizeof(DevScalars)),
+             "cudaMallocHost");
+  std::vector<int> tr;
+  tr.reserve(3 * (size_t)ntriples_);
+  for (int a = 0; a < m; ++a)
+    for (int b = a + 1; b < m; ++b)
+      for (int c = b + 1; c < m; ++c) {
+        tr.push_back(a);
+        tr.push_back(b);
+        tr.push_back(c);
+      }
+  std::vector<int> fp(fpairs_);
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) fp[i * m - i * (i + 1) / 2 + (j - i - 1)] = i | (j << 16);
+  cuda_check(cudaMemcpy(triples_, tr.data(), tr.size() * sizeof(int), cudaMemcpyHostToDevice),
+             "H2D triples");
+  cuda_check(cudaMemcpy(fpair_ij_, fp.data(), fp.size() * sizeof(int), cudaMemcpyHostToDevice),
+             "H2D fpairs");
+  ensure_hist(std::max(cfg_.iter_limit, 64) + 1);
+}
+
+void Engine::init_state() {
+  auto z = [&](void* p, size_t bytes) {
+    if (p) cuda_check(cudaMemsetAsync(p, 0, bytes, st_), "memset");
+  };
+  z(piz_, nd_ * 8);
+  z(incz_, nd_ * 8);
+  z(piy_, nc_ * 8);
+  z(pix_, nb_ * 8);
+  z(theta_, tiles_ * 8);
+  z(theta1_, tiles_ * 8);
+  z(delta_, nb_ * 8);
+  z(ybar_, tiles_ * 8);
+  z(dx_, nb_ * 8);
+  z(push_, tiles_ * 8);
+  z(sa_fac_, m_ * 8);
+  z(sa_loc_, m_ * 8);
+  cuda_check(cudaMemsetAsync(xrow_, 0xff, m_ * sizeof(int), st_), "memset");
+  cuda_check(cudaMemsetAsync(xcol_, 0xff, m_ * sizeof(int), st_), "memset");
+  std::memset(&hS_, 0, sizeof hS_);
+  hS_.best = -kInf;
+  hS_.err_tile = INT_MAX;
+  hS_.term = QAPB_TERM_ITERATION_LIMIT;
+}
+
+Engine::~Engine() {
+  if (st_) cudaStreamSynchronize(st_);
+  if (graph_) cudaGraphExecDestroy(graph_);
+  dfree(b_); dfree(c_); dfree(d_); dfree(piz_); dfree(incz_); dfree(piy_); dfree(pix_);
+  dfree(theta_); dfree(theta1_); dfree(delta_); dfree(ybar_); dfree(dx_); dfree(push_);
+  dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
+  dfree(fpair_ij_); dfree(counter_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
+  if (hSpin_) cudaFreeHost(hSpin_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Engine::ensure_hist(int need) {
+  if (need <= hist_cap_) return;
+  int cap = std::max(need, 2 * hist_cap_);
+  double *nb = nullptr, *nbest = nullptr;
+  dalloc(&nb, cap);
+  dalloc(&nbest, cap);
+  if (hist_cap_) {
+    cuda_check(cudaMemcpyAsync(nb, hist_bound_, hist_cap_ * 8, cudaMemcpyDeviceToDevice, st_),
+               "hist");
+    cuda_check(cudaMemcpyAsync(nbest, hist_best_, hist_cap_ * 8, cudaMemcpyDeviceToDevice, st_),
+               "hist");
+    cuda_check(cudaStreamSynchronize(st_), "hist");
+  }
+  dfree(hist_bound_);
+  dfree(hist_best_);
+  hist_bound_ = nb;
+  hist_best_ = nbest;
+  hist_cap_ = cap;
+  if (graph_) {  // the captured X stage writes the history arrays
+    cudaGraphExecDestroy(graph_);
+    graph_ = nullptr;
+  }
+}
+
+void Engine::push_scalars() {
+  *hSpin_ = hS_;
+  cuda_check(cudaMemcpyAsync(S_, hSpin_, sizeof(DevScalars), cudaMemcpyHostToDevice, st_),
+             "H2D scalars");
+}
+
+void Engine::pull_scalars() {
+  cuda_check(cudaMemcpyAsync(hSpin_, S_, sizeof(DevScalars), cudaMemcpyDeviceToHost, st_),
+             "D2H scalars");
+  cuda_check(cudaStreamSynchronize(st_), "iteration");
+  hS_ = *hSpin_;
+}
+
+void Engine::enqueue_stage_z(int it) {  // rlt2.cpp:301-338
+  double* costs = (is_fast() && it > 0) ? incz_ : d_;
+  BatchLapParams p{};
+  p.costs = costs;
+  p.m = m_ - 2;
+  p.count = tiles_;
+  p.counter = counter_;
+  p.stop = &S_->stop;
+  p.stop_w = &S_->stop;
+  p.values = is_two_phase() ? theta1_ : theta_;
+  p.pi = piz_;
+  cuda_check(cudaMemsetAsync(counter_, 0, sizeof(int), st_), "memset counter");
+  cuda_check(launch_lap_batch(p, st_), "z-stage");
+  ++launches_;
+  if (is_two_phase()) {  // rlt2.cpp:328-336
+    FoldParams f{};
+    f.m = m_;
+    f.triples = triples_;
+    f.ntriples = ntriples_;
+    f.chunk = chunk_;
+    f.nchunks = nchunks_;
+    f.piz = piz_;
+    f.costs = costs;
+    f.stop = &S_->stop;
+    cuda_check(launch_phase2(f, st_), "phase-2");
+    ++launches_;
+    p.values = theta_;
+    p.theta_ref = theta1_;
+    p.err_tile = &S_->err_tile;
+    cuda_check(cudaMemsetAsync(counter_, 0, sizeof(int), st_), "memset counter");
+    cuda_check(launch_lap_batch(p, st_), "z-stage phase 2");
+    ++launches_;
+  }
+}
+
+void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
+  const bool inc = is_fast() && it > 0;
+  const bool steady = it > 0;
+  if (steady && graph_) {
+    cuda_check(cudaGraphLaunch(graph_, st_), "graph launch");
+    launches_ += graph_launches_;
+    return;
+  }
+  const bool capture = steady && it >= 2 && !graph_ && !env_flag("QAPB_NO_GRAPH");
+  cudaGraph_t g = nullptr;
+  const long long l0 = launches_;
+  if (capture)
+    cuda_check(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "capture");
+  if (steady) {  // ascent_update, rlt2.cpp:237-299
+    XYFoldParams x{};
+    x.m = m_;
+    x.kx = cfg_.kappa_x;
+    x.ky = cfg_.kappa_y;
+    x.vph = cfg_.varphi;
+    x.pix = pix_;
+    x.sa_fac = sa_fac_;
+    x.sa_loc = sa_loc_;
+    x.dx = dx_;
+    x.b = b_;
+    x.c = c_;
+    x.piy = piy_;
+    x.ybar = ybar_;
+    x.push = push_;
+    x.fpair_ij = fpair_ij_;
+    x.stop = &S_->stop;
+    cuda_check(launch_xyfold(x, tiles_, st_), "xy-fold");
+    ++launches_;
+    FoldParams f{};
+    f.m = m_;
+    f.triples = triples_;
+    f.ntriples = ntriples_;
+    f.chunk = chunk_;
+    f.nchunks = nchunks_;
+    f.kz = cfg_.kappa_z_upper;
+    f.phi = cfg_.phi_split;
+    f.fast = is_fast();
+    f.d = d_;
+    f.piz = piz_;
+    f.incz = incz_;
+    f.push = push_;
+    f.sa_fac = sa_fac_;
+    f.sa_loc = sa_loc_;
+    f.stop = &S_->stop;
+    cuda_check(launch_zfold(f, st_), "z-fold");
+    ++launches_;
+  }
+  enqueue_stage_z(it);
+  YStageParams y{};
+  y.m = m_;
+  y.c = c_;
+  y.theta = theta_;
+  y.ybar = ybar_;
+  y.dx = dx_;
+  y.inc = inc;
+  y.delta = delta_;
+  y.piy = piy_;
+  y.stop = &S_->stop;
+  cuda_check(launch_ystage(y, st_), "y-stage");
+  ++launches_;
+  XStageParams xs{};
+  xs.m = m_;
+  xs.delta = delta_;
+  xs.b = b_;
+  xs.inc = inc;
+  xs.fast = is_fast();
+  xs.pix = pix_;
+  xs.xrow = xrow_;
+  xs.xcol = xcol_;
+  xs.piy = piy_;
+  xs.piz = piz_;
+  xs.S = S_;
+  xs.hist_bound = hist_bound_;
+  xs.hist_best = hist_best_;
+  xs.cert = cert_;
+  xs.upper_bound = cfg_.upper_bound;
+  xs.min_gap = cfg_.min_gap;
+  xs.fathom = cfg_.fathom_threshold;
+  xs.es_delta = cfg_.early_stop_delta;
+  xs.es_window = cfg_.early_stop_window;
+  xs.iter_limit = cfg_.iter_limit;
+  cuda_check(launch_xstage(xs, st_), "x-stage");
+  ++launches_;
+  if (capture) {
+    cuda_check(cudaStreamEndCapture(st_, &g), "end capture");
+    cuda_check(cudaGraphInstantiate(&graph_, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    graph_launches_ = (int)(launches_ - l0);
+    launches_ = l0;
+    cuda_check(cudaGraphLaunch(graph_, st_), "graph launch");
+    launches_ += graph_launches_;
+  }
+}
+
+void Engine::check_phase2() {
+  if (hS_.err_tile != INT_MAX) {
+    const int t = hS_.err_tile;
+    hS_.err_tile = INT_MAX;
+    hS_.stop = 0;
+    push_scalars();
+    throw std::logic_error("phase-2 theta regressed on tile " + std::to_string(t));
+  }
+}
+
+double Engine::gap() const {  // rlt2.cpp:532-535
+  if (!std::isfinite(cfg_.upper_bound) || cfg_.upper_bound == 0) return kInf;
+  return (cfg_.upper_bound - hS_.best) / cfg_.upper_bound;
+}
+
+// Type-4 SA (rlt2.cpp:477-513).  Draws with std::mt19937_64 /
+// uniform_real_distribution / std::exp exactly as the reference; the b drain
+// and running update run on the device.
+void Engine::sa_perturb() {
+  const double nu = hS_.best;
+  if (nu <= 0) return;
+  if (temp_ <= 0) {
+    const double ub = std::isfinite(cfg_.upper_bound) ? cfg_.upper_bound : 1.05 * nu + 1.0;
+    temp_ = cfg_.sa_t0_fraction * ub;
+  }
+  const double cap = cfg_.sa_kappa_lb_cap * nu;
+  const int m = m_;
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  std::vector<double> amt(2 * m, 0.0);
+  double total = 0;
+  for (int s = 0; s < 2 * m; ++s) {
+    const double kap = U(rng_) * cap;
+    const bool accept = U(rng_) < std::exp(-kap / temp_);
+    if (accept) {
+      amt[s] = kap;
+      total += kap;
+    }
+  }
+  if (total > cap)
+    for (double& a : amt) a *= cap / total;
+  std::vector<double> fac(m), loc(m);
+  for (int i = 0; i < m; ++i) fac[i] = amt[i] / m;
+  for (int p = 0; p < m; ++p) loc[p] = amt[m + p] / m;
+  double drained = 0;
+  for (int i = 0; i < m; ++i) drained += fac[i] + loc[i];
+  cuda_check(cudaMemcpyAsync(sa_fac_, fac.data(), m * 8, cudaMemcpyHostToDevice, st_), "H2D sa");
+  cuda_check(cudaMemcpyAsync(sa_loc_, loc.data(), m * 8, cudaMemcpyHostToDevice, st_), "H2D sa");
+  cuda_check(launch_sa_apply(m, b_, sa_fac_, sa_loc_, S_, drained, is_fast(), st_), "sa");
+  ++launches_;
+  const int iter_before = hS_.iter - 1;  // sa_perturb runs before ++iter_
+  if ((iter_before + 1) % cfg_.sa_cool_period == 0) temp_ *= cfg_.sa_cool_factor;
+  pull_scalars();
+}
+
+double Engine::iterate() {
+  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  hS_.run_mode = 0;
+  hS_.stop = 0;
+  push_scalars();
+  ensure_hist(hS_.iter + 1);
+  enqueue_iteration(hS_.iter);
+  pull_scalars();
+  check_phase2();
+  if (cfg_.sa_enabled && !hS_.has_cert) sa_perturb();
+  last_rec_ = qapb_record{hS_.iter, hS_.last_bound, gap(), 0, 0, 0};
+  return hS_.last_bound;
+}
+
+void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) const {
+  if (!recs || to <= from) return;
+  std::vector<double> bnd(to - from), bst(to - from);
+  cuda_check(cudaMemcpy(bnd.data(), hist_bound_ + from, (to - from) * 8, cudaMemcpyDeviceToHost),
+             "D2H hist");
+  cuda_check(cudaMemcpy(bst.data(), hist_best_ + from, (to - from) * 8, cudaMemcpyDeviceToHost),
+             "D2H hist");
+  for (int k = from; k < to; ++k) {
+    qapb_record r{};
+    r.iteration = k + 1;
+    r.bound = bnd[k - from];
+    const double best = bst[k - from];
+    r.gap = (!std::isfinite(cfg_.upper_bound) || cfg_.upper_bound == 0)
+                ? kInf
+                : (cfg_.upper_bound - best) / cfg_.upper_bound;
+    recs->push_back(r);
+  }
+}
+
+void Engine::run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<int>* cert) {
+  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  const auto t0 = std::chrono::steady_clock::now();
+  const int from = hS_.iter;
+  hS_.run_mode = 1;
+  hS_.run_start = hS_.iter;
+  hS_.stop = 0;
+  hS_.term = QAPB_TERM_ITERATION_LIMIT;
+  push_scalars();
+  if (hS_.iter < cfg_.iter_limit) {
+    int batch = 4;
+    while (true) {
+      const int remaining = cfg_.iter_limit - hS_.iter;
+      const int B = cfg_.sa_enabled ? 1 : std::max(1, std::min(remaining, batch));
+      ensure_hist(hS_.iter + B);
+      for (int k = 0; k < B; ++k) enqueue_iteration(hS_.iter + k);
+      pull_scalars();
+      check_phase2();
+      if (cfg_.sa_enabled && !hS_.has_cert) sa_perturb();
+      if (hS_.stop || hS_.iter >= cfg_.iter_limit) break;
+      batch = std::min(batch * 2, 64);
+    }
+  }
+  const int to = hS_.iter;
+  if (recs && cfg_.record_history) fill_records(from, to, recs);
+  hS_.run_mode = 0;
+  hS_.stop = 0;
+  push_scalars();
+  if (rep) {
+    rep->best_bound = hS_.best;
+    rep->upper_bound = cfg_.upper_bound;
+    rep->gap = gap();
+    rep->termination = hS_.term;
+    rep->iterations = hS_.iter;
+    rep->has_certificate = hS_.has_cert;
+    rep->certificate_value = hS_.has_cert ? hS_.cert_val : 0.0;
+    rep->n_records = recs ? (int)recs->size() : 0;
+    rep->wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  if (cert && hS_.has_cert) *cert = certificate();
+  if (to > from) {
+    const int k = to - 1;
+    double bnd = 0;
+    cuda_check(cudaMemcpy(&bnd, hist_bound_ + k, 8, cudaMemcpyDeviceToHost), "D2H");
+    last_rec_ = qapb_record{to, bnd, gap(), 0, 0, 0};
+  }
+}
+
+std::vector<int> Engine::certificate() const {
+  std::vector<int> out;
+  if (!hS_.has_cert) return out;
+  out.resize(m_);
+  cuda_check(cudaMemcpy(out.data(), cert_, m_ * sizeof(int), cudaMemcpyDeviceToHost), "D2H cert");
+  return out;
+}
+
+std::vector<int> Engine::x_assignment() const {
+  std::vector<int> out(m_);
+  cuda_check(cudaMemcpy(out.data(), xrow_, m_ * sizeof(int), cudaMemcpyDeviceToHost), "D2H xrow");
+  return out;
+}
+
+size_t Engine::array_size(int which) const {
+  switch (which) {
+    case QAPB_ARR_PI_Z: return nd_;
+    case QAPB_ARR_PI_Y: return nc_;
+    case QAPB_ARR_PI_X: return nb_;
+    case QAPB_ARR_STORE_B: return nb_;
+    case QAPB_ARR_STORE_C: return nc_;
+    case QAPB_ARR_STORE_D: return nd_;
+    case QAPB_ARR_THETA: return tiles_;
+    case QAPB_ARR_DELTA: return nb_;
+    case QAPB_ARR_INCZ: return incz_ ? nd_ : 0;
+  }
+  throw std::invalid_argument("unknown engine array");
+}
+
+void Engine::get_array(int which, double* dst, size_t count) const {
+  const size_t n = array_size(which);
+  if (count != n) throw std::invalid_argument("array size mismatch");
+  const double* src = nullptr;
+  switch (which) {
+    case QAPB_ARR_PI_Z: src = piz_; break;
+    case QAPB_ARR_PI_Y: src = piy_; break;
+    case QAPB_ARR_PI_X: src = pix_; break;
+    case QAPB_ARR_STORE_B: src = b_; break;
+    case QAPB_ARR_STORE_C: src = c_; break;
+    case QAPB_ARR_STORE_D: src = d_; break;
+    case QAPB_ARR_THETA: src = theta_; break;
+    case QAPB_ARR_DELTA: src = delta_; break;
+    case QAPB_ARR_INCZ: src = incz_; break;
+  }
+  if (n) cuda_check(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H array");
+}
+
+}  // namespace qapb

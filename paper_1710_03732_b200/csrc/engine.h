@@ -1,0 +1,103 @@
+// engine.h — device-resident RLT2 dual-ascent engine (host side, C++).
+//
+// Mirrors qap::AscentEngine (rlt2.hpp:151-213): same state, same stage order
+// (iterate, rlt2.cpp:515-530), same run() termination (rlt2.cpp:544-588), but
+// all O(n^4)..O(n^6) state lives in HBM and a run() enqueues batches of
+// iterations with no host round trip (device-side stop flag); the host only
+// touches the device between batches, or once per iteration when SA is on
+// (the Type-4 draws use the reference's own RNG, rlt2.cpp:477-513).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/qapb200.h"
+#include "kernels.h"
+
+namespace qapb {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+class Engine {
+ public:
+  // AscentEngine(CoefficientStore, cfg) (rlt2.cpp:207-230); d == nullptr
+  // means D' = 0.
+  Engine(int m, const double* b, const double* c, const double* d, double offset,
+         const qapb_config& cfg);
+  // AscentEngine(init_coefficients(inst), cfg): store built on the device.
+  Engine(int n, const double* flow, const double* dist, const double* linear,
+         const qapb_config& cfg);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  double iterate();                                  // rlt2.cpp:515-530
+  void run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<int>* cert);
+
+  int m() const { return m_; }
+  int iteration() const { return hS_.iter; }
+  double best_bound() const { return hS_.best; }
+  double gap() const;                                // rlt2.cpp:532-535
+  bool has_certificate() const { return hS_.has_cert != 0; }
+  double certificate_value() const { return hS_.cert_val; }
+  double offset() const { return hS_.offset; }
+  bool is_fast() const { return cfg_.variant == QAPB_F1 || cfg_.variant == QAPB_F2; }
+  bool is_two_phase() const { return cfg_.variant == QAPB_F2 || cfg_.variant == QAPB_S2; }
+  std::vector<int> certificate() const;
+  std::vector<int> x_assignment() const;
+  size_t array_size(int which) const;
+  void get_array(int which, double* dst, size_t count) const;
+  qapb_record last_record() const { return last_rec_; }
+  long long launches() const { return launches_; }
+
+  // device pointers for in-process consumers (bench / multi-GPU layer)
+  double* dev_d() const { return d_; }
+  double* dev_piz() const { return piz_; }
+  cudaStream_t stream() const { return st_; }
+
+ private:
+  void alloc();
+  void init_state();
+  void enqueue_iteration(int iter_index);
+  void enqueue_stage_z(int iter_index);
+  void ensure_hist(int need);
+  void pull_scalars();
+  void push_scalars();
+  void sa_perturb();                                 // rlt2.cpp:477-513 (host draws)
+  void check_phase2();
+  void fill_records(int from, int to, std::vector<qapb_record>* recs) const;
+  void build_graph();
+
+  int m_, dev_;
+  qapb_config cfg_;
+  int tiles_, esz_, fpairs_, lpairs_, ntriples_, chunk_, nchunks_;
+  size_t nb_, nc_, nd_;
+  cudaStream_t st_ = nullptr;
+  double *b_ = nullptr, *c_ = nullptr, *d_ = nullptr, *piz_ = nullptr, *incz_ = nullptr;
+  double *piy_ = nullptr, *pix_ = nullptr, *theta_ = nullptr, *theta1_ = nullptr;
+  double *delta_ = nullptr, *ybar_ = nullptr, *dx_ = nullptr, *push_ = nullptr;
+  double *sa_fac_ = nullptr, *sa_loc_ = nullptr;
+  int *xrow_ = nullptr, *xcol_ = nullptr, *cert_ = nullptr, *triples_ = nullptr;
+  int *fpair_ij_ = nullptr, *counter_ = nullptr;
+  DevScalars* S_ = nullptr;
+  double *hist_bound_ = nullptr, *hist_best_ = nullptr;
+  int hist_cap_ = 0;
+  DevScalars* hSpin_ = nullptr;  // pinned mirror for async copies
+  DevScalars hS_{};
+  std::mt19937_64 rng_;
+  double temp_ = 0;
+  qapb_record last_rec_{};
+  long long launches_ = 0;
+  cudaGraphExec_t graph_ = nullptr;
+  int graph_launches_ = 0;
+};
+
+}  // namespace qapb

@@ -1,0 +1,636 @@
+// kernels.cu — the RLT2 dual-ascent hot path on sm_100a.
+//
+//   xyfold_kernel   x- and y-level ascent update           rlt2.cpp:244-262
+//   zfold_kernel    z-level family fold (O(n^6), HBM)      rlt2.cpp:264-298
+//   phase2_kernel   2-phase family redistribution          rlt2.cpp:340-381
+//   lap_batch_kernel  Z-LAP batch / public batch API      rlt2.cpp:301-326, lap.cpp:104-138
+//   ystage_kernel   Y-cost build + Y-LAPs                  rlt2.cpp:383-426
+//   xstage_kernel   X-LAP, bound, feasibility, termination rlt2.cpp:428-473, 544-578
+//
+// Layouts are the reference's (StoreIndex); every Z tile and Y block is
+// contiguous.  See DESIGN.md for the roofline of each kernel.
+#include <climits>
+#include <cstdio>
+
+#include "../../include/qapb200.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "lap_warp.cuh"
+
+namespace qapb {
+
+namespace {
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// init_coefficients (rlt2.cpp:66-89): b' = b + f_ii d_pp, C' = f_ij d_pq.
+// D' is zeroed by the caller (cudaMemsetAsync).
+__global__ void init_store_kernel(int n, const double* __restrict__ flow,
+                                  const double* __restrict__ dist,
+                                  const double* __restrict__ linear, double* __restrict__ b,
+                                  double* __restrict__ c) {
+  const int m = n, m1 = m - 1;
+  const size_t nc = (size_t)m * m * m1 * m1;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < nc;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int ip = (int)(e / ((size_t)m1 * m1));
+    const int rem = (int)(e - (size_t)ip * m1 * m1);
+    const int a = rem / m1, bq = rem - a * m1;
+    const int i = ip / m, p = ip - i * m;
+    const int j = a + (a >= i), q = bq + (bq >= p);
+    c[e] = dmul(flow[i * n + j], dist[p * n + q]);  // rlt2.cpp:84
+    if (e < (size_t)m * m) {
+      const int ii = (int)e / m, pp = (int)e - ii * m;
+      b[e] = dadd(linear ? linear[e] : 0.0, dmul(flow[ii * n + ii], dist[pp * n + pp]));  // :76
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// x- and y-level fold (rlt2.cpp:244-262).  One thread per tile.  dx is
+// recomputed from pi(x) wherever it is needed (same expression, same bits),
+// so the x level needs no separate launch; tiles < m*m also store dx and b.
+__global__ void __launch_bounds__(256) xyfold_kernel(XYFoldParams P, int tiles) {
+  if (P.stop && *P.stop) return;
+  const DIdx ix(P.m);
+  const int m = P.m;
+  const double dm1 = (double)(m - 1), dm2 = (double)(m - 2);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += gridDim.x * blockDim.x) {
+    if (t < m * m) {
+      const int i = t / m, p = t - i * m;
+      P.dx[t] = dadd(dadd(dmul(P.kx, P.pix[t]), P.sa_fac[i]), P.sa_loc[p]);  // :247
+      P.b[t] = dsub(P.b[t], dmul(P.kx, P.pix[t]));                            // :248
+    }
+    const int fp = t / ix.lpairs, lp = t - fp * ix.lpairs;
+    const int ij = P.fpair_ij[fp];
+    const int i = ij & 0xffff, j = ij >> 16;
+    int p, q;
+    ix.unlpair(lp, &p, &q);
+    const size_t up_ix = ix.cidx(i, p, j, q), lo_ix = ix.cidx(j, q, i, p);
+    const double up = P.piy[up_ix], lo = P.piy[lo_ix];
+    const double dxjq =
+        dadd(dadd(dmul(P.kx, P.pix[j * m + q]), P.sa_fac[j]), P.sa_loc[q]);
+    const double dxip =
+        dadd(dadd(dmul(P.kx, P.pix[i * m + p]), P.sa_fac[i]), P.sa_loc[p]);
+    const double yb = dmul(0.5, dadd(up, lo));  // :258
+    P.ybar[t] = yb;
+    P.c[up_ix] = dadd(P.c[up_ix], dsub(dmul(P.vph, dsub(lo, up)), dmul(P.ky, yb)));  // :259
+    P.c[lo_ix] =
+        dadd(P.c[lo_ix], dadd(dmul(P.vph, dsub(up, lo)), ddiv(dxjq, dm1)));  // :260
+    P.push[t] = ddiv(dadd(dmul(P.ky, yb), ddiv(dxip, dm1)), dm2);           // :261
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Family-blocked z-level kernels.
+//
+// A symmetric family of the half-Z store is one facility triple a<b<c with
+// distinct locations (pa,pb,pc); its three stored members are
+//   X1 = T(a,b,pa,pb)[c,pc]   row c-2 of the (a,b) tiles, contiguous in pc
+//   X2 = T(a,c,pa,pc)[b,pb]   row b-1 of the (a,c) tiles, contiguous in pb
+//   X3 = T(b,c,pb,pc)[a,pa]   row a   of the (b,c) tiles, contiguous in pa
+// (partner formulas rlt2.cpp:280-288 / :355-356).  A CTA owns one triple and a
+// chunk of `chunk` values of pa: it stages pi(z) of all three members in
+// shared memory (coalesced row segments), then streams D' / incz / phase-2
+// costs of each member in its own row order.
+struct FamilyCtx {
+  int n, nm1, nm2, a, b, c, pa0, Pe, fab, fac, fbc;
+  size_t esz;
+  int lpairs;
+};
+
+__device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
+  FamilyCtx f;
+  f.n = P.m;
+  f.nm1 = f.n - 1;
+  f.nm2 = f.n - 2;
+  const int T = blockIdx.x / P.nchunks, ch = blockIdx.x - T * P.nchunks;
+  f.a = P.triples[3 * T];
+  f.b = P.triples[3 * T + 1];
+  f.c = P.triples[3 * T + 2];
+  f.pa0 = ch * P.chunk;
+  f.Pe = min(P.chunk, f.n - f.pa0);
+  const DIdx ix(f.n);
+  f.fab = ix.fpair(f.a, f.b);
+  f.fac = ix.fpair(f.a, f.c);
+  f.fbc = ix.fpair(f.b, f.c);
+  f.esz = (size_t)ix.esz;
+  f.lpairs = ix.lpairs;
+  return f;
+}
+
+// Visit every member cell of the CTA's families: fn(member, pa_l, pb, pc, g)
+// with g the cell's offset in the reference layout.  Consecutive threads get
+// consecutive columns of one tile row (coalesced for X1 and X2; X3 rows are
+// read `chunk` doubles at a time, the rest of the row by the sibling CTAs).
+template <class Fn>
+__device__ __forceinline__ void for_family_cells(const FamilyCtx& f, Fn&& fn) {
+  const DIdx ix(f.n);
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int seg1 = f.Pe * f.nm1, cnt12 = seg1 * f.nm2;
+  // X1: tiles (a,b,pa,pb), row c-2, column -> pc
+  for (int e = tid; e < cnt12; e += bd) {
+    const int sg = e / f.nm2, r = e - sg * f.nm2;
+    const int pa_l = sg / f.nm1, pbi = sg - pa_l * f.nm1;
+    const int pa = f.pa0 + pa_l, pb = pbi + (pbi >= pa);
+    const int pc = skip2(r, min(pa, pb), max(pa, pb));
+    const size_t g = (size_t)(f.fab * f.lpairs + ix.lpair(pa, pb)) * f.esz +
+                     (size_t)(f.c - 2) * f.nm2 + r;
+    fn(0, pa_l, pb, pc, g);
+  }
+  // X2: tiles (a,c,pa,pc), row b-1, column -> pb
+  for (int e = tid; e < cnt12; e += bd) {
+    const int sg = e / f.nm2, r = e - sg * f.nm2;
+    const int pa_l = sg / f.nm1, pci = sg - pa_l * f.nm1;
+    const int pa = f.pa0 + pa_l, pc = pci + (pci >= pa);
+    const int pb = skip2(r, min(pa, pc), max(pa, pc));
+    const size_t g = (size_t)(f.fac * f.lpairs + ix.lpair(pa, pc)) * f.esz +
+                     (size_t)(f.b - 1) * f.nm2 + r;
+    fn(1, pa_l, pb, pc, g);
+  }
+  // X3: tiles (b,c,pb,pc), row a, column <- pa
+  const int cnt3 = f.n * f.nm1 * f.Pe;
+  for (int e = tid; e < cnt3; e += bd) {
+    const int pair = e / f.Pe, pa_l = e - pair * f.Pe;
+    const int pb = pair / f.nm1, pci = pair - pb * f.nm1;
+    const int pc = pci + (pci >= pb);
+    const int pa = f.pa0 + pa_l;
+    if (pa == pb || pa == pc) continue;
+    const int lo = min(pb, pc), hi = max(pb, pc);
+    const int col = pa - (pa > lo) - (pa > hi);
+    const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
+                     (size_t)f.a * f.nm2 + col;
+    fn(2, pa_l, pb, pc, g);
+  }
+}
+
+__device__ __forceinline__ void stage_family_pi(const FamilyCtx& f, const double* __restrict__ piz,
+                                                double* S, int chunk) {
+  const int nn = f.n * f.n;
+  for_family_cells(f, [&](int mem, int pa_l, int pb, int pc, size_t g) {
+    S[(size_t)mem * chunk * nn + (pa_l * f.n + pb) * f.n + pc] = piz[g];
+  });
+}
+
+// z-level fold, rlt2.cpp:269-298 (Type-1 rule with the half-Z phi split).
+__global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ double sm[];
+  const FamilyCtx f = family_ctx(P);
+  const int n = f.n, nn = n * n, C = P.chunk;
+  double* S = sm;                      // [3][C][n][n] pi(z) of X1, X2, X3
+  double* U1 = S + (size_t)3 * C * nn;  // [C][n]  push of tile (a,b,pa,pb)
+  double* U2 = U1 + C * n;             // [C][n]  push of tile (a,c,pa,pc)
+  double* U3 = U2 + C * n;             // [n][n]  push of tile (b,c,pb,pc)
+  const DIdx ix(n);
+  const int tid = threadIdx.x, bd = blockDim.x;
+  for (int e = tid; e < f.Pe * n; e += bd) {
+    const int pa_l = e / n, q = e - pa_l * n, pa = f.pa0 + pa_l;
+    if (q == pa) continue;
+    U1[e] = P.push[f.fab * f.lpairs + ix.lpair(pa, q)];
+    U2[e] = P.push[f.fac * f.lpairs + ix.lpair(pa, q)];
+  }
+  for (int e = tid; e < nn; e += bd) {
+    const int pb = e / n, pc = e - pb * n;
+    if (pb != pc) U3[e] = P.push[f.fbc * f.lpairs + ix.lpair(pb, pc)];
+  }
+  stage_family_pi(f, P.piz, S, C);
+  __syncthreads();
+  const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
+  double* __restrict__ d = P.d;
+  double* __restrict__ incz = P.incz;
+  const int fast = P.fast;
+  for_family_cells(f, [&](int mem, int pa_l, int pb, int pc, size_t g) {
+    const int fi = (pa_l * n + pb) * n + pc;
+    const double p1 = S[fi], p2 = S[(size_t)C * nn + fi], p3 = S[(size_t)2 * C * nn + fi];
+    const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
+    const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
+    const double s3 = dadd(dmul(kz, p3), U3[pb * n + pc]);
+    double own, gain;  // partners in ascending member order (B, C of rlt2.cpp:280-288)
+    if (mem == 0) {
+      own = p1;
+      gain = dadd(dmul(phi, s2), dmul(phi, s3));
+    } else if (mem == 1) {
+      own = p2;
+      gain = dadd(dmul(phi, s1), dmul(phi, s3));
+    } else {
+      own = p3;
+      gain = dadd(dmul(phi, s1), dmul(phi, s2));
+    }
+    d[g] = dadd(d[g], dsub(gain, dmul(kz, own)));   // rlt2.cpp:292
+    if (fast) incz[g] = dadd(dmul(omk, own), gain);  // rlt2.cpp:293
+  });
+  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
+    P.sa_fac[tid] = 0.0;
+    P.sa_loc[tid] = 0.0;
+  }
+}
+
+// Phase 2, rlt2.cpp:344-381 with redistribute_family (rlt2.cpp:184-205):
+// every member's cost gets add[s] + share from its family's pi triple.
+__global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ double sm[];
+  const FamilyCtx f = family_ctx(P);
+  const int n = f.n, nn = n * n, C = P.chunk;
+  double* S = sm;
+  stage_family_pi(f, P.piz, S, C);
+  __syncthreads();
+  double* __restrict__ costs = P.costs;
+  const double tol = 1e-9;
+  for_family_cells(f, [&](int mem, int pa_l, int pb, int pc, size_t g) {
+    const int fi = (pa_l * n + pb) * n + pc;
+    const double p1 = S[fi], p2 = S[(size_t)C * nn + fi], p3 = S[(size_t)2 * C * nn + fi];
+    double total = 0.0;
+    int nb = 3;
+    if (p1 > tol) total = dadd(total, p1); else ++nb;
+    if (p2 > tol) total = dadd(total, p2); else ++nb;
+    if (p3 > tol) total = dadd(total, p3); else ++nb;
+    const double share = ddiv(total, (double)nb);
+    const double own = mem == 0 ? p1 : (mem == 1 ? p2 : p3);
+    const double add = (total <= 0.0) ? 0.0 : ((own > tol) ? -own : share);
+    costs[g] = dadd(costs[g], dadd(add, share));  // rlt2.cpp:376-378
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Batched LAPs, one warp per LAP (Z stage and the public batch API).
+// Persistent CTAs; each warp pulls tiles from a global counter and
+// double-buffers them in shared memory with TMA bulk copies
+// (cp.async.bulk + mbarrier), prefetching tile k+1 while solving tile k.
+template <int CPL>
+__global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
+                                                        int buf_elems, int use_bulk) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* ws = smem_raw + (size_t)warp * warp_smem;
+  double* buf0 = reinterpret_cast<double*>(ws);
+  double* buf1 = buf0 + buf_elems;
+  double* urow = buf0 + (use_bulk ? 2 : 1) * buf_elems;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(urow + ((P.m + 1) & ~1));
+  const int m = P.m;
+  const size_t esz = (size_t)m * m;
+  const unsigned bytes = (unsigned)(esz * sizeof(double));
+  if (use_bulk && lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  int t = 0;
+  if (lane == 0) t = atomicAdd(P.counter, 1);
+  t = __shfl_sync(QAPB_FULL, t, 0);
+  if (use_bulk && lane == 0 && t < P.count) {
+    mbar_expect_tx(&bar[0], bytes);
+    bulk_g2s(buf0, P.costs + (size_t)t * esz, bytes, &bar[0]);
+  }
+  int cur = 0;
+  unsigned phases = 0;
+  while (t < P.count) {
+    int tn = 0;
+    if (lane == 0) tn = atomicAdd(P.counter, 1);
+    tn = __shfl_sync(QAPB_FULL, tn, 0);
+    double* cb = cur ? buf1 : buf0;
+    if (use_bulk) {
+      if (lane == 0 && tn < P.count) {
+        double* nb = cur ? buf0 : buf1;
+        uint64_t* nbar = cur ? &bar[0] : &bar[1];
+        fence_proxy_async();
+        mbar_expect_tx(nbar, bytes);
+        bulk_g2s(nb, P.costs + (size_t)tn * esz, bytes, nbar);
+      }
+      mbar_wait(cur ? &bar[1] : &bar[0], (phases >> cur) & 1u);
+      phases ^= 1u << cur;
+    } else {
+      const double* src = P.costs + (size_t)t * esz;
+      for (int e = lane; e < (int)esz; e += 32) cb[e] = src[e];
+      __syncwarp();
+    }
+    LapLane<CPL> L;
+    const double value = warp_lap_solve<CPL>(cb, m, lane, L);
+    if (lane == 0) {
+      if (P.values) P.values[t] = value;
+      if (P.theta_ref && value < dsub(P.theta_ref[t], 1e-7)) {  // rlt2.cpp:332-335
+        atomicMin(P.err_tile, t);
+        if (P.stop_w) atomicExch(P.stop_w, 1);
+      }
+    }
+    warp_lap_write_duals<CPL>(m, lane, L, P.r2c ? P.r2c + (size_t)t * m : nullptr,
+                              P.c2r ? P.c2r + (size_t)t * m : nullptr,
+                              P.u ? P.u + (size_t)t * m : nullptr,
+                              P.v ? P.v + (size_t)t * m : nullptr);
+    if (P.pi) warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)t * esz);
+    __syncwarp();
+    t = tn;
+    if (use_bulk) cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Y stage (rlt2.cpp:383-426): warp per (i,p); the Y cost block is built
+// directly in shared memory (fused rlt2.cpp:391-408), then solved.
+template <int CPL>
+__global__ void __launch_bounds__(128) ystage_kernel(YStageParams P, int warps_per_block) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ double ysm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = P.m, my = m - 1;
+  const int ipf = blockIdx.x * warps_per_block + warp;
+  if (ipf >= m * m) return;
+  const int i = ipf / m, p = ipf - i * m;
+  const size_t mye = (size_t)my * my;
+  double* cost = ysm + (size_t)warp * (mye + my + 1);
+  double* urow = cost + mye;
+  const DIdx ix(m);
+  const double dm1 = (double)(m - 1);
+  const size_t base = (size_t)ipf * mye;
+  for (int e = lane; e < (int)mye; e += 32) {
+    const int a = e / my, bq = e - a * my;
+    const int j = a + (a >= i), q = bq + (bq >= p);
+    const int t = (i < j) ? ix.tile(i, j, p, q) : ix.tile(j, i, q, p);
+    double val;
+    if (!P.inc)
+      val = dadd(P.c[base + e], (i < j) ? P.theta[t] : 0.0);  // rlt2.cpp:401
+    else if (i < j)
+      val = P.theta[t];                                       // :403
+    else
+      val = dadd(P.ybar[t], ddiv(P.dx[(size_t)i * m + p], dm1));  // :405
+    cost[e] = val;
+  }
+  __syncwarp();
+  LapLane<CPL> L;
+  const double value = warp_lap_solve<CPL>(cost, my, lane, L);
+  if (lane == 0) P.delta[ipf] = value;
+  warp_lap_write_slack<CPL>(cost, my, lane, L, urow, P.piy + base);
+}
+
+// ---------------------------------------------------------------------------
+// X stage + bound (rlt2.cpp:428-449), feasibility (rlt2.cpp:453-473) and the
+// device-loop bookkeeping / termination tests of run() (rlt2.cpp:552-577).
+template <int CPL>
+__global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
+  DevScalars* S = P.S;
+  if (S->stop) return;
+  extern __shared__ double xsm[];
+  __shared__ int feas_bad;
+  __shared__ int sx[128];
+  const int m = P.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* xc = xsm;
+  double* urow = xsm + (size_t)m * m;
+  for (int e = tid; e < m * m; e += blockDim.x)
+    xc[e] = dadd(P.delta[e], P.inc ? 0.0 : P.b[e]);  // rlt2.cpp:433
+  if (tid == 0) feas_bad = 0;
+  __syncthreads();
+  if (warp == 0) {
+    LapLane<CPL> L;
+    const double nu = warp_lap_solve<CPL>(xc, m, lane, L);
+    warp_lap_write_slack<CPL>(xc, m, lane, L, urow, P.pix);
+    warp_lap_write_duals<CPL>(m, lane, L, P.xrow, P.xcol, nullptr, nullptr);
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int j = s * 32 + lane;
+      if (j < m) sx[L.p[s]] = j;
+    }
+    if (lane == 0) {  // rlt2.cpp:441-447
+      double last;
+      if (P.fast) {
+        S->running = dadd(S->running, nu);
+        last = dadd(S->running, S->offset);
+      } else {
+        last = dadd(nu, S->offset);
+      }
+      S->last_bound = last;
+      if (last > S->best) S->best = last;
+    }
+  }
+  __syncthreads();
+  const int had_cert = S->has_cert;
+  if (!had_cert) {  // rlt2.cpp:453-469
+    const DIdx ix(m);
+    const double tol = 1e-7;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = e / m, j = e - i * m;
+      if (i != j && P.piy[ix.cidx(i, sx[i], j, sx[j])] > tol) feas_bad = 1;
+    }
+    const size_t esz = (size_t)ix.esz;
+    for (int e = tid; e < m * m * m; e += blockDim.x) {
+      const int i = e / (m * m), rem = e - i * m * m, j = rem / m, k = rem - j * m;
+      if (!(i < j) || k == i || k == j) continue;
+      const int t = ix.tile(i, j, sx[i], sx[j]);
+      if (P.piz[(size_t)t * esz + ix.cell(i, j, sx[i], sx[j], k, sx[k])] > tol) feas_bad = 1;
+    }
+  }
+  __syncthreads();
+  if (!had_cert && !feas_bad) {
+    for (int e = tid; e < m; e += blockDim.x) P.cert[e] = sx[e];
+  }
+  if (tid == 0) {
+    if (!had_cert && !feas_bad) {  // rlt2.cpp:470-472
+      S->has_cert = 1;
+      S->cert_val = S->last_bound;
+    }
+    const int it = S->iter;
+    P.hist_bound[it] = S->last_bound;
+    P.hist_best[it] = S->best;
+    S->iter = it + 1;
+    if (S->run_mode) {  // run() termination, rlt2.cpp:556-577
+      const double best = S->best;
+      int term = -1;
+      if (S->has_cert) {
+        term = QAPB_TERM_FEASIBLE_FOUND;
+      } else {
+        double gap = __longlong_as_double(0x7ff0000000000000ll);
+        if (isfinite(P.upper_bound) && P.upper_bound != 0.0)
+          gap = ddiv(dsub(P.upper_bound, best), P.upper_bound);
+        if (P.min_gap > 0 && gap <= P.min_gap) {
+          term = QAPB_TERM_GAP_CLOSED;
+        } else if (best >= P.fathom) {
+          term = QAPB_TERM_EARLY_STOP;
+        } else if (P.es_window > 0 && (it + 1 - S->run_start) > P.es_window) {
+          const double prev = P.hist_best[it - P.es_window];
+          if (dsub(best, prev) < dmul(P.es_delta, fmax(1.0, fabs(best))))
+            term = QAPB_TERM_EARLY_STOP;
+        }
+      }
+      if (term < 0 && it + 1 >= P.iter_limit) term = QAPB_TERM_ITERATION_LIMIT;
+      if (term >= 0) {
+        S->term = term;
+        S->stop = 1;
+      }
+    }
+  }
+}
+
+// SA drain of b and running (rlt2.cpp:500-509); the draws are made on the
+// host with the reference's RNG (sa_fac / sa_loc uploaded before this).
+__global__ void sa_apply_kernel(int m, double* b, const double* sa_fac, const double* sa_loc,
+                                DevScalars* S, double drained, int fast) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+    const int i = e / m, p = e - i * m;
+    b[e] = dsub(b[e], dadd(sa_fac[i], sa_loc[p]));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && fast) S->running = dsub(S->running, drained);
+}
+
+// ===========================================================================
+// host launchers
+int lap_max_m() { return 127; }
+
+cudaError_t launch_init_store(int n, const double* flow, const double* dist,
+                              const double* linear, double* b, double* c, cudaStream_t st) {
+  const size_t nc = (size_t)n * n * (n - 1) * (n - 1);
+  const int blocks = (int)std::min<size_t>((nc + 255) / 256, (size_t)num_sms() * 8);
+  init_store_kernel<<<blocks, 256, 0, st>>>(n, flow, dist, linear, b, c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xyfold(const XYFoldParams& p, int tiles, cudaStream_t st) {
+  const int blocks = std::max(1, std::min((tiles + 255) / 256, num_sms() * 8));
+  xyfold_kernel<<<blocks, 256, 0, st>>>(p, tiles);
+  return cudaGetLastError();
+}
+
+int fold_chunk(int m) {
+  const size_t budget = 100 * 1024;  // 2 CTAs per SM
+  const size_t per = (size_t)3 * m * m * sizeof(double) + 2 * m * sizeof(double);
+  size_t c = (budget - (size_t)m * m * sizeof(double)) / per;
+  if (c < 1) c = 1;
+  if (c > (size_t)m) c = m;
+  return (int)c;
+}
+
+size_t fold_smem_bytes(int m, int chunk) {
+  return ((size_t)3 * chunk * m * m + 2 * (size_t)chunk * m + (size_t)m * m) * sizeof(double);
+}
+
+cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
+  const size_t smem = fold_smem_bytes(p.m, p.chunk);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  zfold_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st) {
+  const size_t smem = (size_t)3 * p.chunk * p.m * p.m * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  phase2_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+namespace {
+template <int CPL>
+cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
+  const int m = p.m;
+  const size_t esz = (size_t)m * m;
+  const size_t tile_bytes = esz * sizeof(double);
+  const bool aligned = (((uintptr_t)p.costs) & 15) == 0;
+  bool use_bulk = (tile_bytes % 16 == 0) && aligned;
+  const size_t buf_elems = align_up(esz, 16);  // 128-byte aligned buffers
+  auto wsm = [&](bool bulk) {
+    return align_up(((bulk ? 2 : 1) * buf_elems + ((m + 1) & ~1)) * sizeof(double) + 16, 128);
+  };
+  size_t warp_smem = wsm(use_bulk);
+  if (use_bulk && warp_smem > 200 * 1024) {
+    use_bulk = false;
+    warp_smem = wsm(false);
+  }
+  int W = (int)std::max<size_t>(1, std::min<size_t>(8, (110 * 1024) / warp_smem));
+  if (warp_smem * W > 220 * 1024) W = 1;
+  const size_t smem = warp_smem * W;
+  cudaFuncSetAttribute(lap_batch_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lap_batch_kernel<CPL>, 32 * W, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int need = (p.count + W - 1) / W;
+  const int blocks = std::max(1, std::min(need, per_sm * num_sms()));
+  lap_batch_kernel<CPL><<<blocks, 32 * W, smem, st>>>(p, (unsigned)warp_smem, (int)buf_elems,
+                                                       use_bulk ? 1 : 0);
+  return cudaGetLastError();
+}
+
+template <int CPL>
+cudaError_t launch_ystage_t(const YStageParams& p, cudaStream_t st) {
+  const int my = p.m - 1;
+  const int W = 4;
+  const size_t smem = (size_t)W * ((size_t)my * my + my + 1) * sizeof(double);
+  cudaFuncSetAttribute(ystage_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
+  const int blocks = (p.m * p.m + W - 1) / W;
+  ystage_kernel<CPL><<<blocks, 32 * W, smem, st>>>(p, W);
+  return cudaGetLastError();
+}
+
+template <int CPL>
+cudaError_t launch_xstage_t(const XStageParams& p, cudaStream_t st) {
+  const size_t smem = ((size_t)p.m * p.m + p.m + 1) * sizeof(double);
+  cudaFuncSetAttribute(xstage_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
+  xstage_kernel<CPL><<<1, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+inline int cpl_for(int m) { return m <= 31 ? 1 : (m <= 63 ? 2 : (m <= 95 ? 3 : 4)); }
+}  // namespace
+
+cudaError_t launch_lap_batch(const BatchLapParams& p, cudaStream_t st) {
+  if (p.count <= 0) return cudaSuccess;
+  switch (cpl_for(p.m)) {
+    case 1: return launch_lap_batch_t<1>(p, st);
+    case 2: return launch_lap_batch_t<2>(p, st);
+    case 3: return launch_lap_batch_t<3>(p, st);
+    default: return launch_lap_batch_t<4>(p, st);
+  }
+}
+
+cudaError_t launch_ystage(const YStageParams& p, cudaStream_t st) {
+  switch (cpl_for(p.m - 1)) {
+    case 1: return launch_ystage_t<1>(p, st);
+    case 2: return launch_ystage_t<2>(p, st);
+    case 3: return launch_ystage_t<3>(p, st);
+    default: return launch_ystage_t<4>(p, st);
+  }
+}
+
+cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st) {
+  switch (cpl_for(p.m)) {
+    case 1: return launch_xstage_t<1>(p, st);
+    case 2: return launch_xstage_t<2>(p, st);
+    case 3: return launch_xstage_t<3>(p, st);
+    default: return launch_xstage_t<4>(p, st);
+  }
+}
+
+cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
+                            DevScalars* S, double drained, int fast, cudaStream_t st) {
+  sa_apply_kernel<<<std::max(1, (m * m + 255) / 256), 256, 0, st>>>(m, b, sa_fac, sa_loc, S,
+                                                                    drained, fast);
+  return cudaGetLastError();
+}
+
+}  // namespace qapb

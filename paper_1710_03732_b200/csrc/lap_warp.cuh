@@ -1,0 +1,201 @@
+// lap_warp.cuh — warp-per-LAP shortest-augmenting-path Hungarian (sm_100a).
+//
+// Bit-exact re-design of LapSolver::solve (lap.cpp:24-84) for one warp:
+// lane l owns columns j = s*32 + l (s < CPL), including the virtual start
+// column m (lap.cpp:21-23).  Per Dijkstra step (lap.cpp:40-67) every lane
+// relaxes its columns in parallel; the reference's ascending scan with a
+// strict `<` ("first minimum wins", lap.cpp:53) becomes a warp argmin over an
+// order-preserving 64-bit key with the lowest column on ties, done with
+// `redux.sync` on the key halves (+ ballot / a third redux for the column).
+// Every per-element update (lap.cpp:48-65) is order independent, so the
+// result — assignment, duals, and the optimum summed in column order
+// (lap.cpp:75-80) — is bitwise identical to the serial reference.
+//
+// Row duals are kept per *column* (w[j] == u[p[j]]): u[i0] for the row that
+// just entered the tree is then read from the same lane as p[j1], so a step
+// needs one round of shuffles instead of two dependent ones.
+#pragma once
+
+#include "common.cuh"
+
+namespace qapb {
+
+// Order-preserving map double -> u64.  x + 0.0 canonicalises -0.0 to +0.0:
+// the serial scan's `<` treats them as equal, so they must share a key.
+__device__ __forceinline__ unsigned long long ordkey(double x) {
+  x = dadd(x, 0.0);
+  const long long b = __double_as_longlong(x);
+  return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+}
+
+template <int CPL>
+struct LapLane {
+  int p[CPL];     // row matched to column s*32+lane, -1 when free   (lap.cpp:30)
+  double w[CPL];  // dual of that row, u[p[j]]                       (lap.cpp:31 uu)
+  double v[CPL];  // column dual                                     (lap.cpp:31 vv)
+};
+
+// a[s] for a warp-uniform runtime slot s, without spilling `a` to local memory
+template <int CPL, class T>
+__device__ __forceinline__ T pick(const T (&a)[CPL], int s) {
+  T r = a[0];
+#pragma unroll
+  for (int k = 1; k < CPL; ++k)
+    if (s == k) r = a[k];
+  return r;
+}
+
+// Solve the m x m LAP whose row-major costs sit in shared memory `cost`.
+// All 32 lanes must call it.  Returns the optimum (warp-uniform).
+template <int CPL>
+__device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost, int m,
+                                                 int lane, LapLane<CPL>& L) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  double minv[CPL];
+  int way[CPL];
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    L.p[s] = -1;
+    L.w[s] = 0.0;
+    L.v[s] = 0.0;
+    way[s] = 0;
+  }
+  const int vs = m >> 5, vl = m & 31;  // owner of the virtual column m
+  for (int i = 0; i < m; ++i) {        // lap.cpp:33
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      minv[s] = INF;
+      if (s == vs && lane == vl) {  // p[m] = i; u[i] is still 0
+        L.p[s] = i;
+        L.w[s] = 0.0;
+      }
+    }
+    unsigned used = 0;
+    int j0 = m, i0 = i;
+    double ui0 = 0.0;
+    while (true) {  // Dijkstra step, lap.cpp:40-67
+      if ((j0 & 31) == lane) used |= 1u << (j0 >> 5);
+      const double* row = cost + (size_t)i0 * m;
+      unsigned long long bkey = ~0ull;
+      int bcol = 0x7fffffff;
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {
+        const int j = s * 32 + lane;
+        if (j < m && !((used >> s) & 1u)) {
+          const double cur = dsub(dsub(row[j], ui0), L.v[s]);  // lap.cpp:48
+          if (cur < minv[s]) {                                 // lap.cpp:49-52
+            minv[s] = cur;
+            way[s] = j0;
+          }
+          const unsigned long long k = ordkey(minv[s]);
+          if (k < bkey) {
+            bkey = k;
+            bcol = j;
+          }
+        }
+      }
+      // argmin over unused columns, lowest column on ties (lap.cpp:53-56)
+      const unsigned hi = (unsigned)(bkey >> 32), lo = (unsigned)bkey;
+      const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
+      const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
+      const bool cand = (hi == hmin) && (lo == lmin) && (bcol != 0x7fffffff);
+      int j1;
+      if (CPL == 1) {
+        j1 = __ffs(__ballot_sync(QAPB_FULL, cand)) - 1;
+      } else {
+        j1 = (int)__reduce_min_sync(QAPB_FULL, cand ? (unsigned)bcol : 0xffffffffu);
+      }
+      const int s1 = j1 >> 5, l1 = j1 & 31;
+      const double delta = __shfl_sync(QAPB_FULL, pick<CPL>(minv, s1), l1);
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {  // dual update, lap.cpp:58-65
+        const int j = s * 32 + lane;
+        if (j <= m) {
+          if ((used >> s) & 1u) {
+            L.w[s] = dadd(L.w[s], delta);
+            L.v[s] = dsub(L.v[s], delta);
+          } else {
+            minv[s] = dsub(minv[s], delta);
+          }
+        }
+      }
+      j0 = j1;
+      const int pj = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, s1), l1);
+      const double wj = __shfl_sync(QAPB_FULL, pick<CPL>(L.w, s1), l1);
+      if (pj == -1) break;  // lap.cpp:67
+      i0 = pj;
+      ui0 = wj;
+    }
+    while (j0 != m) {  // augment, lap.cpp:68-72
+      const int s0 = j0 >> 5, l0 = j0 & 31;
+      const int jw = __shfl_sync(QAPB_FULL, pick<CPL>(way, s0), l0);
+      const int sw = jw >> 5, lw = jw & 31;
+      const int pw = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, sw), lw);
+      const double ww = __shfl_sync(QAPB_FULL, pick<CPL>(L.w, sw), lw);
+      if (lane == l0) {
+#pragma unroll
+        for (int s = 0; s < CPL; ++s)
+          if (s == s0) {
+            L.p[s] = pw;
+            L.w[s] = ww;
+          }
+      }
+      j0 = jw;
+    }
+  }
+  // value = sum_j cost[p[j]][j], accumulated in column order (lap.cpp:75-80)
+  double term[CPL];
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = s * 32 + lane;
+    term[s] = (j < m) ? cost[(size_t)L.p[s] * m + j] : 0.0;
+  }
+  double value = 0.0;
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int lim = m - s * 32 < 32 ? m - s * 32 : 32;
+    for (int l = 0; l < lim; ++l) value = dadd(value, __shfl_sync(QAPB_FULL, term[s], l));
+  }
+  return value;
+}
+
+// pi[a][b] = (cost[a][b] - u[a]) - v[b]   (rlt2.cpp:320-322, :420-422, :439-440)
+// `urow` is m doubles of per-warp shared scratch.  `out` may be global.
+template <int CPL>
+__device__ __forceinline__ void warp_lap_write_slack(const double* __restrict__ cost, int m,
+                                                     int lane, const LapLane<CPL>& L,
+                                                     double* urow, double* __restrict__ out) {
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = s * 32 + lane;
+    if (j < m) urow[L.p[s]] = L.w[s];
+  }
+  __syncwarp();
+  for (int a = 0; a < m; ++a) {
+    const double ua = urow[a];
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int b = s * 32 + lane;
+      if (b < m) out[(size_t)a * m + b] = dsub(dsub(cost[(size_t)a * m + b], ua), L.v[s]);
+    }
+  }
+  __syncwarp();
+}
+
+// row_to_col / col_to_row / u / v outputs of LapSolver::solve (lap.cpp:76-82)
+template <int CPL>
+__device__ __forceinline__ void warp_lap_write_duals(int m, int lane, const LapLane<CPL>& L,
+                                                     int* r2c, int* c2r, double* u, double* v) {
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = s * 32 + lane;
+    if (j < m) {
+      if (c2r) c2r[j] = L.p[s];
+      if (r2c) r2c[L.p[s]] = j;
+      if (u) u[L.p[s]] = L.w[s];
+      if (v) v[j] = L.v[s];
+    }
+  }
+}
+
+}  // namespace qapb
