@@ -210,6 +210,30 @@ QAPB_API qapb_status qapb_engine_snapshot(qapb_engine* e, double* b, double* c,
  * the bench's gpu_launches claim). */
 QAPB_API qapb_status qapb_engine_launch_count(qapb_engine* e, long long* n);
 
+/* ---- device-loop / measurement hooks (B200 extension) ----------------
+ * enqueue: put `iters` iterate() steps on the engine's stream without any
+ * host synchronisation (SA must be off); synchronize: wait, then surface any
+ * deferred error (phase-2 regression -> QAPB_ELOGIC).  stream returns the
+ * engine's cudaStream_t.  With profiling on, every kernel is bracketed by
+ * CUDA events on that stream; kernel_times returns the accumulated device
+ * milliseconds and launch counts per kernel kind (QAPB_K_*) since the last
+ * reset, and run() fills IterationRecord::{z,y,x}_ms. */
+enum {
+  QAPB_K_XYFOLD = 0,  /* ascent_update x/y levels, rlt2.cpp:244-262 */
+  QAPB_K_ZFOLD = 1,   /* ascent_update z level,    rlt2.cpp:269-298 */
+  QAPB_K_ZLAP = 2,    /* Z-LAP batch,              rlt2.cpp:308-325 */
+  QAPB_K_PHASE2 = 3,  /* stage_z_second_phase,     rlt2.cpp:344-381 */
+  QAPB_K_YSTAGE = 4,  /* stage_y,                  rlt2.cpp:383-426 */
+  QAPB_K_XSTAGE = 5,  /* stage_x + feasibility,    rlt2.cpp:428-473 */
+  QAPB_K_COUNT = 6
+};
+QAPB_API qapb_status qapb_engine_enqueue(qapb_engine* e, int iters);
+QAPB_API qapb_status qapb_engine_synchronize(qapb_engine* e);
+QAPB_API qapb_status qapb_engine_stream(qapb_engine* e, void** stream);
+QAPB_API qapb_status qapb_engine_set_profiling(qapb_engine* e, int on);
+QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms,
+                                              long long* launches, int reset);
+
 /* run_ascent(inst, cfg), rlt2.cpp:590-597: instance in, report out.  The
  * certificate value is re-evaluated on the instance as the reference does. */
 QAPB_API qapb_status qapb_run_ascent(int n, const double* flow,

@@ -480,6 +480,24 @@ QAPB_API qapb_status qapb_engine_launch_count(qapb_engine* e, long long* n) {
   return QAPB_OK;
 }
 
+QAPB_API qapb_status qapb_engine_enqueue(qapb_engine* e, int iters) {
+  return guard([&] { e->e->enqueue(iters); });
+}
+QAPB_API qapb_status qapb_engine_synchronize(qapb_engine* e) {
+  return guard([&] { e->e->synchronize(); });
+}
+QAPB_API qapb_status qapb_engine_stream(qapb_engine* e, void** stream) {
+  *stream = (void*)e->e->stream();
+  return QAPB_OK;
+}
+QAPB_API qapb_status qapb_engine_set_profiling(qapb_engine* e, int on) {
+  return guard([&] { e->e->set_profiling(on != 0); });
+}
+QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms, long long* launches,
+                                              int reset) {
+  return guard([&] { e->e->kernel_times(ms, launches, reset != 0); });
+}
+
 QAPB_API qapb_status qapb_run_ascent(int n, const double* flow, const double* dist,
                                      const double* linear, const qapb_config* cfg,
                                      qapb_report* rep, qapb_record* records, int max_records,

@@ -165,6 +165,11 @@ void Engine::init_state() {
 Engine::~Engine() {
   if (st_) cudaStreamSynchronize(st_);
   if (graph_) cudaGraphExecDestroy(graph_);
+  for (auto& pe : pending_) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
+  for (auto e : ev_pool_) cudaEventDestroy(e);
   dfree(b_); dfree(c_); dfree(d_); dfree(piz_); dfree(incz_); dfree(piy_); dfree(pix_);
   dfree(theta_); dfree(theta1_); dfree(delta_); dfree(ybar_); dfree(dx_); dfree(push_);
   dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
@@ -222,7 +227,9 @@ void Engine::enqueue_stage_z(int it) {  // rlt2.cpp:301-338
   p.values = is_two_phase() ? theta1_ : theta_;
   p.pi = piz_;
   cuda_check(cudaMemsetAsync(counter_, 0, sizeof(int), st_), "memset counter");
+  kbegin(QAPB_K_ZLAP);
   cuda_check(launch_lap_batch(p, st_), "z-stage");
+  kend();
   ++launches_;
   if (is_two_phase()) {  // rlt2.cpp:328-336
     FoldParams f{};
@@ -234,13 +241,17 @@ void Engine::enqueue_stage_z(int it) {  // rlt2.cpp:301-338
     f.piz = piz_;
     f.costs = costs;
     f.stop = &S_->stop;
+    kbegin(QAPB_K_PHASE2);
     cuda_check(launch_phase2(f, st_), "phase-2");
+    kend();
     ++launches_;
     p.values = theta_;
     p.theta_ref = theta1_;
     p.err_tile = &S_->err_tile;
     cuda_check(cudaMemsetAsync(counter_, 0, sizeof(int), st_), "memset counter");
+    kbegin(QAPB_K_ZLAP);
     cuda_check(launch_lap_batch(p, st_), "z-stage phase 2");
+    kend();
     ++launches_;
   }
 }
@@ -248,12 +259,14 @@ void Engine::enqueue_stage_z(int it) {  // rlt2.cpp:301-338
 void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   const bool inc = is_fast() && it > 0;
   const bool steady = it > 0;
-  if (steady && graph_) {
+  cur_iter_ = it;
+  if (steady && graph_ && !profiling_) {
     cuda_check(cudaGraphLaunch(graph_, st_), "graph launch");
     launches_ += graph_launches_;
     return;
   }
-  const bool capture = steady && it >= 2 && !graph_ && !env_flag("QAPB_NO_GRAPH");
+  const bool capture =
+      steady && it >= 2 && !graph_ && !profiling_ && !env_flag("QAPB_NO_GRAPH");
   cudaGraph_t g = nullptr;
   const long long l0 = launches_;
   if (capture)
@@ -275,7 +288,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     x.push = push_;
     x.fpair_ij = fpair_ij_;
     x.stop = &S_->stop;
+    kbegin(QAPB_K_XYFOLD);
     cuda_check(launch_xyfold(x, tiles_, st_), "xy-fold");
+    kend();
     ++launches_;
     FoldParams f{};
     f.m = m_;
@@ -293,7 +308,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     f.sa_fac = sa_fac_;
     f.sa_loc = sa_loc_;
     f.stop = &S_->stop;
+    kbegin(QAPB_K_ZFOLD);
     cuda_check(launch_zfold(f, st_), "z-fold");
+    kend();
     ++launches_;
   }
   enqueue_stage_z(it);
@@ -307,7 +324,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   y.delta = delta_;
   y.piy = piy_;
   y.stop = &S_->stop;
+  kbegin(QAPB_K_YSTAGE);
   cuda_check(launch_ystage(y, st_), "y-stage");
+  kend();
   ++launches_;
   XStageParams xs{};
   xs.m = m_;
@@ -330,7 +349,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   xs.es_delta = cfg_.early_stop_delta;
   xs.es_window = cfg_.early_stop_window;
   xs.iter_limit = cfg_.iter_limit;
+  kbegin(QAPB_K_XSTAGE);
   cuda_check(launch_xstage(xs, st_), "x-stage");
+  kend();
   ++launches_;
   if (capture) {
     cuda_check(cudaStreamEndCapture(st_, &g), "end capture");
@@ -405,9 +426,16 @@ double Engine::iterate() {
   ensure_hist(hS_.iter + 1);
   enqueue_iteration(hS_.iter);
   pull_scalars();
+  if (profiling_) collect_events();
   check_phase2();
   if (cfg_.sa_enabled && !hS_.has_cert) sa_perturb();
   last_rec_ = qapb_record{hS_.iter, hS_.last_bound, gap(), 0, 0, 0};
+  const int k = hS_.iter - 1;
+  if ((int)stage_ms_.size() >= 3 * (k + 1)) {
+    last_rec_.z_ms = stage_ms_[3 * k];
+    last_rec_.y_ms = stage_ms_[3 * k + 1];
+    last_rec_.x_ms = stage_ms_[3 * k + 2];
+  }
   return hS_.last_bound;
 }
 
@@ -426,6 +454,11 @@ void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) cons
     r.gap = (!std::isfinite(cfg_.upper_bound) || cfg_.upper_bound == 0)
                 ? kInf
                 : (cfg_.upper_bound - best) / cfg_.upper_bound;
+    if ((int)stage_ms_.size() >= 3 * (k + 1)) {
+      r.z_ms = stage_ms_[3 * k];
+      r.y_ms = stage_ms_[3 * k + 1];
+      r.x_ms = stage_ms_[3 * k + 2];
+    }
     recs->push_back(r);
   }
 }
@@ -454,6 +487,7 @@ void Engine::run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<i
     }
   }
   const int to = hS_.iter;
+  if (profiling_) collect_events();
   if (recs && cfg_.record_history) fill_records(from, to, recs);
   hS_.run_mode = 0;
   hS_.stop = 0;
@@ -524,6 +558,91 @@ void Engine::get_array(int which, double* dst, size_t count) const {
     case QAPB_ARR_INCZ: src = incz_; break;
   }
   if (n) cuda_check(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H array");
+}
+
+// ---- measurement hooks ---------------------------------------------------
+void Engine::kbegin(int kind) {
+  if (!profiling_) return;
+  if (ev_pool_.size() < 2) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      ev_pool_.push_back(e);
+    }
+  }
+  ev_open_ = ev_pool_.back();
+  ev_pool_.pop_back();
+  kind_open_ = kind;
+  cuda_check(cudaEventRecord(ev_open_, st_), "cudaEventRecord");
+}
+
+void Engine::kend() {
+  if (!profiling_ || kind_open_ < 0) return;
+  cudaEvent_t b = ev_pool_.back();
+  ev_pool_.pop_back();
+  cuda_check(cudaEventRecord(b, st_), "cudaEventRecord");
+  pending_.push_back(PendingEvent{kind_open_, cur_iter_, ev_open_, b});
+  kind_open_ = -1;
+}
+
+void Engine::collect_events() {
+  for (auto& pe : pending_) {
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, pe.a, pe.b), "cudaEventElapsedTime");
+    kms_[pe.kind] += ms;
+    kcnt_[pe.kind] += 1;
+    const int stage = (pe.kind == QAPB_K_ZLAP || pe.kind == QAPB_K_PHASE2)
+                          ? 0
+                          : (pe.kind == QAPB_K_YSTAGE ? 1 : (pe.kind == QAPB_K_XSTAGE ? 2 : -1));
+    if (stage >= 0) {
+      if ((int)stage_ms_.size() < 3 * (pe.iter + 1)) stage_ms_.resize(3 * (pe.iter + 1), 0.0);
+      stage_ms_[3 * pe.iter + stage] += ms;
+    }
+    ev_pool_.push_back(pe.a);
+    ev_pool_.push_back(pe.b);
+  }
+  pending_.clear();
+}
+
+void Engine::enqueue(int iters) {
+  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  if (cfg_.sa_enabled)
+    throw std::invalid_argument("enqueue: SA needs a host step per iteration; use iterate()");
+  if (iters <= 0) return;
+  if (hS_.run_mode || hS_.stop) {
+    hS_.run_mode = 0;
+    hS_.stop = 0;
+    push_scalars();
+  }
+  ensure_hist(hS_.iter + iters);
+  for (int k = 0; k < iters; ++k) enqueue_iteration(hS_.iter + k);
+  hS_.iter += iters;  // host view; refreshed by synchronize()
+}
+
+void Engine::synchronize() {
+  pull_scalars();
+  if (profiling_) collect_events();
+  check_phase2();
+}
+
+void Engine::set_profiling(bool on) {
+  if (on == profiling_) return;
+  cuda_check(cudaStreamSynchronize(st_), "sync");
+  if (profiling_) collect_events();
+  profiling_ = on;
+}
+
+void Engine::kernel_times(double* ms, long long* launches, bool reset) {
+  cuda_check(cudaStreamSynchronize(st_), "sync");
+  collect_events();
+  for (int k = 0; k < QAPB_K_COUNT; ++k) {
+    if (ms) ms[k] = kms_[k];
+    if (launches) launches[k] = kcnt_[k];
+    if (reset) {
+      kms_[k] = 0;
+      kcnt_[k] = 0;
+    }
+  }
 }
 
 }  // namespace qapb

@@ -58,6 +58,12 @@ class Engine {
   qapb_record last_record() const { return last_rec_; }
   long long launches() const { return launches_; }
 
+  // measurement / device-loop hooks (qapb_engine_enqueue & co.)
+  void enqueue(int iters);
+  void synchronize();
+  void set_profiling(bool on);
+  void kernel_times(double* ms, long long* launches, bool reset);
+
   // device pointers for in-process consumers (bench / multi-GPU layer)
   double* dev_d() const { return d_; }
   double* dev_piz() const { return piz_; }
@@ -75,6 +81,23 @@ class Engine {
   void check_phase2();
   void fill_records(int from, int to, std::vector<qapb_record>* recs) const;
   void build_graph();
+  void kbegin(int kind);
+  void kend();
+  void collect_events();
+
+  struct PendingEvent {
+    int kind, iter;
+    cudaEvent_t a, b;
+  };
+  bool profiling_ = false;
+  int cur_iter_ = 0;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<PendingEvent> pending_;
+  cudaEvent_t ev_open_ = nullptr;
+  int kind_open_ = -1;
+  double kms_[QAPB_K_COUNT] = {0};
+  long long kcnt_[QAPB_K_COUNT] = {0};
+  std::vector<double> stage_ms_;  // per iteration: z, y, x
 
   int m_, dev_;
   qapb_config cfg_;
