@@ -231,6 +231,10 @@ QAPB_API qapb_status qapb_engine_enqueue(qapb_engine* e, int iters);
 QAPB_API qapb_status qapb_engine_synchronize(qapb_engine* e);
 QAPB_API qapb_status qapb_engine_stream(qapb_engine* e, void** stream);
 QAPB_API qapb_status qapb_engine_set_profiling(qapb_engine* e, int on);
+/* Per-iteration bound history (IterationRecord::bound of iterations
+ * [from, from+count), 0-based), kept on the device for every iteration. */
+QAPB_API qapb_status qapb_engine_history(qapb_engine* e, int from, int count,
+                                         double* bounds, double* best);
 QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms,
                                               long long* launches, int reset);
 

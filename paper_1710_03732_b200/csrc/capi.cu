@@ -493,6 +493,10 @@ QAPB_API qapb_status qapb_engine_stream(qapb_engine* e, void** stream) {
 QAPB_API qapb_status qapb_engine_set_profiling(qapb_engine* e, int on) {
   return guard([&] { e->e->set_profiling(on != 0); });
 }
+QAPB_API qapb_status qapb_engine_history(qapb_engine* e, int from, int count, double* bounds,
+                                         double* best) {
+  return guard([&] { e->e->history(from, count, bounds, best); });
+}
 QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms, long long* launches,
                                               int reset) {
   return guard([&] { e->e->kernel_times(ms, launches, reset != 0); });

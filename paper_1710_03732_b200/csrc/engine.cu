@@ -625,6 +625,16 @@ void Engine::synchronize() {
   check_phase2();
 }
 
+void Engine::history(int from, int count, double* bounds, double* best) const {
+  if (from < 0 || count < 0 || from + count > hS_.iter)
+    throw std::invalid_argument("history: range outside completed iterations");
+  if (!count) return;
+  if (bounds)
+    cuda_check(cudaMemcpy(bounds, hist_bound_ + from, count * 8, cudaMemcpyDeviceToHost), "D2H");
+  if (best)
+    cuda_check(cudaMemcpy(best, hist_best_ + from, count * 8, cudaMemcpyDeviceToHost), "D2H");
+}
+
 void Engine::set_profiling(bool on) {
   if (on == profiling_) return;
   cuda_check(cudaStreamSynchronize(st_), "sync");

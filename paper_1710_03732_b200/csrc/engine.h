@@ -63,6 +63,7 @@ class Engine {
   void synchronize();
   void set_profiling(bool on);
   void kernel_times(double* ms, long long* launches, bool reset);
+  void history(int from, int count, double* bounds, double* best) const;
 
   // device pointers for in-process consumers (bench / multi-GPU layer)
   double* dev_d() const { return d_; }

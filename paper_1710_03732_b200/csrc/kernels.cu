@@ -11,6 +11,7 @@
 // contiguous.  See DESIGN.md for the roofline of each kernel.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/qapb200.h"
 #include "common.cuh"
@@ -132,15 +133,18 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
   return f;
 }
 
-// Visit every member cell of the CTA's families: fn(member, pa_l, pb, pc, g)
-// with g the cell's offset in the reference layout.  Consecutive threads get
-// consecutive columns of one tile row (coalesced for X1 and X2; X3 rows are
-// read `chunk` doubles at a time, the rest of the row by the sibling CTAs).
+// Visit every member cell of the CTA's families: fn(member, pa_l, pb, pc, g, slot)
+// with g the cell's offset in the reference layout and slot a dense per-CTA
+// index (member-major) used to stage the cell's D' / cost value.
+// Consecutive threads get consecutive columns of one tile row (coalesced for
+// X1 and X2; X3 rows are read `chunk` doubles at a time, the rest of each row
+// by the sibling CTAs that run next to it, through L2).
 template <class Fn>
-__device__ __forceinline__ void for_family_cells(const FamilyCtx& f, Fn&& fn) {
+__device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, Fn&& fn) {
   const DIdx ix(f.n);
   const int tid = threadIdx.x, bd = blockDim.x;
-  const int seg1 = f.Pe * f.nm1, cnt12 = seg1 * f.nm2;
+  const int cnt12 = f.Pe * f.nm1 * f.nm2;
+  const int base2 = chunk * f.nm1 * f.nm2, base3 = 2 * base2;
   // X1: tiles (a,b,pa,pb), row c-2, column -> pc
   for (int e = tid; e < cnt12; e += bd) {
     const int sg = e / f.nm2, r = e - sg * f.nm2;
@@ -149,7 +153,7 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, Fn&& fn) {
     const int pc = skip2(r, min(pa, pb), max(pa, pb));
     const size_t g = (size_t)(f.fab * f.lpairs + ix.lpair(pa, pb)) * f.esz +
                      (size_t)(f.c - 2) * f.nm2 + r;
-    fn(0, pa_l, pb, pc, g);
+    fn(0, pa_l, pb, pc, g, e);
   }
   // X2: tiles (a,c,pa,pc), row b-1, column -> pb
   for (int e = tid; e < cnt12; e += bd) {
@@ -159,7 +163,7 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, Fn&& fn) {
     const int pb = skip2(r, min(pa, pc), max(pa, pc));
     const size_t g = (size_t)(f.fac * f.lpairs + ix.lpair(pa, pc)) * f.esz +
                      (size_t)(f.b - 1) * f.nm2 + r;
-    fn(1, pa_l, pb, pc, g);
+    fn(1, pa_l, pb, pc, g, base2 + e);
   }
   // X3: tiles (b,c,pb,pc), row a, column <- pa
   const int cnt3 = f.n * f.nm1 * f.Pe;
@@ -173,15 +177,37 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, Fn&& fn) {
     const int col = pa - (pa > lo) - (pa > hi);
     const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
                      (size_t)f.a * f.nm2 + col;
-    fn(2, pa_l, pb, pc, g);
+    fn(2, pa_l, pb, pc, g, base3 + e);
   }
 }
 
-__device__ __forceinline__ void stage_family_pi(const FamilyCtx& f, const double* __restrict__ piz,
-                                                double* S, int chunk) {
-  const int nn = f.n * f.n;
-  for_family_cells(f, [&](int mem, int pa_l, int pb, int pc, size_t g) {
-    S[(size_t)mem * chunk * nn + (pa_l * f.n + pb) * f.n + pc] = piz[g];
+// shared-memory plan of a fold CTA (doubles): pi(z) of the three members as a
+// dense [chunk][n][n+1] cube each (odd pitch: conflict-free column walks),
+// the CTA's D' / cost values in visit order, and the push terms.
+struct FoldSmem {
+  int np, cube, nslots;
+  __host__ __device__ FoldSmem(int n, int chunk)
+      : np(n + 1), cube(chunk * n * (n + 1)),
+        nslots(2 * chunk * (n - 1) * (n - 2) + chunk * n * (n - 1)) {}
+  __host__ __device__ size_t pi_off() const { return 0; }
+  __host__ __device__ size_t val_off() const { return (size_t)3 * cube; }
+  __host__ __device__ size_t push_off() const { return (size_t)3 * cube + nslots; }
+  __host__ __device__ size_t total(int n, int chunk) const {
+    return push_off() + 2 * (size_t)chunk * n + (size_t)n * n;
+  }
+};
+
+// Stage pi(z) of all members and the D'/cost value of every member cell with
+// cp.async; everything is in flight before the CTA waits once.
+__device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
+                                             const double* __restrict__ piz,
+                                             const double* __restrict__ vals, double* sm,
+                                             const FoldSmem& L) {
+  double* S = sm + L.pi_off();
+  double* V = sm + L.val_off();
+  for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
+    cp_async8(S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc, piz + g);
+    cp_async8(V + slot, vals + g);
   });
 }
 
@@ -190,32 +216,35 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
   const FamilyCtx f = family_ctx(P);
-  const int n = f.n, nn = n * n, C = P.chunk;
-  double* S = sm;                      // [3][C][n][n] pi(z) of X1, X2, X3
-  double* U1 = S + (size_t)3 * C * nn;  // [C][n]  push of tile (a,b,pa,pb)
-  double* U2 = U1 + C * n;             // [C][n]  push of tile (a,c,pa,pc)
-  double* U3 = U2 + C * n;             // [n][n]  push of tile (b,c,pb,pc)
+  const int n = f.n, C = P.chunk;
+  const FoldSmem L(n, C);
+  double* S = sm + L.pi_off();
+  double* V = sm + L.val_off();
+  double* U1 = sm + L.push_off();  // [C][n]  push of tile (a,b,pa,pb)
+  double* U2 = U1 + C * n;         // [C][n]  push of tile (a,c,pa,pc)
+  double* U3 = U2 + C * n;         // [n][n]  push of tile (b,c,pb,pc)
   const DIdx ix(n);
   const int tid = threadIdx.x, bd = blockDim.x;
+  stage_family(f, C, P.piz, P.d, sm, L);
   for (int e = tid; e < f.Pe * n; e += bd) {
     const int pa_l = e / n, q = e - pa_l * n, pa = f.pa0 + pa_l;
     if (q == pa) continue;
     U1[e] = P.push[f.fab * f.lpairs + ix.lpair(pa, q)];
     U2[e] = P.push[f.fac * f.lpairs + ix.lpair(pa, q)];
   }
-  for (int e = tid; e < nn; e += bd) {
+  for (int e = tid; e < n * n; e += bd) {
     const int pb = e / n, pc = e - pb * n;
     if (pb != pc) U3[e] = P.push[f.fbc * f.lpairs + ix.lpair(pb, pc)];
   }
-  stage_family_pi(f, P.piz, S, C);
+  cp_async_wait_all();
   __syncthreads();
   const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
   double* __restrict__ d = P.d;
   double* __restrict__ incz = P.incz;
   const int fast = P.fast;
-  for_family_cells(f, [&](int mem, int pa_l, int pb, int pc, size_t g) {
-    const int fi = (pa_l * n + pb) * n + pc;
-    const double p1 = S[fi], p2 = S[(size_t)C * nn + fi], p3 = S[(size_t)2 * C * nn + fi];
+  for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
+    const int fi = (pa_l * n + pb) * L.np + pc;
+    const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
     const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
     const double s3 = dadd(dmul(kz, p3), U3[pb * n + pc]);
@@ -230,8 +259,8 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
       own = p3;
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
     }
-    d[g] = dadd(d[g], dsub(gain, dmul(kz, own)));   // rlt2.cpp:292
-    if (fast) incz[g] = dadd(dmul(omk, own), gain);  // rlt2.cpp:293
+    d[g] = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
+    if (fast) incz[g] = dadd(dmul(omk, own), gain);   // rlt2.cpp:293
   });
   if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
     P.sa_fac[tid] = 0.0;
@@ -245,15 +274,18 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
   const FamilyCtx f = family_ctx(P);
-  const int n = f.n, nn = n * n, C = P.chunk;
-  double* S = sm;
-  stage_family_pi(f, P.piz, S, C);
+  const int n = f.n, C = P.chunk;
+  const FoldSmem L(n, C);
+  double* S = sm + L.pi_off();
+  double* V = sm + L.val_off();
+  stage_family(f, C, P.piz, P.costs, sm, L);
+  cp_async_wait_all();
   __syncthreads();
   double* __restrict__ costs = P.costs;
   const double tol = 1e-9;
-  for_family_cells(f, [&](int mem, int pa_l, int pb, int pc, size_t g) {
-    const int fi = (pa_l * n + pb) * n + pc;
-    const double p1 = S[fi], p2 = S[(size_t)C * nn + fi], p3 = S[(size_t)2 * C * nn + fi];
+  for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
+    const int fi = (pa_l * n + pb) * L.np + pc;
+    const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     double total = 0.0;
     int nb = 3;
     if (p1 > tol) total = dadd(total, p1); else ++nb;
@@ -262,7 +294,7 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
     const double share = ddiv(total, (double)nb);
     const double own = mem == 0 ? p1 : (mem == 1 ? p2 : p3);
     const double add = (total <= 0.0) ? 0.0 : ((own > tol) ? -own : share);
-    costs[g] = dadd(costs[g], dadd(add, share));  // rlt2.cpp:376-378
+    costs[g] = dadd(V[slot], dadd(add, share));  // rlt2.cpp:376-378
   });
 }
 
@@ -273,46 +305,45 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
 // (cp.async.bulk + mbarrier), prefetching tile k+1 while solving tile k.
 template <int CPL>
 __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
-                                                        int buf_elems, int use_bulk) {
+                                                        int buf_elems, int use_bulk, int nbuf) {
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char* ws = smem_raw + (size_t)warp * warp_smem;
   double* buf0 = reinterpret_cast<double*>(ws);
   double* buf1 = buf0 + buf_elems;
-  double* urow = buf0 + (use_bulk ? 2 : 1) * buf_elems;
+  double* urow = buf0 + nbuf * buf_elems;
   uint64_t* bar = reinterpret_cast<uint64_t*>(urow + ((P.m + 1) & ~1));
   const int m = P.m;
   const size_t esz = (size_t)m * m;
   const unsigned bytes = (unsigned)(esz * sizeof(double));
+  auto grab = [&]() {
+    int x = 0;
+    if (lane == 0) x = atomicAdd(P.counter, 1);
+    return __shfl_sync(QAPB_FULL, x, 0);
+  };
+  auto issue = [&](double* dst, int tile, uint64_t* b) {  // lane 0 only
+    fence_proxy_async();
+    mbar_expect_tx(b, bytes);
+    bulk_g2s(dst, P.costs + (size_t)tile * esz, bytes, b);
+  };
   if (use_bulk && lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
   __syncwarp();
-  int t = 0;
-  if (lane == 0) t = atomicAdd(P.counter, 1);
-  t = __shfl_sync(QAPB_FULL, t, 0);
-  if (use_bulk && lane == 0 && t < P.count) {
-    mbar_expect_tx(&bar[0], bytes);
-    bulk_g2s(buf0, P.costs + (size_t)t * esz, bytes, &bar[0]);
+  int t = grab();
+  int tn = grab();
+  if (use_bulk && lane == 0) {
+    if (t < P.count) issue(buf0, t, &bar[0]);
+    if (nbuf == 2 && tn < P.count) issue(buf1, tn, &bar[1]);
   }
   int cur = 0;
   unsigned phases = 0;
   while (t < P.count) {
-    int tn = 0;
-    if (lane == 0) tn = atomicAdd(P.counter, 1);
-    tn = __shfl_sync(QAPB_FULL, tn, 0);
     double* cb = cur ? buf1 : buf0;
     if (use_bulk) {
-      if (lane == 0 && tn < P.count) {
-        double* nb = cur ? buf0 : buf1;
-        uint64_t* nbar = cur ? &bar[0] : &bar[1];
-        fence_proxy_async();
-        mbar_expect_tx(nbar, bytes);
-        bulk_g2s(nb, P.costs + (size_t)tn * esz, bytes, nbar);
-      }
       mbar_wait(cur ? &bar[1] : &bar[0], (phases >> cur) & 1u);
       phases ^= 1u << cur;
     } else {
@@ -320,6 +351,7 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
       for (int e = lane; e < (int)esz; e += 32) cb[e] = src[e];
       __syncwarp();
     }
+    const int tnn = grab();
     LapLane<CPL> L;
     const double value = warp_lap_solve<CPL>(cb, m, lane, L);
     if (lane == 0) {
@@ -335,8 +367,16 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
                               P.v ? P.v + (size_t)t * m : nullptr);
     if (P.pi) warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)t * esz);
     __syncwarp();
+    if (use_bulk && lane == 0) {  // buffer `cur` is free again
+      if (nbuf == 2) {
+        if (tnn < P.count) issue(cb, tnn, cur ? &bar[1] : &bar[0]);
+      } else if (tn < P.count) {
+        issue(cb, tn, &bar[0]);
+      }
+    }
+    if (nbuf == 2) cur ^= 1;
     t = tn;
-    if (use_bulk) cur ^= 1;
+    tn = tnn;
   }
 }
 
@@ -505,62 +545,64 @@ cudaError_t launch_xyfold(const XYFoldParams& p, int tiles, cudaStream_t st) {
 }
 
 int fold_chunk(int m) {
-  const size_t budget = 100 * 1024;  // 2 CTAs per SM
-  const size_t per = (size_t)3 * m * m * sizeof(double) + 2 * m * sizeof(double);
-  size_t c = (budget - (size_t)m * m * sizeof(double)) / per;
-  if (c < 1) c = 1;
-  if (c > (size_t)m) c = m;
-  return (int)c;
+  // largest pa-chunk whose CTA plan fits ~52 KB (4 CTAs / SM), at least 1
+  int best = 1;
+  for (int c = 1; c <= m; ++c) {
+    const FoldSmem L(m, c);
+    if (L.total(m, c) * sizeof(double) <= 52 * 1024) best = c;
+  }
+  const char* e = std::getenv("QAPB_FOLD_CHUNK");
+  if (e && *e) best = std::max(1, std::min(m, std::atoi(e)));
+  return best;
 }
 
 size_t fold_smem_bytes(int m, int chunk) {
-  return ((size_t)3 * chunk * m * m + 2 * (size_t)chunk * m + (size_t)m * m) * sizeof(double);
+  const FoldSmem L(m, chunk);
+  return L.total(m, chunk) * sizeof(double);
 }
 
 cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr = true;
-  }
+  cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
   zfold_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st) {
-  const size_t smem = (size_t)3 * p.chunk * p.m * p.m * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr = true;
-  }
+  const size_t smem = fold_smem_bytes(p.m, p.chunk);
+  cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
   phase2_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
 
 namespace {
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
 template <int CPL>
 cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const int m = p.m;
   const size_t esz = (size_t)m * m;
   const size_t tile_bytes = esz * sizeof(double);
   const bool aligned = (((uintptr_t)p.costs) & 15) == 0;
-  bool use_bulk = (tile_bytes % 16 == 0) && aligned;
+  const bool use_bulk = (tile_bytes % 16 == 0) && aligned;
   const size_t buf_elems = align_up(esz, 16);  // 128-byte aligned buffers
-  auto wsm = [&](bool bulk) {
-    return align_up(((bulk ? 2 : 1) * buf_elems + ((m + 1) & ~1)) * sizeof(double) + 16, 128);
+  // tile buffers per warp: 1 (more resident warps) unless QAPB_LAP_NBUF=2
+  int nbuf = use_bulk ? std::max(1, std::min(2, env_int("QAPB_LAP_NBUF", 1))) : 1;
+  auto wsm = [&](int nb) {
+    return align_up((nb * buf_elems + ((m + 1) & ~1)) * sizeof(double) + 16, 128);
   };
-  size_t warp_smem = wsm(use_bulk);
-  if (use_bulk && warp_smem > 200 * 1024) {
-    use_bulk = false;
-    warp_smem = wsm(false);
+  size_t warp_smem = wsm(nbuf);
+  if (nbuf == 2 && warp_smem > 100 * 1024) {
+    nbuf = 1;
+    warp_smem = wsm(1);
   }
-  int W = (int)std::max<size_t>(1, std::min<size_t>(8, (110 * 1024) / warp_smem));
-  if (warp_smem * W > 220 * 1024) W = 1;
+  const int wmax = std::max(1, std::min(8, env_int("QAPB_LAP_WARPS", 8)));
+  int W = (int)std::max<size_t>(1, std::min<size_t>(wmax, (110 * 1024) / warp_smem));
   const size_t smem = warp_smem * W;
   cudaFuncSetAttribute(lap_batch_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
@@ -570,7 +612,7 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const int need = (p.count + W - 1) / W;
   const int blocks = std::max(1, std::min(need, per_sm * num_sms()));
   lap_batch_kernel<CPL><<<blocks, 32 * W, smem, st>>>(p, (unsigned)warp_smem, (int)buf_elems,
-                                                       use_bulk ? 1 : 0);
+                                                       use_bulk ? 1 : 0, nbuf);
   return cudaGetLastError();
 }
 

@@ -23,9 +23,8 @@ namespace qapb {
 // Order-preserving map double -> u64.  x + 0.0 canonicalises -0.0 to +0.0:
 // the serial scan's `<` treats them as equal, so they must share a key.
 __device__ __forceinline__ unsigned long long ordkey(double x) {
-  x = dadd(x, 0.0);
-  const long long b = __double_as_longlong(x);
-  return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+  const long long b = __double_as_longlong(dadd(x, 0.0));
+  return (unsigned long long)(b ^ ((b >> 63) | (long long)0x8000000000000000ull));
 }
 
 template <int CPL>
@@ -45,11 +44,77 @@ __device__ __forceinline__ T pick(const T (&a)[CPL], int s) {
   return r;
 }
 
+// One-column-per-lane form (m <= 31): the hot path of the Z stage at n <= 33.
+// Same arithmetic as the generic form; minv of a used column is dead until
+// the next row (lap.cpp:36-39 resets it), so it is shifted unconditionally.
+__device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ cost, int m,
+                                                   int lane, LapLane<1>& L) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const bool real = lane < m;
+  const double* __restrict__ colp = cost + (real ? lane : m - 1);
+  L.p[0] = -1;
+  L.w[0] = 0.0;
+  L.v[0] = 0.0;
+  int way = 0;
+  for (int i = 0; i < m; ++i) {  // lap.cpp:33
+    double minv = INF;
+    if (lane == m) {  // p[m] = i; u[i] is still 0
+      L.p[0] = i;
+      L.w[0] = 0.0;
+    }
+    bool used = false;
+    int j0 = m, i0 = i;
+    double ui0 = 0.0;
+    while (true) {  // lap.cpp:40-67
+      used = used || (lane == j0);
+      const double cur = dsub(dsub(colp[i0 * m], ui0), L.v[0]);  // lap.cpp:48
+      const bool act = real && !used;
+      const bool upd = act && (cur < minv);
+      minv = upd ? cur : minv;
+      way = upd ? j0 : way;
+      const unsigned long long k = ordkey(minv);
+      const unsigned hi = act ? (unsigned)(k >> 32) : 0xffffffffu;
+      const unsigned lo = act ? (unsigned)k : 0xffffffffu;
+      const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
+      const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
+      const int j1 = __ffs(__ballot_sync(QAPB_FULL, act && hi == hmin && lo == lmin)) - 1;
+      const double delta = __shfl_sync(QAPB_FULL, minv, j1);
+      minv = dsub(minv, delta);  // lap.cpp:63 (dead for used columns)
+      const double wn = dadd(L.w[0], delta), vn = dsub(L.v[0], delta);
+      L.w[0] = used ? wn : L.w[0];  // lap.cpp:60-61
+      L.v[0] = used ? vn : L.v[0];
+      j0 = j1;
+      const int pj = __shfl_sync(QAPB_FULL, L.p[0], j1);
+      const double wj = __shfl_sync(QAPB_FULL, L.w[0], j1);
+      if (pj == -1) break;
+      i0 = pj;
+      ui0 = wj;
+    }
+    while (j0 != m) {  // augment, lap.cpp:68-72
+      const int jw = __shfl_sync(QAPB_FULL, way, j0);
+      const int pw = __shfl_sync(QAPB_FULL, L.p[0], jw);
+      const double ww = __shfl_sync(QAPB_FULL, L.w[0], jw);
+      if (lane == j0) {
+        L.p[0] = pw;
+        L.w[0] = ww;
+      }
+      j0 = jw;
+    }
+  }
+  const double term = real ? cost[(size_t)L.p[0] * m + lane] : 0.0;
+  double value = 0.0;  // lap.cpp:75-80
+  for (int l = 0; l < m; ++l) value = dadd(value, __shfl_sync(QAPB_FULL, term, l));
+  return value;
+}
+
 // Solve the m x m LAP whose row-major costs sit in shared memory `cost`.
 // All 32 lanes must call it.  Returns the optimum (warp-uniform).
 template <int CPL>
 __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost, int m,
                                                  int lane, LapLane<CPL>& L) {
+  if constexpr (CPL == 1) {
+    return warp_lap_solve_1(cost, m, lane, L);
+  }
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double minv[CPL];
   int way[CPL];
@@ -79,19 +144,21 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
       unsigned long long bkey = ~0ull;
       int bcol = 0x7fffffff;
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {
+      for (int s = 0; s < CPL; ++s) {  // branch-free relaxation of this lane's columns
         const int j = s * 32 + lane;
-        if (j < m && !((used >> s) & 1u)) {
-          const double cur = dsub(dsub(row[j], ui0), L.v[s]);  // lap.cpp:48
-          if (cur < minv[s]) {                                 // lap.cpp:49-52
-            minv[s] = cur;
-            way[s] = j0;
-          }
-          const unsigned long long k = ordkey(minv[s]);
-          if (k < bkey) {
-            bkey = k;
-            bcol = j;
-          }
+        const double cv = row[j < m ? j : m - 1];
+        const bool act = (j < m) && !((used >> s) & 1u);
+        const double cur = dsub(dsub(cv, ui0), L.v[s]);  // lap.cpp:48
+        const bool upd = act && (cur < minv[s]);           // lap.cpp:49-52
+        minv[s] = upd ? cur : minv[s];
+        way[s] = upd ? j0 : way[s];
+        const unsigned long long k = act ? ordkey(minv[s]) : ~0ull;
+        if (CPL == 1) {
+          bkey = k;
+          bcol = act ? j : 0x7fffffff;
+        } else if (k < bkey) {
+          bkey = k;
+          bcol = j;
         }
       }
       // argmin over unused columns, lowest column on ties (lap.cpp:53-56)
@@ -110,14 +177,13 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
 #pragma unroll
       for (int s = 0; s < CPL; ++s) {  // dual update, lap.cpp:58-65
         const int j = s * 32 + lane;
-        if (j <= m) {
-          if ((used >> s) & 1u) {
-            L.w[s] = dadd(L.w[s], delta);
-            L.v[s] = dsub(L.v[s], delta);
-          } else {
-            minv[s] = dsub(minv[s], delta);
-          }
-        }
+        const bool us = ((used >> s) & 1u) != 0;
+        const bool inr = j <= m;
+        const double wn = dadd(L.w[s], delta), vn = dsub(L.v[s], delta);
+        const double mn = dsub(minv[s], delta);
+        L.w[s] = (inr && us) ? wn : L.w[s];
+        L.v[s] = (inr && us) ? vn : L.v[s];
+        minv[s] = (inr && !us) ? mn : minv[s];
       }
       j0 = j1;
       const int pj = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, s1), l1);

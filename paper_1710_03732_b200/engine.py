@@ -59,6 +59,14 @@ lib.qapb_engine_launch_count.argtypes = [_vp, _P(C.c_longlong)]
 lib.qapb_run_ascent.argtypes = [C.c_int, _vp, _vp, _vp, _P(Config), _P(Report), _vp, C.c_int,
                                 _vp]
 lib.qapb_device_count.argtypes = [_P(C.c_int)]
+lib.qapb_engine_enqueue.argtypes = [_vp, C.c_int]
+lib.qapb_engine_synchronize.argtypes = [_vp]
+lib.qapb_engine_stream.argtypes = [_vp, _P(_vp)]
+lib.qapb_engine_set_profiling.argtypes = [_vp, C.c_int]
+lib.qapb_engine_kernel_times.argtypes = [_vp, _vp, _vp, C.c_int]
+lib.qapb_engine_history.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
+
+KERNEL_NAMES = ["xyfold", "zfold", "zlap", "phase2", "ystage", "xstage"]
 
 
 class QapbError(RuntimeError):
@@ -420,6 +428,36 @@ class AscentEngine:
         x = np.empty(self.m, np.int32)
         _check(lib.qapb_engine_x_assignment(self._h, iptr(x)))
         return [int(v) for v in x]
+
+    # ---- device-loop / measurement hooks (B200 extension) ----
+    def enqueue(self, iters: int):
+        """Enqueue `iters` iterate() steps with no host synchronisation."""
+        _check(lib.qapb_engine_enqueue(self._h, iters))
+
+    def synchronize(self):
+        _check(lib.qapb_engine_synchronize(self._h))
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(lib.qapb_engine_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def set_profiling(self, on: bool):
+        _check(lib.qapb_engine_set_profiling(self._h, int(on)))
+
+    def kernel_times(self, reset: bool = False):
+        ms = np.zeros(len(KERNEL_NAMES))
+        n = np.zeros(len(KERNEL_NAMES), np.int64)
+        _check(lib.qapb_engine_kernel_times(self._h, dptr(ms), n.ctypes.data_as(C.c_void_p),
+                                            int(reset)))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNEL_NAMES)}
+
+    def history(self, start: int = 0, count: Optional[int] = None):
+        if count is None:
+            count = self.iteration() - start
+        b, best = np.empty(count), np.empty(count)
+        _check(lib.qapb_engine_history(self._h, start, count, dptr(b), dptr(best)))
+        return b, best
 
     def launch_count(self) -> int:
         n = C.c_longlong()

@@ -100,6 +100,11 @@ def main():
         tr[f"rand{nn}_S2"] = trace(orc, f, d, "S2", 40, snap_at=(40,))
         tr[f"rand{nn}_F1_SA"] = trace(orc, f, d, "F1", 40, sa=True, ub=float("inf"), seed=seed,
                                       snap_at=(40,))
+    # n=30 pins: the bench workload and the tai-a-shaped case
+    g30f, g30d = grid(5, 6, orc)
+    tr["grid30_F1"] = trace(orc, g30f, g30d, "F1", 6, snap_at=(2,))
+    f30, d30 = orc.generate_instance(30, 1, 99)
+    tr["rand30_S1"] = trace(orc, f30, d30, "S1", 3)
     out["traces"] = tr
     # iteration-1 (Gilmore-Lawler) values of the reference test instances
     gl = {}
