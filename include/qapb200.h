@@ -231,6 +231,12 @@ QAPB_API qapb_status qapb_engine_enqueue(qapb_engine* e, int iters);
 QAPB_API qapb_status qapb_engine_synchronize(qapb_engine* e);
 QAPB_API qapb_status qapb_engine_stream(qapb_engine* e, void** stream);
 QAPB_API qapb_status qapb_engine_set_profiling(qapb_engine* e, int on);
+/* Kernel-isolation timing (tuning only): launch kernel `kind` (QAPB_K_*)
+ * `reps` times on the engine's current state and return the mean device
+ * milliseconds.  DESTROYS the engine's numerical state (the fold is applied
+ * repeatedly); the engine must not be used for results afterwards. */
+QAPB_API qapb_status qapb_engine_time_kernel(qapb_engine* e, int kind, int reps,
+                                             double* ms);
 /* Per-iteration bound history (IterationRecord::bound of iterations
  * [from, from+count), 0-based), kept on the device for every iteration. */
 QAPB_API qapb_status qapb_engine_history(qapb_engine* e, int from, int count,

@@ -493,6 +493,9 @@ QAPB_API qapb_status qapb_engine_stream(qapb_engine* e, void** stream) {
 QAPB_API qapb_status qapb_engine_set_profiling(qapb_engine* e, int on) {
   return guard([&] { e->e->set_profiling(on != 0); });
 }
+QAPB_API qapb_status qapb_engine_time_kernel(qapb_engine* e, int kind, int reps, double* ms) {
+  return guard([&] { *ms = e->e->time_kernel(kind, reps); });
+}
 QAPB_API qapb_status qapb_engine_history(qapb_engine* e, int from, int count, double* bounds,
                                          double* best) {
   return guard([&] { e->e->history(from, count, bounds, best); });

@@ -29,6 +29,11 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
 bool env_flag(const char* name) {
   const char* v = std::getenv(name);
   return v && *v && std::strcmp(v, "0") != 0;
@@ -84,6 +89,7 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
 void Engine::alloc() {
   cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
   const int m = m_;
   fpairs_ = m * (m - 1) / 2;
   lpairs_ = m * (m - 1);
@@ -115,7 +121,8 @@ void Engine::alloc() {
   dalloc(&cert_, m);
   dalloc(&triples_, 3 * (size_t)ntriples_);
   dalloc(&fpair_ij_, fpairs_);
-  dalloc(&counter_, 4);
+  plan_pipeline();
+  dalloc(&counter_, stage_ev_.size() + 2);
   dalloc(&S_, 1);
   cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hSpin_), sizeof(DevScalars)),
              "cudaMallocHost");
@@ -175,6 +182,9 @@ Engine::~Engine() {
   dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
   dfree(fpair_ij_); dfree(counter_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
   if (hSpin_) cudaFreeHost(hSpin_);
+  for (auto e : stage_ev_) cudaEventDestroy(e);
+  if (join_ev_) cudaEventDestroy(join_ev_);
+  if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -215,44 +225,122 @@ void Engine::pull_scalars() {
   hS_ = *hSpin_;
 }
 
-void Engine::enqueue_stage_z(int it) {  // rlt2.cpp:301-338
-  double* costs = (is_fast() && it > 0) ? incz_ : d_;
+void Engine::plan_pipeline() {
+  // Stage k folds the triples whose first facility is in [A_k, A_k+1)
+  // (contiguous in lexicographic order) and then completes every facility
+  // pair (i, j) with i in that range: no later triple touches those tiles, so
+  // their Z-LAPs may overwrite pi(z) in place while stage k+1 folds.
+  const int m = m_;
+  const int K = std::max(1, std::min(m - 1, env_int("QAPB_ZSTAGES", 1)));
+  const int total = (m - 1) * m / 2;  // facility pairs
+  stage_a_.assign(1, 0);
+  int acc = 0;
+  for (int a = 0; a < m - 1; ++a) {
+    acc += m - 1 - a;
+    if ((int)stage_a_.size() < K && acc * K >= total * (int)stage_a_.size() && a + 1 < m - 1)
+      stage_a_.push_back(a + 1);
+  }
+  stage_a_.push_back(m - 1);
+  auto c2 = [](int x) { return x >= 2 ? x * (x - 1) / 2 : 0; };
+  auto tri_before = [&](int a) {  // triples whose first facility is < a
+    int t = 0;
+    for (int x = 0; x < a; ++x) t += c2(m - 1 - x);
+    return t;
+  };
+  auto fp_first = [&](int i) { return i * m - i * (i + 1) / 2; };  // fpair(i, i+1)
+  const int S = (int)stage_a_.size() - 1;
+  stage_t0_.resize(S);
+  stage_tiles_.resize(S);
+  stage_z0_.resize(S);
+  stage_zn_.resize(S);
+  for (int k = 0; k < S; ++k) {
+    const int A0 = stage_a_[k], A1 = stage_a_[k + 1];
+    stage_t0_[k] = tri_before(A0);
+    stage_tiles_[k] = tri_before(A1) - stage_t0_[k];
+    stage_z0_[k] = fp_first(A0) * lpairs_;
+    stage_zn_[k] = fp_first(A1) * lpairs_ - stage_z0_[k];
+  }
+  stage_ev_.resize(S);
+  for (auto& e : stage_ev_)
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming), "event");
+}
+
+void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
+                          const double* theta_ref, int slot, cudaStream_t st) {
+  if (count <= 0) return;
+  const size_t esz = (size_t)esz_;
   BatchLapParams p{};
-  p.costs = costs;
+  p.costs = costs + (size_t)t0 * esz;
   p.m = m_ - 2;
-  p.count = tiles_;
-  p.counter = counter_;
+  p.count = count;
+  p.counter = counter_ + slot;
   p.stop = &S_->stop;
   p.stop_w = &S_->stop;
-  p.values = is_two_phase() ? theta1_ : theta_;
-  p.pi = piz_;
-  cuda_check(cudaMemsetAsync(counter_, 0, sizeof(int), st_), "memset counter");
-  kbegin(QAPB_K_ZLAP);
-  cuda_check(launch_lap_batch(p, st_), "z-stage");
-  kend();
+  p.values = values + t0;
+  p.pi = piz_ + (size_t)t0 * esz;
+  p.theta_ref = theta_ref ? theta_ref + t0 : nullptr;
+  p.err_tile = &S_->err_tile;
+  p.tile_base = t0;
+  kbegin(QAPB_K_ZLAP, st);
+  cuda_check(launch_lap_batch(p, st), "z-stage");
+  kend(st);
   ++launches_;
+}
+
+FoldParams Engine::fold_params(int stage) const {
+  FoldParams f{};
+  f.m = m_;
+  f.triples = triples_ + 3 * (size_t)(stage < 0 ? 0 : stage_t0_[stage]);
+  f.ntriples = stage < 0 ? ntriples_ : stage_tiles_[stage];
+  f.chunk = chunk_;
+  f.nchunks = nchunks_;
+  f.kz = cfg_.kappa_z_upper;
+  f.phi = cfg_.phi_split;
+  f.fast = is_fast();
+  f.d = d_;
+  f.piz = piz_;
+  f.incz = incz_;
+  f.push = push_;
+  f.sa_fac = sa_fac_;
+  f.sa_loc = sa_loc_;
+  f.stop = &S_->stop;
+  return f;
+}
+
+// stage_z, rlt2.cpp:301-338.  Steady F/S iterations run fold+Z-LAP as the
+// stage pipeline; iteration 0 (no fold) solves every tile at once.
+void Engine::enqueue_stage_z(int it) {
+  double* costs = (is_fast() && it > 0) ? incz_ : d_;
+  double* vals1 = is_two_phase() ? theta1_ : theta_;
+  const int S = (int)stage_ev_.size();
+  cuda_check(cudaMemsetAsync(counter_, 0, (S + 2) * sizeof(int), st_), "memset counters");
+  if (it > 0) {
+    for (int k = 0; k < S; ++k) {
+      if (stage_tiles_[k] > 0) {  // z-level fold of this stage, rlt2.cpp:269-298
+        const FoldParams f = fold_params(k);
+        kbegin(QAPB_K_ZFOLD, st_);
+        cuda_check(launch_zfold(f, st_), "z-fold");
+        kend(st_);
+        ++launches_;
+      }
+      cuda_check(cudaEventRecord(stage_ev_[k], st_), "event record");
+      cuda_check(cudaStreamWaitEvent(st2_, stage_ev_[k], 0), "stream wait");
+      enqueue_zlap(costs, stage_z0_[k], stage_zn_[k], vals1, nullptr, k, st2_);
+    }
+    cuda_check(cudaEventRecord(join_ev_, st2_), "event record");
+    cuda_check(cudaStreamWaitEvent(st_, join_ev_, 0), "stream wait");
+  } else {
+    enqueue_zlap(costs, 0, tiles_, vals1, nullptr, S, st_);
+  }
   if (is_two_phase()) {  // rlt2.cpp:328-336
-    FoldParams f{};
-    f.m = m_;
-    f.triples = triples_;
-    f.ntriples = ntriples_;
-    f.chunk = chunk_;
-    f.nchunks = nchunks_;
-    f.piz = piz_;
+    FoldParams f = fold_params(-1);
     f.costs = costs;
-    f.stop = &S_->stop;
-    kbegin(QAPB_K_PHASE2);
+    kbegin(QAPB_K_PHASE2, st_);
     cuda_check(launch_phase2(f, st_), "phase-2");
-    kend();
+    kend(st_);
     ++launches_;
-    p.values = theta_;
-    p.theta_ref = theta1_;
-    p.err_tile = &S_->err_tile;
-    cuda_check(cudaMemsetAsync(counter_, 0, sizeof(int), st_), "memset counter");
-    kbegin(QAPB_K_ZLAP);
-    cuda_check(launch_lap_batch(p, st_), "z-stage phase 2");
-    kend();
-    ++launches_;
+    enqueue_zlap(costs, 0, tiles_, theta_, theta1_, S + 1, st_);
   }
 }
 
@@ -271,7 +359,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   const long long l0 = launches_;
   if (capture)
     cuda_check(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "capture");
-  if (steady) {  // ascent_update, rlt2.cpp:237-299
+  if (steady) {  // ascent_update x/y levels, rlt2.cpp:244-262 (z level: enqueue_stage_z)
     XYFoldParams x{};
     x.m = m_;
     x.kx = cfg_.kappa_x;
@@ -288,29 +376,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     x.push = push_;
     x.fpair_ij = fpair_ij_;
     x.stop = &S_->stop;
-    kbegin(QAPB_K_XYFOLD);
+    kbegin(QAPB_K_XYFOLD, st_);
     cuda_check(launch_xyfold(x, tiles_, st_), "xy-fold");
-    kend();
-    ++launches_;
-    FoldParams f{};
-    f.m = m_;
-    f.triples = triples_;
-    f.ntriples = ntriples_;
-    f.chunk = chunk_;
-    f.nchunks = nchunks_;
-    f.kz = cfg_.kappa_z_upper;
-    f.phi = cfg_.phi_split;
-    f.fast = is_fast();
-    f.d = d_;
-    f.piz = piz_;
-    f.incz = incz_;
-    f.push = push_;
-    f.sa_fac = sa_fac_;
-    f.sa_loc = sa_loc_;
-    f.stop = &S_->stop;
-    kbegin(QAPB_K_ZFOLD);
-    cuda_check(launch_zfold(f, st_), "z-fold");
-    kend();
+    kend(st_);
     ++launches_;
   }
   enqueue_stage_z(it);
@@ -324,9 +392,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   y.delta = delta_;
   y.piy = piy_;
   y.stop = &S_->stop;
-  kbegin(QAPB_K_YSTAGE);
+  kbegin(QAPB_K_YSTAGE, st_);
   cuda_check(launch_ystage(y, st_), "y-stage");
-  kend();
+  kend(st_);
   ++launches_;
   XStageParams xs{};
   xs.m = m_;
@@ -349,9 +417,9 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   xs.es_delta = cfg_.early_stop_delta;
   xs.es_window = cfg_.early_stop_window;
   xs.iter_limit = cfg_.iter_limit;
-  kbegin(QAPB_K_XSTAGE);
+  kbegin(QAPB_K_XSTAGE, st_);
   cuda_check(launch_xstage(xs, st_), "x-stage");
-  kend();
+  kend(st_);
   ++launches_;
   if (capture) {
     cuda_check(cudaStreamEndCapture(st_, &g), "end capture");
@@ -561,7 +629,7 @@ void Engine::get_array(int which, double* dst, size_t count) const {
 }
 
 // ---- measurement hooks ---------------------------------------------------
-void Engine::kbegin(int kind) {
+void Engine::kbegin(int kind, cudaStream_t st) {
   if (!profiling_) return;
   if (ev_pool_.size() < 2) {
     for (int k = 0; k < 64; ++k) {
@@ -573,14 +641,14 @@ void Engine::kbegin(int kind) {
   ev_open_ = ev_pool_.back();
   ev_pool_.pop_back();
   kind_open_ = kind;
-  cuda_check(cudaEventRecord(ev_open_, st_), "cudaEventRecord");
+  cuda_check(cudaEventRecord(ev_open_, st), "cudaEventRecord");
 }
 
-void Engine::kend() {
+void Engine::kend(cudaStream_t st) {
   if (!profiling_ || kind_open_ < 0) return;
   cudaEvent_t b = ev_pool_.back();
   ev_pool_.pop_back();
-  cuda_check(cudaEventRecord(b, st_), "cudaEventRecord");
+  cuda_check(cudaEventRecord(b, st), "cudaEventRecord");
   pending_.push_back(PendingEvent{kind_open_, cur_iter_, ev_open_, b});
   kind_open_ = -1;
 }
@@ -635,6 +703,50 @@ void Engine::history(int from, int count, double* bounds, double* best) const {
     cuda_check(cudaMemcpy(best, hist_best_ + from, count * 8, cudaMemcpyDeviceToHost), "D2H");
 }
 
+double Engine::time_kernel(int kind, int reps) {
+  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  cuda_check(cudaStreamSynchronize(st_), "sync");
+  cudaEvent_t a, b;
+  cuda_check(cudaEventCreate(&a), "event");
+  cuda_check(cudaEventCreate(&b), "event");
+  hS_.stop = 0;
+  hS_.run_mode = 0;
+  push_scalars();
+  const int S = (int)stage_ev_.size();
+  double* costs = is_fast() ? incz_ : d_;
+  auto one = [&]() {
+    switch (kind) {
+      case QAPB_K_ZFOLD: {
+        FoldParams f = fold_params(-1);
+        cuda_check(launch_zfold(f, st_), "z-fold");
+        break;
+      }
+      case QAPB_K_PHASE2: {
+        FoldParams f = fold_params(-1);
+        f.costs = costs;
+        cuda_check(launch_phase2(f, st_), "phase-2");
+        break;
+      }
+      case QAPB_K_ZLAP:
+        cuda_check(cudaMemsetAsync(counter_, 0, (S + 2) * sizeof(int), st_), "memset");
+        enqueue_zlap(costs, 0, tiles_, theta_, nullptr, S, st_);
+        break;
+      default:
+        throw std::invalid_argument("time_kernel: unsupported kernel kind");
+    }
+  };
+  one();  // warm
+  cuda_check(cudaEventRecord(a, st_), "event");
+  for (int r = 0; r < reps; ++r) one();
+  cuda_check(cudaEventRecord(b, st_), "event");
+  cuda_check(cudaEventSynchronize(b), "sync");
+  float ms = 0;
+  cuda_check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms / std::max(1, reps);
+}
+
 void Engine::set_profiling(bool on) {
   if (on == profiling_) return;
   cuda_check(cudaStreamSynchronize(st_), "sync");
@@ -644,6 +756,7 @@ void Engine::set_profiling(bool on) {
 
 void Engine::kernel_times(double* ms, long long* launches, bool reset) {
   cuda_check(cudaStreamSynchronize(st_), "sync");
+  cuda_check(cudaStreamSynchronize(st2_), "sync");
   collect_events();
   for (int k = 0; k < QAPB_K_COUNT; ++k) {
     if (ms) ms[k] = kms_[k];

@@ -64,6 +64,7 @@ class Engine {
   void set_profiling(bool on);
   void kernel_times(double* ms, long long* launches, bool reset);
   void history(int from, int count, double* bounds, double* best) const;
+  double time_kernel(int kind, int reps);
 
   // device pointers for in-process consumers (bench / multi-GPU layer)
   double* dev_d() const { return d_; }
@@ -75,6 +76,9 @@ class Engine {
   void init_state();
   void enqueue_iteration(int iter_index);
   void enqueue_stage_z(int iter_index);
+  void enqueue_zlap(double* costs, int t0, int count, double* values, const double* theta_ref,
+                    int counter_slot, cudaStream_t st);
+  void plan_pipeline();
   void ensure_hist(int need);
   void pull_scalars();
   void push_scalars();
@@ -82,8 +86,9 @@ class Engine {
   void check_phase2();
   void fill_records(int from, int to, std::vector<qapb_record>* recs) const;
   void build_graph();
-  void kbegin(int kind);
-  void kend();
+  void kbegin(int kind, cudaStream_t st);
+  void kend(cudaStream_t st);
+  FoldParams fold_params(int stage) const;
   void collect_events();
 
   struct PendingEvent {
@@ -105,12 +110,21 @@ class Engine {
   int tiles_, esz_, fpairs_, lpairs_, ntriples_, chunk_, nchunks_;
   size_t nb_, nc_, nd_;
   cudaStream_t st_ = nullptr;
+  // Z pipeline: fold stage k (triples with first facility in [A_k, A_k+1)) on
+  // st_, then the Z-LAPs of the facility pairs it completed on st2_, which
+  // overlap fold stage k+1.
+  cudaStream_t st2_ = nullptr;
+  std::vector<int> stage_a_;                 // stage boundaries in first facility
+  std::vector<int> stage_t0_, stage_tiles_;  // triple range per stage
+  std::vector<int> stage_z0_, stage_zn_;     // tile range per stage
+  std::vector<cudaEvent_t> stage_ev_;
+  cudaEvent_t join_ev_ = nullptr;
   double *b_ = nullptr, *c_ = nullptr, *d_ = nullptr, *piz_ = nullptr, *incz_ = nullptr;
   double *piy_ = nullptr, *pix_ = nullptr, *theta_ = nullptr, *theta1_ = nullptr;
   double *delta_ = nullptr, *ybar_ = nullptr, *dx_ = nullptr, *push_ = nullptr;
   double *sa_fac_ = nullptr, *sa_loc_ = nullptr;
   int *xrow_ = nullptr, *xcol_ = nullptr, *cert_ = nullptr, *triples_ = nullptr;
-  int *fpair_ij_ = nullptr, *counter_ = nullptr;
+  int *fpair_ij_ = nullptr, *counter_ = nullptr;  // counter_: one per Z launch
   DevScalars* S_ = nullptr;
   double *hist_bound_ = nullptr, *hist_best_ = nullptr;
   int hist_cap_ = 0;

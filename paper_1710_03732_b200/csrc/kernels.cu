@@ -34,6 +34,10 @@ int num_sms() {
   return g_num_sms;
 }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -143,41 +147,67 @@ template <class Fn>
 __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, Fn&& fn) {
   const DIdx ix(f.n);
   const int tid = threadIdx.x, bd = blockDim.x;
-  const int cnt12 = f.Pe * f.nm1 * f.nm2;
-  const int base2 = chunk * f.nm1 * f.nm2, base3 = 2 * base2;
-  // X1: tiles (a,b,pa,pb), row c-2, column -> pc
-  for (int e = tid; e < cnt12; e += bd) {
-    const int sg = e / f.nm2, r = e - sg * f.nm2;
-    const int pa_l = sg / f.nm1, pbi = sg - pa_l * f.nm1;
-    const int pa = f.pa0 + pa_l, pb = pbi + (pbi >= pa);
-    const int pc = skip2(r, min(pa, pb), max(pa, pb));
-    const size_t g = (size_t)(f.fab * f.lpairs + ix.lpair(pa, pb)) * f.esz +
-                     (size_t)(f.c - 2) * f.nm2 + r;
-    fn(0, pa_l, pb, pc, g, e);
+  const int nm1 = f.nm1, nm2 = f.nm2;
+  const int cnt12 = f.Pe * nm1 * nm2;
+  const int base2 = chunk * nm1 * nm2, base3 = 2 * base2;
+  // index stepping without divisions: e advances by bd per iteration
+  const int dsg = bd / nm2, dr = bd - dsg * nm2;
+  const int sg0 = tid / nm2, r0 = tid - sg0 * nm2;
+  const int pl0 = sg0 / nm1, qi0 = sg0 - pl0 * nm1;
+  for (int mem = 0; mem < 2; ++mem) {
+    // X1: tiles (a,b,pa,pb), row c-2, column -> pc
+    // X2: tiles (a,c,pa,pc), row b-1, column -> pb
+    const int fpr = mem ? f.fac : f.fab;
+    const size_t rowoff = (size_t)(mem ? f.b - 1 : f.c - 2) * nm2;
+    int r = r0, pa_l = pl0, qi = qi0;
+    for (int e = tid; e < cnt12; e += bd) {
+      const int pa = f.pa0 + pa_l, q = qi + (qi >= pa);
+      const int other = skip2(r, min(pa, q), max(pa, q));
+      const size_t g = (size_t)(fpr * f.lpairs + ix.lpair(pa, q)) * f.esz + rowoff + r;
+      if (mem == 0)
+        fn(0, pa_l, q, other, g, e);
+      else
+        fn(1, pa_l, other, q, g, base2 + e);
+      r += dr;
+      int inc = dsg;
+      if (r >= nm2) {
+        r -= nm2;
+        ++inc;
+      }
+      qi += inc;
+      while (qi >= nm1) {
+        qi -= nm1;
+        ++pa_l;
+      }
+    }
   }
-  // X2: tiles (a,c,pa,pc), row b-1, column -> pb
-  for (int e = tid; e < cnt12; e += bd) {
-    const int sg = e / f.nm2, r = e - sg * f.nm2;
-    const int pa_l = sg / f.nm1, pci = sg - pa_l * f.nm1;
-    const int pa = f.pa0 + pa_l, pc = pci + (pci >= pa);
-    const int pb = skip2(r, min(pa, pc), max(pa, pc));
-    const size_t g = (size_t)(f.fac * f.lpairs + ix.lpair(pa, pc)) * f.esz +
-                     (size_t)(f.b - 1) * f.nm2 + r;
-    fn(1, pa_l, pb, pc, g, base2 + e);
-  }
-  // X3: tiles (b,c,pb,pc), row a, column <- pa
-  const int cnt3 = f.n * f.nm1 * f.Pe;
+  // X3: tiles (b,c,pb,pc), row a, column <- pa; e = (pair, pa_l), pa fastest
+  const int Pe = f.Pe;
+  const int cnt3 = f.n * nm1 * Pe;
+  const int dpr = bd / Pe, dpl = bd - dpr * Pe;
+  int pair = tid / Pe, pa_l = tid - pair * Pe;
+  int pb = pair / nm1, pci = pair - pb * nm1;
   for (int e = tid; e < cnt3; e += bd) {
-    const int pair = e / f.Pe, pa_l = e - pair * f.Pe;
-    const int pb = pair / f.nm1, pci = pair - pb * f.nm1;
     const int pc = pci + (pci >= pb);
     const int pa = f.pa0 + pa_l;
-    if (pa == pb || pa == pc) continue;
-    const int lo = min(pb, pc), hi = max(pb, pc);
-    const int col = pa - (pa > lo) - (pa > hi);
-    const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
-                     (size_t)f.a * f.nm2 + col;
-    fn(2, pa_l, pb, pc, g, base3 + e);
+    if (pa != pb && pa != pc) {
+      const int lo = min(pb, pc), hi = max(pb, pc);
+      const int col = pa - (pa > lo) - (pa > hi);
+      const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
+                       (size_t)f.a * nm2 + col;
+      fn(2, pa_l, pb, pc, g, base3 + e);
+    }
+    pa_l += dpl;
+    int inc = dpr;
+    if (pa_l >= Pe) {
+      pa_l -= Pe;
+      ++inc;
+    }
+    pci += inc;
+    while (pci >= nm1) {
+      pci -= nm1;
+      ++pb;
+    }
   }
 }
 
@@ -357,7 +387,7 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
     if (lane == 0) {
       if (P.values) P.values[t] = value;
       if (P.theta_ref && value < dsub(P.theta_ref[t], 1e-7)) {  // rlt2.cpp:332-335
-        atomicMin(P.err_tile, t);
+        atomicMin(P.err_tile, P.tile_base + t);
         if (P.stop_w) atomicExch(P.stop_w, 1);
       }
     }
@@ -545,11 +575,11 @@ cudaError_t launch_xyfold(const XYFoldParams& p, int tiles, cudaStream_t st) {
 }
 
 int fold_chunk(int m) {
-  // largest pa-chunk whose CTA plan fits ~52 KB (4 CTAs / SM), at least 1
+  // largest pa-chunk whose CTA plan fits ~96 KB (2 CTAs / SM), at least 1
   int best = 1;
   for (int c = 1; c <= m; ++c) {
     const FoldSmem L(m, c);
-    if (L.total(m, c) * sizeof(double) <= 52 * 1024) best = c;
+    if (L.total(m, c) * sizeof(double) <= 96 * 1024) best = c;
   }
   const char* e = std::getenv("QAPB_FOLD_CHUNK");
   if (e && *e) best = std::max(1, std::min(m, std::atoi(e)));
@@ -577,12 +607,8 @@ cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-namespace {
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return (v && *v) ? std::atoi(v) : dflt;
-}
 
+namespace {
 template <int CPL>
 cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const int m = p.m;

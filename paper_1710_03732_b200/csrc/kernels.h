@@ -36,12 +36,13 @@ struct BatchLapParams {
   double *u, *v;        // optional
   const double* theta_ref;  // optional: phase-2 regression check (rlt2.cpp:332-335)
   int* err_tile;
+  int tile_base;            // global index of tile 0 of this launch (error reports)
 };
 
 struct FoldParams {
   int m;
-  const int* triples;  // (a,b,c) a<b<c, 3 ints each
-  int ntriples, chunk, nchunks;
+  const int* triples;  // (a,b,c) a<b<c, 3 ints each, lexicographic
+  int ntriples, chunk, nchunks;  // triples of this launch start at `triples`
   double kz, phi;
   int fast;
   double* d;           // D' (store)

@@ -62,27 +62,39 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
       L.p[0] = i;
       L.w[0] = 0.0;
     }
-    bool used = false;
+    bool used = !real;  // padding lanes (and the virtual column m) never relax
     int j0 = m, i0 = i;
     double ui0 = 0.0;
-    while (true) {  // lap.cpp:40-67
-      used = used || (lane == j0);
+    // every step uses one more column, so a row takes at most m steps; more
+    // means non-finite costs (the reference is undefined there too): stop
+    for (int guard = 0;; ++guard) {  // lap.cpp:40-67
+      if (guard > m) {  // leave a valid permutation behind for the writers
+        L.p[0] = real ? lane : -1;
+        L.w[0] = L.v[0] = __longlong_as_double(0x7ff8000000000000ll);
+        return L.w[0];
+      }
+      // a used column's minv is never read again in this row (lap.cpp:47,58-64):
+      // park it at +inf so the order key needs no activity mask
+      if (lane == j0) {
+        used = true;
+        minv = INF;
+      }
       const double cur = dsub(dsub(colp[i0 * m], ui0), L.v[0]);  // lap.cpp:48
-      const bool act = real && !used;
-      const bool upd = act && (cur < minv);
-      minv = upd ? cur : minv;
-      way = upd ? j0 : way;
-      const unsigned long long k = ordkey(minv);
-      const unsigned hi = act ? (unsigned)(k >> 32) : 0xffffffffu;
-      const unsigned lo = act ? (unsigned)k : 0xffffffffu;
+      if (!used && cur < minv) {                                  // lap.cpp:49-52
+        minv = cur;
+        way = j0;
+      }
+      const unsigned long long k = ordkey(minv);  // +inf for used / padding lanes
+      const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
       const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
       const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
-      const int j1 = __ffs(__ballot_sync(QAPB_FULL, act && hi == hmin && lo == lmin)) - 1;
+      const int j1 = (__ffs(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin)) - 1) & 31;
       const double delta = __shfl_sync(QAPB_FULL, minv, j1);
-      minv = dsub(minv, delta);  // lap.cpp:63 (dead for used columns)
-      const double wn = dadd(L.w[0], delta), vn = dsub(L.v[0], delta);
-      L.w[0] = used ? wn : L.w[0];  // lap.cpp:60-61
-      L.v[0] = used ? vn : L.v[0];
+      minv = dsub(minv, delta);  // lap.cpp:63 (inf stays inf for used lanes)
+      if (used) {                // lap.cpp:60-61
+        L.w[0] = dadd(L.w[0], delta);
+        L.v[0] = dsub(L.v[0], delta);
+      }
       j0 = j1;
       const int pj = __shfl_sync(QAPB_FULL, L.p[0], j1);
       const double wj = __shfl_sync(QAPB_FULL, L.w[0], j1);
@@ -90,7 +102,7 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
       i0 = pj;
       ui0 = wj;
     }
-    while (j0 != m) {  // augment, lap.cpp:68-72
+    for (int g2 = 0; j0 != m && g2 <= m; ++g2) {  // augment, lap.cpp:68-72
       const int jw = __shfl_sync(QAPB_FULL, way, j0);
       const int pw = __shfl_sync(QAPB_FULL, L.p[0], jw);
       const double ww = __shfl_sync(QAPB_FULL, L.w[0], jw);
@@ -138,7 +150,15 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
     unsigned used = 0;
     int j0 = m, i0 = i;
     double ui0 = 0.0;
-    while (true) {  // Dijkstra step, lap.cpp:40-67
+    for (int guard = 0;; ++guard) {  // Dijkstra step, lap.cpp:40-67
+      if (guard > m) {  // non-finite input: leave a valid permutation behind
+#pragma unroll
+        for (int s = 0; s < CPL; ++s) {
+          L.p[s] = (s * 32 + lane < m) ? s * 32 + lane : -1;
+          L.w[s] = L.v[s] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+        return L.w[0];
+      }
       if ((j0 & 31) == lane) used |= 1u << (j0 >> 5);
       const double* row = cost + (size_t)i0 * m;
       unsigned long long bkey = ~0ull;
@@ -192,7 +212,7 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
       i0 = pj;
       ui0 = wj;
     }
-    while (j0 != m) {  // augment, lap.cpp:68-72
+    for (int g2 = 0; j0 != m && g2 <= m; ++g2) {  // augment, lap.cpp:68-72
       const int s0 = j0 >> 5, l0 = j0 & 31;
       const int jw = __shfl_sync(QAPB_FULL, pick<CPL>(way, s0), l0);
       const int sw = jw >> 5, lw = jw & 31;

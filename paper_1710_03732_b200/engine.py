@@ -65,6 +65,7 @@ lib.qapb_engine_stream.argtypes = [_vp, _P(_vp)]
 lib.qapb_engine_set_profiling.argtypes = [_vp, C.c_int]
 lib.qapb_engine_kernel_times.argtypes = [_vp, _vp, _vp, C.c_int]
 lib.qapb_engine_history.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
+lib.qapb_engine_time_kernel.argtypes = [_vp, C.c_int, C.c_int, _P(C.c_double)]
 
 KERNEL_NAMES = ["xyfold", "zfold", "zlap", "phase2", "ystage", "xstage"]
 
@@ -458,6 +459,12 @@ class AscentEngine:
         b, best = np.empty(count), np.empty(count)
         _check(lib.qapb_engine_history(self._h, start, count, dptr(b), dptr(best)))
         return b, best
+
+    def time_kernel(self, kind: str, reps: int = 5) -> float:
+        """Tuning only: mean ms of one kernel kind; destroys the numerical state."""
+        ms = C.c_double()
+        _check(lib.qapb_engine_time_kernel(self._h, KERNEL_NAMES.index(kind), reps, C.byref(ms)))
+        return ms.value
 
     def launch_count(self) -> int:
         n = C.c_longlong()
