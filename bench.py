@@ -9,9 +9,11 @@ SA off.  A "step" is one steady-state dual-ascent iteration (ascent update ->
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N>1) every rank runs an independent replica engine on its own
-GPU ("replicas only" in round 1); value is all ranks'
-iterations / max-over-ranks device time.  `--impl reference` times the
+Under torchrun (N>1) the ranks run ONE z-sharded engine (each
+rank owns a first-facility range of the half-Z tiles; sigma/gain of the cross-
+shard family members move by NCCL send/recv each iteration); value is that
+problem's iterations / max-over-ranks device time ("scaling": "strong").
+`--replicas` instead runs N independent engines ("weak").  `--impl reference` times the
 reference's own CPU implementation (oracle/_ref, compiled from the unmodified
 reference sources) on the host cores, rank 0 only.
 """
@@ -192,13 +194,15 @@ def run_reference_arm(args):
     return 0
 
 
-def config_block(args, world):
+def config_block(args, world, sharded=False):
     s = sizes(args.n)
     return {"workload": f"nug{args.n}-shaped (Manhattan grid, flows U{{0..10}} seed 1), "
                         f"variant {args.variant}, SA off, steady-state iterations",
             "n": args.n, "variant": args.variant, "z_laps_per_iteration": s["tiles"],
             "laps_per_iteration": s["tiles"] + args.n * args.n + 1,
-            "z_cells": s["n_z"], "parallelism": f"replica{world}" if world > 1 else "single",
+            "z_cells": s["n_z"],
+            "parallelism": (f"zshard{world}" if sharded else f"replica{world}") if world > 1
+            else "single",
             "l2": "no flush: z arrays (3 x %.2f GB) exceed the 126 MB L2" % (s["n_z"] * 8 / 1e9)}
 
 
@@ -212,13 +216,19 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    sharded = world > 1 and not args.replicas
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
     inst = workload(args.n)
     cfg = q.AscentConfig(variant=args.variant, iter_limit=10 ** 6, record_history=False,
                          device=local)
-    eng = q.AscentEngine.from_instance(inst, cfg)
+    if sharded:
+        idobj = [q.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(idobj, src=0)
+        eng = q.AscentEngine.from_instance_sharded(inst, cfg, rank, world, idobj[0])
+    else:
+        eng = q.AscentEngine.from_instance(inst, cfg)
     eng.enqueue(args.warmup)
     eng.synchronize()
     stream = torch.cuda.ExternalStream(eng.stream(), device=local)
@@ -259,15 +269,9 @@ def run_ours(args):
     final_bound = float(eng.history(eng.iteration() - 1, 1)[0][0])
     eng.close()
 
-    if world > 1:
-        torch.distributed.barrier()
-    if rank != 0:
-        torch.distributed.destroy_process_group()
-        return 0
-
     s = sizes(args.n)
     laps = s["tiles"] + args.n * args.n + 1
-    its = world * args.steps / (ms / 1000.0)
+    its = (1 if sharded else world) * args.steps / (ms / 1000.0)
     peak, peak_src = peaks()
     kb = kernel_bytes(args.n, args.variant)
     kernels = {}
@@ -289,17 +293,35 @@ def run_ours(args):
                 "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_launch": kb[dom]}
     ib = iteration_bytes(args.n)
-    iteration_roofline = {"alg_bytes": ib, "achieved_gbs": ib * (its / world) / 1e9,
-                          "frac": ib * (its / world) / 1e9 / peak,
+    per_gpu_its = its / world if not sharded else its  # sharded: bytes split over world GPUs
+    agg_peak = peak * (world if sharded else 1)
+    iteration_roofline = {"alg_bytes": ib, "achieved_gbs": ib * per_gpu_its / 1e9,
+                          "frac": ib * per_gpu_its / 1e9 / agg_peak,
                           "note": "SURVEY.md §8(d) B=32Nz+32Ny+16tiles per 1-phase iteration"}
 
     # e2e: the user's call (run_ascent through the C-ABI, host instance in,
     # host report out), 100 iterations = the reference's default iter_limit
     e2e_iters = 100
-    q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=2))  # warm context
-    t0 = time.perf_counter()
-    rep = q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters))
-    e2e_s = time.perf_counter() - t0
+    if sharded:  # every rank runs its shard of the same run_ascent-equivalent call
+        idobj = [q.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(idobj, src=0)
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        e = q.AscentEngine.from_instance_sharded(
+            inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters, device=local), rank,
+            world, idobj[0])
+        rep = e.run()
+        e.close()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    else:
+        q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=2))  # warm context
+        t0 = time.perf_counter()
+        rep = q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters))
+        e2e_s = time.perf_counter() - t0
     rec_bytes = ctypes.sizeof(q.abi.Record)
     e2e = {"value": rep.iterations / e2e_s, "unit": "iterations/s",
            "h2d_bytes_per_step": 3 * args.n * args.n * 8 / rep.iterations,
@@ -308,6 +330,9 @@ def run_ours(args):
                    "100 iterations, report + records to host",
            "seconds": e2e_s, "final_bound": rep.best_bound}
 
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return 0
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -322,8 +347,9 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": its, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "laps_per_s": its * laps, "config": config_block(args, world),
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "laps_per_s": its * laps, "config": config_block(args, world, sharded),
         "roofline": roofline, "iteration_roofline": iteration_roofline, "kernels": kernels,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         "parity": parity, "bound_after": final_bound,
@@ -343,6 +369,8 @@ def main():
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--variant", default="F1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent engines instead of one z-sharded engine")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.impl == "reference":

@@ -244,6 +244,32 @@ QAPB_API qapb_status qapb_engine_history(qapb_engine* e, int from, int count,
 QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms,
                                               long long* launches, int reset);
 
+/* ---- multi-GPU: one process per GPU, z state sharded -----
+ * Rank r owns the facility pairs (a, b>a) with a in [a_bounds[r],
+ * a_bounds[r+1]) -- a contiguous range of half-Z tiles -- and folds the
+ * triples whose first facility it owns.  In a family (a<b<c) the X3 member
+ * T(b,c)[a] belongs to owner(b): each iteration owner(b) sends
+ * sigma = kz*pi + push of those cells to owner(a) and receives their gain
+ * back (NCCL grouped send/recv); theta is re-assembled with broadcasts and
+ * the O(n^4) Y/X stages run replicated, so every rank holds the same bound.
+ * Results are bitwise those of the single-GPU engine. */
+/* Facility ranges per rank (a_bounds has world+1 entries), balanced over the
+ * fold and Z-LAP work of each first facility. */
+QAPB_API qapb_status qapb_shard_plan(int n, int world, int* a_bounds);
+/* Doubles rank `rank` sends (send[p]) to / receives (recv[p]) from every
+ * peer p in ONE of the two per-iteration exchanges (both exchanges move the
+ * same amounts in opposite directions). */
+QAPB_API qapb_status qapb_shard_exchange_counts(int n, int world, int rank,
+                                                long long* send, long long* recv);
+QAPB_API qapb_status qapb_nccl_unique_id(unsigned char id[128]);
+/* AscentEngine(init_coefficients(inst), cfg) on rank `rank` of `world`;
+ * every rank passes the same instance, cfg and NCCL unique id, and the
+ * device cfg->device.  F1 and S1 variants. */
+QAPB_API qapb_status qapb_engine_create_instance_sharded(
+    int n, const double* flow, const double* dist, const double* linear,
+    const qapb_config* cfg, int rank, int world, const unsigned char nccl_id[128],
+    qapb_engine** out);
+
 /* run_ascent(inst, cfg), rlt2.cpp:590-597: instance in, report out.  The
  * certificate value is re-evaluated on the instance as the reference does. */
 QAPB_API qapb_status qapb_run_ascent(int n, const double* flow,

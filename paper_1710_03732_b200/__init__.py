@@ -21,4 +21,5 @@ from .engine import (AscentConfig, AscentEngine, BoundReport, CoefficientStore, 
                      IterationRecord, LapBatch, LapResult, QapbError, collapse_store,
                      init_coefficients, lib, library_path, redistribute_family, run_ascent,
                      run_ascent_warm, solve_batch, solve_batch_device, solve_batch_serial,
-                     solve_lap, store_evaluate, variant_name, parse_variant)
+                     solve_lap, store_evaluate, variant_name, parse_variant, shard_plan,
+                     shard_exchange_counts, nccl_unique_id)

@@ -17,6 +17,12 @@
 using qapb::CudaError;
 using qapb::Engine;
 
+namespace qapb {
+std::vector<int> shard_plan(int n, int world);
+void shard_counts(int n, const std::vector<int>& ab, int rank, std::vector<long long>& send,
+                  std::vector<long long>& recv);
+}  // namespace qapb
+
 struct qapb_engine {
   std::unique_ptr<Engine> e;
 };
@@ -503,6 +509,52 @@ QAPB_API qapb_status qapb_engine_history(qapb_engine* e, int from, int count, do
 QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms, long long* launches,
                                               int reset) {
   return guard([&] { e->e->kernel_times(ms, launches, reset != 0); });
+}
+
+QAPB_API qapb_status qapb_shard_plan(int n, int world, int* a_bounds) {
+  return guard([&] {
+    need(n >= 3, "shard_plan: n >= 3 required");
+    auto b = qapb::shard_plan(n, world);
+    std::copy(b.begin(), b.end(), a_bounds);
+  });
+}
+
+QAPB_API qapb_status qapb_shard_exchange_counts(int n, int world, int rank, long long* send,
+                                                long long* recv) {
+  return guard([&] {
+    need(n >= 3, "shard_plan: n >= 3 required");
+    need(rank >= 0 && rank < world, "bad rank");
+    std::vector<long long> s, r;
+    qapb::shard_counts(n, qapb::shard_plan(n, world), rank, s, r);
+    std::copy(s.begin(), s.end(), send);
+    std::copy(r.begin(), r.end(), recv);
+  });
+}
+
+QAPB_API qapb_status qapb_nccl_unique_id(unsigned char id[128]) {
+  return guard([&] {
+    ncclUniqueId u;
+    const ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) throw CudaError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(u) == 128, "NCCL unique id size");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+QAPB_API qapb_status qapb_engine_create_instance_sharded(int n, const double* flow,
+                                                         const double* dist, const double* linear,
+                                                         const qapb_config* cfg, int rank,
+                                                         int world,
+                                                         const unsigned char nccl_id[128],
+                                                         qapb_engine** out) {
+  return guard([&] {
+    qapb_config c0;
+    qapb_config_init(&c0);
+    auto h = std::make_unique<qapb_engine>();
+    h->e = std::make_unique<Engine>(n, flow, dist, linear, cfg ? *cfg : c0, rank, world,
+                                    nccl_id);
+    *out = h.release();
+  });
 }
 
 QAPB_API qapb_status qapb_run_ascent(int n, const double* flow, const double* dist,

@@ -10,6 +10,54 @@
 
 namespace qapb {
 
+std::vector<int> shard_plan(int n, int world) {
+  // contiguous first-facility ranges; a facility's work = its share of the
+  // fold (triples a<b<c: C(n-1-a,2)) and of the Z-LAPs (pairs: n-1-a),
+  // weighted by their measured split of an n=30 iteration (0.55 / 0.45)
+  const int F = n - 1;  // first facilities 0..n-2 own pairs
+  if (world < 1 || world > F) throw std::invalid_argument("shard_plan: bad world size");
+  auto c2 = [](double x) { return x >= 2 ? x * (x - 1) / 2 : 0.0; };
+  const double tri = std::max(1.0, c2(n) * (n - 2) / 3.0), pairs = std::max(1.0, c2(n));
+  std::vector<double> pre(F + 1, 0.0);
+  for (int a = 0; a < F; ++a)
+    pre[a + 1] = pre[a] + 0.55 * c2(n - 1 - a) / tri + 0.45 * (n - 1 - a) / pairs;
+  const double INF = std::numeric_limits<double>::infinity();
+  std::vector<std::vector<double>> f(world + 1, std::vector<double>(F + 1, INF));
+  std::vector<std::vector<int>> arg(world + 1, std::vector<int>(F + 1, -1));
+  f[0][0] = 0;
+  for (int k = 1; k <= world; ++k)
+    for (int i = k; i <= F; ++i)
+      for (int j = k - 1; j < i; ++j) {
+        const double v = std::max(f[k - 1][j], pre[i] - pre[j]);
+        if (v < f[k][i]) {
+          f[k][i] = v;
+          arg[k][i] = j;
+        }
+      }
+  std::vector<int> b(world + 1);
+  b[world] = F;
+  for (int k = world, i = F; k > 0; --k) {
+    i = arg[k][i];
+    b[k - 1] = i;
+  }
+  return b;
+}
+
+void shard_counts(int n, const std::vector<int>& ab, int rank, std::vector<long long>& send,
+                  std::vector<long long>& recv) {
+  const int world = (int)ab.size() - 1;
+  const long long lp = (long long)n * (n - 1), nm2 = n - 2;
+  auto fpf = [&](int i) { return (long long)i * n - (long long)i * (i + 1) / 2; };
+  auto tiles = [&](int r) { return (fpf(ab[r + 1]) - fpf(ab[r])) * lp; };
+  auto rows = [&](int r) { return (long long)(ab[r + 1] - ab[r]); };
+  send.assign(world, 0);
+  recv.assign(world, 0);
+  for (int p = 0; p < world; ++p) {
+    if (p < rank) send[p] = tiles(rank) * rows(p) * nm2;  // sigma of my rows a in p's range
+    if (p > rank) recv[p] = tiles(p) * rows(rank) * nm2;
+  }
+}
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
@@ -46,6 +94,7 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
   if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");  // rlt2.cpp:209
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
   alloc();
+  setup_shards(nullptr);
   init_state();
   cuda_check(cudaMemcpyAsync(b_, b, nb_ * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D b");
   cuda_check(cudaMemcpyAsync(c_, c, nc_ * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D c");
@@ -60,11 +109,18 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
 }
 
 Engine::Engine(int n, const double* flow, const double* dist, const double* linear,
-               const qapb_config& cfg)
-    : m_(n), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
+               const qapb_config& cfg, int rank, int world, const unsigned char* nccl_id)
+    : rank_(rank), world_(world), m_(n), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
   if (n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
+  if (world_ < 1 || world_ > kMaxRanks || rank_ < 0 || rank_ >= world_)
+    throw std::invalid_argument("AscentEngine: bad rank/world");
+  if (world_ > 1 && (is_two_phase() || cfg.sa_enabled))
+    throw std::invalid_argument("sharded engine: F1/S1 without SA only (round 1)");
+  if (world_ > std::max(1, n - 2))
+    throw std::invalid_argument("sharded engine: more ranks than first facilities");
   alloc();
+  setup_shards(nccl_id);
   init_state();
   double *df = nullptr, *dd = nullptr, *dl = nullptr;
   const size_t nn = (size_t)n * n;
@@ -182,6 +238,10 @@ Engine::~Engine() {
   dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
   dfree(fpair_ij_); dfree(counter_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
   if (hSpin_) cudaFreeHost(hSpin_);
+  for (auto* p : xbufs_) cudaFree(p);
+  if (shard_dev_) cudaFree(shard_dev_);
+  if (feas_bad_) cudaFree(feas_bad_);
+  if (comm_) ncclCommDestroy(comm_);
   for (auto e : stage_ev_) cudaEventDestroy(e);
   if (join_ev_) cudaEventDestroy(join_ev_);
   if (st2_) cudaStreamDestroy(st2_);
@@ -223,6 +283,121 @@ void Engine::pull_scalars() {
              "D2H scalars");
   cuda_check(cudaStreamSynchronize(st_), "iteration");
   hS_ = *hSpin_;
+}
+
+void Engine::nccl_check(ncclResult_t r, const char* what) const {
+  if (r != ncclSuccess)
+    throw CudaError(std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+}
+
+void Engine::setup_shards(const unsigned char* nccl_id) {
+  const int m = m_;
+  std::vector<int> ab = world_ > 1 ? shard_plan(m, world_) : std::vector<int>{0, m - 1};
+  auto fpf = [&](int i) { return i * m - i * (i + 1) / 2; };
+  auto c2 = [](int x) { return x >= 2 ? x * (x - 1) / 2 : 0; };
+  auto tri_before = [&](int a) {
+    int t = 0;
+    for (int x = 0; x < a; ++x) t += c2(m - 1 - x);
+    return t;
+  };
+  shard_ = ShardInfo{};
+  shard_.world = world_;
+  shard_.rank = rank_;
+  for (int r = 0; r <= world_; ++r) {
+    shard_.abound[r] = ab[r];
+    shard_.tbase[r] = fpf(ab[r]) * lpairs_;
+  }
+  t_lo_ = shard_.tbase[rank_];
+  t_hi_ = shard_.tbase[rank_ + 1];
+  tri_lo_ = tri_before(ab[rank_]);
+  tri_hi_ = tri_before(ab[rank_ + 1]);
+  dalloc(&feas_bad_, 1);
+  if (world_ == 1) return;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof id);
+  nccl_check(ncclCommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
+  std::vector<long long> send, recv;
+  shard_counts(m, ab, rank_, send, recv);
+  xcount_.assign(2 * world_, 0);
+  for (int p = 0; p < world_; ++p) {
+    if (send[p]) {  // lower peer: sigma out, gain in
+      double *a = nullptr, *b = nullptr;
+      dalloc(&a, send[p]);
+      dalloc(&b, send[p]);
+      xbufs_.push_back(a);
+      xbufs_.push_back(b);
+      shard_.sig_send[p] = a;
+      shard_.gain_recv[p] = b;
+      xcount_[p] = send[p];
+    }
+    if (recv[p]) {  // higher peer: sigma in, gain out
+      double *a = nullptr, *b = nullptr;
+      dalloc(&a, recv[p]);
+      dalloc(&b, recv[p]);
+      xbufs_.push_back(a);
+      xbufs_.push_back(b);
+      shard_.sig_recv[p] = a;
+      shard_.gain_send[p] = b;
+      xcount_[world_ + p] = recv[p];
+    }
+  }
+  dalloc(&shard_dev_, 1);
+  cuda_check(cudaMemcpy(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice), "H2D shard");
+}
+
+// Steady sharded Z stage: sigma out -> fold (owned triples) -> gain back ->
+// X3 update -> Z-LAPs of owned tiles -> theta re-assembled on every rank.
+void Engine::enqueue_sharded_z(int it) {
+  const bool fast = is_fast();
+  double* costs = (fast && it > 0) ? incz_ : d_;
+  const int S = (int)stage_ev_.size();
+  cuda_check(cudaMemsetAsync(counter_, 0, (S + 2) * sizeof(int), st_), "memset counters");
+  if (it > 0) {
+    kbegin(QAPB_K_ZFOLD, st_);
+    cuda_check(launch_sigma_pack(m_, piz_, push_, cfg_.kappa_z_upper, shard_, &S_->stop, st_),
+               "sigma pack");
+    nccl_check(ncclGroupStart(), "group");
+    for (int p = 0; p < world_; ++p) {
+      if (xcount_[p])
+        nccl_check(ncclSend(shard_.sig_send[p], xcount_[p], ncclDouble, p, comm_, st_), "send");
+      if (xcount_[world_ + p])
+        nccl_check(ncclRecv(const_cast<double*>(shard_.sig_recv[p]), xcount_[world_ + p],
+                            ncclDouble, p, comm_, st_),
+                   "recv");
+    }
+    nccl_check(ncclGroupEnd(), "group");
+    FoldParams f = fold_params(-1);
+    f.triples = triples_ + 3 * (size_t)tri_lo_;
+    f.ntriples = tri_hi_ - tri_lo_;
+    f.shard = shard_dev_;
+    cuda_check(launch_zfold(f, st_), "z-fold");
+    nccl_check(ncclGroupStart(), "group");
+    for (int p = 0; p < world_; ++p) {
+      if (xcount_[world_ + p])
+        nccl_check(ncclSend(shard_.gain_send[p], xcount_[world_ + p], ncclDouble, p, comm_, st_),
+                   "send");
+      if (xcount_[p])
+        nccl_check(ncclRecv(const_cast<double*>(shard_.gain_recv[p]), xcount_[p], ncclDouble, p,
+                            comm_, st_),
+                   "recv");
+    }
+    nccl_check(ncclGroupEnd(), "group");
+    cuda_check(launch_x3_update(m_, d_, incz_, piz_, cfg_.kappa_z_upper, fast, shard_, &S_->stop,
+                                st_),
+               "x3 update");
+    kend(st_);
+    launches_ += 3;
+  }
+  enqueue_zlap(costs, t_lo_, t_hi_ - t_lo_, theta_, nullptr, S, st_);
+  nccl_check(ncclGroupStart(), "group");
+  for (int r = 0; r < world_; ++r) {
+    const int c = shard_.tbase[r + 1] - shard_.tbase[r];
+    if (c)
+      nccl_check(ncclBroadcast(theta_ + shard_.tbase[r], theta_ + shard_.tbase[r], c, ncclDouble,
+                               r, comm_, st_),
+                 "theta broadcast");
+  }
+  nccl_check(ncclGroupEnd(), "group");
 }
 
 void Engine::plan_pipeline() {
@@ -353,8 +528,8 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     launches_ += graph_launches_;
     return;
   }
-  const bool capture =
-      steady && it >= 2 && !graph_ && !profiling_ && !env_flag("QAPB_NO_GRAPH");
+  const bool capture = steady && it >= 2 && !graph_ && !profiling_ && world_ == 1 &&
+                       !env_flag("QAPB_NO_GRAPH");
   cudaGraph_t g = nullptr;
   const long long l0 = launches_;
   if (capture)
@@ -381,7 +556,10 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     kend(st_);
     ++launches_;
   }
-  enqueue_stage_z(it);
+  if (world_ > 1)
+    enqueue_sharded_z(it);
+  else
+    enqueue_stage_z(it);
   YStageParams y{};
   y.m = m_;
   y.c = c_;
@@ -417,10 +595,16 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   xs.es_delta = cfg_.early_stop_delta;
   xs.es_window = cfg_.early_stop_window;
   xs.iter_limit = cfg_.iter_limit;
+  xs.feas_bad = feas_bad_;
+  xs.zt_lo = t_lo_;
+  xs.zt_hi = t_hi_;
   kbegin(QAPB_K_XSTAGE, st_);
   cuda_check(launch_xstage(xs, st_), "x-stage");
+  if (world_ > 1)  // feasibility needs every rank's pi(z) tiles
+    nccl_check(ncclAllReduce(feas_bad_, feas_bad_, 1, ncclInt, ncclMax, comm_, st_), "allreduce");
+  cuda_check(launch_xfinish(xs, st_), "x-finish");
   kend(st_);
-  ++launches_;
+  launches_ += 2;
   if (capture) {
     cuda_check(cudaStreamEndCapture(st_, &g), "end capture");
     cuda_check(cudaGraphInstantiate(&graph_, g, 0), "graph instantiate");

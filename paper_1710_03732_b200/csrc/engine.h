@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <random>
 #include <stdexcept>
@@ -34,7 +35,8 @@ class Engine {
          const qapb_config& cfg);
   // AscentEngine(init_coefficients(inst), cfg): store built on the device.
   Engine(int n, const double* flow, const double* dist, const double* linear,
-         const qapb_config& cfg);
+         const qapb_config& cfg, int rank = 0, int world = 1,
+         const unsigned char* nccl_id = nullptr);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -104,6 +106,19 @@ class Engine {
   double kms_[QAPB_K_COUNT] = {0};
   long long kcnt_[QAPB_K_COUNT] = {0};
   std::vector<double> stage_ms_;  // per iteration: z, y, x
+
+  // multi-GPU: facility-range ownership + NCCL exchanges
+  int rank_ = 0, world_ = 1;
+  ncclComm_t comm_ = nullptr;
+  ShardInfo shard_{};
+  ShardInfo* shard_dev_ = nullptr;
+  std::vector<double*> xbufs_;  // all exchange buffers (owned)
+  std::vector<long long> xcount_;  // doubles per peer in one exchange
+  int* feas_bad_ = nullptr;
+  int t_lo_ = 0, t_hi_ = 0, tri_lo_ = 0, tri_hi_ = 0;
+  void setup_shards(const unsigned char* nccl_id);
+  void enqueue_sharded_z(int it);
+  void nccl_check(ncclResult_t r, const char* what) const;
 
   int m_, dev_;
   qapb_config cfg_;

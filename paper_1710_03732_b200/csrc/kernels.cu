@@ -115,6 +115,11 @@ struct FamilyCtx {
   int n, nm1, nm2, a, b, c, pa0, Pe, fab, fac, fbc;
   size_t esz;
   int lpairs;
+  // multi-GPU: X3 = T(b,c)[a] lives on rank xr != this rank
+  int xr;                 // -1 when local
+  const double* xsig;     // sigma of the X3 cells, (tile - tbase[xr]) * rows * nm2 + ...
+  double* xgain;          // gain of the X3 cells, same index
+  int xrows, xa0, xtb;    // rows per tile (my facility count), my first facility, tbase[xr]
 };
 
 __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
@@ -134,7 +139,29 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
   f.fbc = ix.fpair(f.b, f.c);
   f.esz = (size_t)ix.esz;
   f.lpairs = ix.lpairs;
+  f.xr = -1;
+  f.xsig = nullptr;
+  f.xgain = nullptr;
+  f.xrows = f.xa0 = f.xtb = 0;
+  if (P.shard) {
+    const ShardInfo& sh = *P.shard;
+    int r = sh.world - 1;
+    while (r > 0 && f.b < sh.abound[r]) --r;
+    if (r != sh.rank) {
+      f.xr = r;
+      f.xsig = sh.sig_recv[r];
+      f.xgain = sh.gain_send[r];
+      f.xrows = sh.abound[sh.rank + 1] - sh.abound[sh.rank];
+      f.xa0 = sh.abound[sh.rank];
+      f.xtb = sh.tbase[r];
+    }
+  }
   return f;
+}
+
+// exchange-buffer index of X3 cell (tile t, row a, column col) on a remote rank
+__device__ __forceinline__ size_t x3_xindex(const FamilyCtx& f, size_t tile, int col) {
+  return ((tile - (size_t)f.xtb) * f.xrows + (size_t)(f.a - f.xa0)) * f.nm2 + col;
 }
 
 // Visit every member cell of the CTA's families: fn(member, pa_l, pb, pc, g, slot)
@@ -193,8 +220,9 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
     if (pa != pb && pa != pc) {
       const int lo = min(pb, pc), hi = max(pb, pc);
       const int col = pa - (pa > lo) - (pa > hi);
-      const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
-                       (size_t)f.a * nm2 + col;
+      const size_t tile = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc));
+      // local: offset in the z arrays; remote: index in the exchange buffers
+      const size_t g = f.xr < 0 ? tile * f.esz + (size_t)f.a * nm2 + col : x3_xindex(f, tile, col);
       fn(2, pa_l, pb, pc, g, base3 + e);
     }
     pa_l += dpl;
@@ -236,7 +264,12 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
   double* S = sm + L.pi_off();
   double* V = sm + L.val_off();
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
-    cp_async8(S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc, piz + g);
+    double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
+    if (mem == 2 && f.xr >= 0) {  // remote X3: its owner sent sigma (kz*pi + push)
+      cp_async8(sp, f.xsig + g);
+      return;
+    }
+    cp_async8(sp, piz + g);
     cp_async8(V + slot, vals + g);
   });
 }
@@ -272,12 +305,13 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   double* __restrict__ d = P.d;
   double* __restrict__ incz = P.incz;
   const int fast = P.fast;
+  const bool remote3 = f.xr >= 0;
   for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
     const int fi = (pa_l * n + pb) * L.np + pc;
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
     const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
-    const double s3 = dadd(dmul(kz, p3), U3[pb * n + pc]);
+    const double s3 = remote3 ? p3 : dadd(dmul(kz, p3), U3[pb * n + pc]);
     double own, gain;  // partners in ascending member order (B, C of rlt2.cpp:280-288)
     if (mem == 0) {
       own = p1;
@@ -288,6 +322,10 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
     } else {
       own = p3;
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
+    }
+    if (mem == 2 && remote3) {  // the X3 owner applies it (x3_update_kernel)
+      f.xgain[g] = gain;
+      return;
     }
     d[g] = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
     if (fast) incz[g] = dadd(dmul(omk, own), gain);   // rlt2.cpp:293
@@ -449,8 +487,9 @@ __global__ void __launch_bounds__(128) ystage_kernel(YStageParams P, int warps_p
 }
 
 // ---------------------------------------------------------------------------
-// X stage + bound (rlt2.cpp:428-449), feasibility (rlt2.cpp:453-473) and the
-// device-loop bookkeeping / termination tests of run() (rlt2.cpp:552-577).
+// X stage + bound (rlt2.cpp:428-449) and the feasibility test
+// (rlt2.cpp:453-473) over the pi(z) tiles this rank holds; the flag is
+// all-reduced across ranks before xfinish_kernel.
 template <int CPL>
 __global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
   DevScalars* S = P.S;
@@ -488,8 +527,7 @@ __global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
     }
   }
   __syncthreads();
-  const int had_cert = S->has_cert;
-  if (!had_cert) {  // rlt2.cpp:453-469
+  if (!S->has_cert) {  // rlt2.cpp:453-469
     const DIdx ix(m);
     const double tol = 1e-7;
     for (int e = tid; e < m * m; e += blockDim.x) {
@@ -501,15 +539,27 @@ __global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
       const int i = e / (m * m), rem = e - i * m * m, j = rem / m, k = rem - j * m;
       if (!(i < j) || k == i || k == j) continue;
       const int t = ix.tile(i, j, sx[i], sx[j]);
+      if (t < P.zt_lo || t >= P.zt_hi) continue;
       if (P.piz[(size_t)t * esz + ix.cell(i, j, sx[i], sx[j], k, sx[k])] > tol) feas_bad = 1;
     }
   }
   __syncthreads();
-  if (!had_cert && !feas_bad) {
-    for (int e = tid; e < m; e += blockDim.x) P.cert[e] = sx[e];
-  }
+  if (tid == 0) *P.feas_bad = feas_bad;
+}
+
+// Certificate (rlt2.cpp:470-472), history, and run()'s termination tests
+// (rlt2.cpp:552-577) evaluated on the device.
+__global__ void xfinish_kernel(XStageParams P) {
+  DevScalars* S = P.S;
+  if (S->stop) return;
+  const int m = P.m, tid = threadIdx.x;
+  const int had_cert = S->has_cert;
+  const int ok = !had_cert && !*P.feas_bad;
+  if (ok)
+    for (int e = tid; e < m; e += blockDim.x) P.cert[e] = P.xrow[e];
+  __syncthreads();
   if (tid == 0) {
-    if (!had_cert && !feas_bad) {  // rlt2.cpp:470-472
+    if (ok) {
       S->has_cert = 1;
       S->cert_val = S->last_bound;
     }
@@ -517,7 +567,7 @@ __global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
     P.hist_bound[it] = S->last_bound;
     P.hist_best[it] = S->best;
     S->iter = it + 1;
-    if (S->run_mode) {  // run() termination, rlt2.cpp:556-577
+    if (S->run_mode) {
       const double best = S->best;
       int term = -1;
       if (S->has_cert) {
@@ -541,6 +591,57 @@ __global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
         S->term = term;
         S->stop = 1;
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU exchange kernels.  For every lower rank A, the rows a in A's
+// facility range of each tile this rank owns are the X3 members of families
+// A folds.  The rows are contiguous ([abound[A], abound[A+1]) x (n-2) doubles
+// per tile), so both kernels stream them in order.
+__global__ void __launch_bounds__(256) sigma_pack_kernel(int m, const double* __restrict__ piz,
+                                                         const double* __restrict__ push,
+                                                         double kz, ShardInfo sh,
+                                                         const int* stop) {
+  if (stop && *stop) return;
+  const int nm2 = m - 2;
+  const size_t esz = (size_t)nm2 * nm2;
+  const int me = sh.rank, T = sh.tbase[me + 1] - sh.tbase[me];
+  for (int A = 0; A < me; ++A) {
+    const int rows = sh.abound[A + 1] - sh.abound[A];
+    const size_t blk = (size_t)rows * nm2, total = (size_t)T * blk;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)gridDim.x * blockDim.x) {
+      const size_t tl = e / blk, rem = e - tl * blk;
+      const size_t t = (size_t)sh.tbase[me] + tl;
+      const size_t g = t * esz + (size_t)sh.abound[A] * nm2 + rem;
+      sh.sig_send[A][e] = dadd(dmul(kz, piz[g]), push[t]);  // sigma, rlt2.cpp:289-290
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) x3_update_kernel(int m, double* __restrict__ d,
+                                                        double* __restrict__ incz,
+                                                        const double* __restrict__ piz,
+                                                        double kz, int fast, ShardInfo sh,
+                                                        const int* stop) {
+  if (stop && *stop) return;
+  const int nm2 = m - 2;
+  const size_t esz = (size_t)nm2 * nm2;
+  const double omk = dsub(1.0, kz);
+  const int me = sh.rank, T = sh.tbase[me + 1] - sh.tbase[me];
+  for (int A = 0; A < me; ++A) {
+    const int rows = sh.abound[A + 1] - sh.abound[A];
+    const size_t blk = (size_t)rows * nm2, total = (size_t)T * blk;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)gridDim.x * blockDim.x) {
+      const size_t tl = e / blk, rem = e - tl * blk;
+      const size_t g = ((size_t)sh.tbase[me] + tl) * esz + (size_t)sh.abound[A] * nm2 + rem;
+      const double gain = sh.gain_recv[A][e];
+      const double own = piz[g];
+      d[g] = dadd(d[g], dsub(gain, dmul(kz, own)));     // rlt2.cpp:292
+      if (fast) incz[g] = dadd(dmul(omk, own), gain);  // rlt2.cpp:293
     }
   }
 }
@@ -592,6 +693,7 @@ size_t fold_smem_bytes(int m, int chunk) {
 }
 
 cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
+  if (p.ntriples <= 0) return cudaSuccess;
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
   cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
@@ -600,6 +702,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st) {
+  if (p.ntriples <= 0) return cudaSuccess;
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
   cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
@@ -692,6 +795,25 @@ cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st) {
     case 3: return launch_xstage_t<3>(p, st);
     default: return launch_xstage_t<4>(p, st);
   }
+}
+
+cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
+  xfinish_kernel<<<1, 64, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
+                              const ShardInfo& sh, const int* stop, cudaStream_t st) {
+  if (sh.rank == 0) return cudaSuccess;
+  sigma_pack_kernel<<<num_sms() * 4, 256, 0, st>>>(m, piz, push, kz, sh, stop);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
+                             int fast, const ShardInfo& sh, const int* stop, cudaStream_t st) {
+  if (sh.rank == 0) return cudaSuccess;
+  x3_update_kernel<<<num_sms() * 4, 256, 0, st>>>(m, d, incz, piz, kz, fast, sh, stop);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,

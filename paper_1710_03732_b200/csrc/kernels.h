@@ -39,6 +39,21 @@ struct BatchLapParams {
   int tile_base;            // global index of tile 0 of this launch (error reports)
 };
 
+constexpr int kMaxRanks = 8;
+
+// Shard description (multi-GPU).  Rank r owns first facilities
+// [abound[r], abound[r+1]) and tiles [tbase[r], tbase[r+1]).
+struct ShardInfo {
+  int world, rank;
+  int abound[kMaxRanks + 1];
+  int tbase[kMaxRanks + 1];
+  // exchange buffers indexed by peer rank (null where unused)
+  const double* sig_recv[kMaxRanks];   // from higher ranks: sigma of my X3 partners
+  double* gain_send[kMaxRanks];        // to higher ranks: gain of their X3 cells
+  double* sig_send[kMaxRanks];         // to lower ranks
+  const double* gain_recv[kMaxRanks];  // from lower ranks
+};
+
 struct FoldParams {
   int m;
   const int* triples;  // (a,b,c) a<b<c, 3 ints each, lexicographic
@@ -54,6 +69,7 @@ struct FoldParams {
   const int* stop;
   // phase 2 (rlt2.cpp:344-381): costs mutated in place from pi(z)
   double* costs;
+  const ShardInfo* shard;  // null on one GPU
 };
 
 struct XYFoldParams {
@@ -100,6 +116,8 @@ struct XStageParams {
   int* cert;
   double upper_bound, min_gap, fathom, es_delta;
   int es_window, iter_limit;
+  int* feas_bad;           // device flag: 1 if any induced slack > 1e-7
+  int zt_lo, zt_hi;        // tiles whose pi(z) this rank checks (feasibility)
 };
 
 // ---- launches (all asynchronous on `st`) ----
@@ -112,6 +130,12 @@ cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st);
 cudaError_t launch_lap_batch(const BatchLapParams& p, cudaStream_t st);
 cudaError_t launch_ystage(const YStageParams& p, cudaStream_t st);
 cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st);
+cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
+// multi-GPU exchange kernels
+cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
+                              const ShardInfo& sh, const int* stop, cudaStream_t st);
+cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
+                             int fast, const ShardInfo& sh, const int* stop, cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
                             DevScalars* S, double drained, int fast, cudaStream_t st);
 

@@ -66,6 +66,33 @@ lib.qapb_engine_set_profiling.argtypes = [_vp, C.c_int]
 lib.qapb_engine_kernel_times.argtypes = [_vp, _vp, _vp, C.c_int]
 lib.qapb_engine_history.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
 lib.qapb_engine_time_kernel.argtypes = [_vp, C.c_int, C.c_int, _P(C.c_double)]
+lib.qapb_shard_plan.argtypes = [C.c_int, C.c_int, _vp]
+lib.qapb_shard_exchange_counts.argtypes = [C.c_int, C.c_int, C.c_int, _vp, _vp]
+lib.qapb_nccl_unique_id.argtypes = [_vp]
+lib.qapb_engine_create_instance_sharded.argtypes = [C.c_int, _vp, _vp, _vp, _P(Config), C.c_int,
+                                                    C.c_int, _vp, _P(_vp)]
+
+
+def shard_plan(n: int, world: int) -> List[int]:
+    """First-facility boundaries per rank (world+1 entries), SURVEY.md §8(e)."""
+    b = np.zeros(world + 1, np.int32)
+    _check(lib.qapb_shard_plan(n, world, iptr(b)))
+    return [int(x) for x in b]
+
+
+def shard_exchange_counts(n: int, world: int, rank: int):
+    """Doubles `rank` sends to / receives from each peer in one exchange."""
+    s = np.zeros(world, np.int64)
+    r = np.zeros(world, np.int64)
+    _check(lib.qapb_shard_exchange_counts(n, world, rank, s.ctypes.data_as(C.c_void_p),
+                                          r.ctypes.data_as(C.c_void_p)))
+    return s, r
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(lib.qapb_nccl_unique_id(buf))
+    return bytes(buf)
 
 KERNEL_NAMES = ["xyfold", "zfold", "zlap", "phase2", "ystage", "xstage"]
 
@@ -341,6 +368,23 @@ class AscentEngine:
         c = self.cfg.to_c()
         _check(lib.qapb_engine_create_instance(inst.n, dptr(inst.flow), dptr(inst.dist),
                                                dptr(inst.linear), C.byref(c), C.byref(h)))
+        self._h = h
+        return self
+
+    @classmethod
+    def from_instance_sharded(cls, inst: QapInstance, cfg: Optional[AscentConfig], rank: int,
+                              world: int, nccl_id: bytes):
+        """One rank of a z-sharded engine (one process per GPU).
+        Every rank passes the same instance, cfg and NCCL id; cfg.device = its GPU."""
+        self = cls.__new__(cls)
+        self.cfg = cfg or AscentConfig()
+        self.m = inst.n
+        h = C.c_void_p()
+        c = self.cfg.to_c()
+        idbuf = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+        _check(lib.qapb_engine_create_instance_sharded(inst.n, dptr(inst.flow), dptr(inst.dist),
+                                                       dptr(inst.linear), C.byref(c), rank, world,
+                                                       idbuf, C.byref(h)))
         self._h = h
         return self
 
