@@ -12,6 +12,7 @@
 
 #include "../../include/qapb200.h"
 #include "engine.h"
+#include "nccl_dyn.h"
 #include "kernels.h"
 
 using qapb::CudaError;
@@ -534,8 +535,9 @@ QAPB_API qapb_status qapb_shard_exchange_counts(int n, int world, int rank, long
 QAPB_API qapb_status qapb_nccl_unique_id(unsigned char id[128]) {
   return guard([&] {
     ncclUniqueId u;
-    const ncclResult_t r = ncclGetUniqueId(&u);
-    if (r != ncclSuccess) throw CudaError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    const ncclResult_t r = qapb::nccl().GetUniqueId(&u);
+    if (r != ncclSuccess)
+      throw CudaError(std::string("ncclGetUniqueId: ") + qapb::nccl().GetErrorString(r));
     static_assert(sizeof(u) == 128, "NCCL unique id size");
     std::memcpy(id, &u, 128);
   });

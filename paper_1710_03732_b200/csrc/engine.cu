@@ -1,5 +1,6 @@
 // engine.cu — host side of the device-resident RLT2 dual-ascent engine.
 #include "engine.h"
+#include "nccl_dyn.h"
 
 #include <chrono>
 #include <climits>
@@ -241,7 +242,7 @@ Engine::~Engine() {
   for (auto* p : xbufs_) cudaFree(p);
   if (shard_dev_) cudaFree(shard_dev_);
   if (feas_bad_) cudaFree(feas_bad_);
-  if (comm_) ncclCommDestroy(comm_);
+  if (comm_) nccl().CommDestroy(comm_);
   for (auto e : stage_ev_) cudaEventDestroy(e);
   if (join_ev_) cudaEventDestroy(join_ev_);
   if (st2_) cudaStreamDestroy(st2_);
@@ -287,7 +288,7 @@ void Engine::pull_scalars() {
 
 void Engine::nccl_check(ncclResult_t r, const char* what) const {
   if (r != ncclSuccess)
-    throw CudaError(std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+    throw CudaError(std::string("NCCL error in ") + what + ": " + nccl().GetErrorString(r));
 }
 
 void Engine::setup_shards(const unsigned char* nccl_id) {
@@ -315,7 +316,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   if (world_ == 1) return;
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
-  nccl_check(ncclCommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
+  nccl_check(nccl().CommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
   std::vector<long long> send, recv;
   shard_counts(m, ab, rank_, send, recv);
   xcount_.assign(2 * world_, 0);
@@ -356,32 +357,32 @@ void Engine::enqueue_sharded_z(int it) {
     kbegin(QAPB_K_ZFOLD, st_);
     cuda_check(launch_sigma_pack(m_, piz_, push_, cfg_.kappa_z_upper, shard_, &S_->stop, st_),
                "sigma pack");
-    nccl_check(ncclGroupStart(), "group");
+    nccl_check(nccl().GroupStart(), "group");
     for (int p = 0; p < world_; ++p) {
       if (xcount_[p])
-        nccl_check(ncclSend(shard_.sig_send[p], xcount_[p], ncclDouble, p, comm_, st_), "send");
+        nccl_check(nccl().Send(shard_.sig_send[p], xcount_[p], ncclDouble, p, comm_, st_), "send");
       if (xcount_[world_ + p])
-        nccl_check(ncclRecv(const_cast<double*>(shard_.sig_recv[p]), xcount_[world_ + p],
+        nccl_check(nccl().Recv(const_cast<double*>(shard_.sig_recv[p]), xcount_[world_ + p],
                             ncclDouble, p, comm_, st_),
                    "recv");
     }
-    nccl_check(ncclGroupEnd(), "group");
+    nccl_check(nccl().GroupEnd(), "group");
     FoldParams f = fold_params(-1);
     f.triples = triples_ + 3 * (size_t)tri_lo_;
     f.ntriples = tri_hi_ - tri_lo_;
     f.shard = shard_dev_;
     cuda_check(launch_zfold(f, st_), "z-fold");
-    nccl_check(ncclGroupStart(), "group");
+    nccl_check(nccl().GroupStart(), "group");
     for (int p = 0; p < world_; ++p) {
       if (xcount_[world_ + p])
-        nccl_check(ncclSend(shard_.gain_send[p], xcount_[world_ + p], ncclDouble, p, comm_, st_),
+        nccl_check(nccl().Send(shard_.gain_send[p], xcount_[world_ + p], ncclDouble, p, comm_, st_),
                    "send");
       if (xcount_[p])
-        nccl_check(ncclRecv(const_cast<double*>(shard_.gain_recv[p]), xcount_[p], ncclDouble, p,
+        nccl_check(nccl().Recv(const_cast<double*>(shard_.gain_recv[p]), xcount_[p], ncclDouble, p,
                             comm_, st_),
                    "recv");
     }
-    nccl_check(ncclGroupEnd(), "group");
+    nccl_check(nccl().GroupEnd(), "group");
     cuda_check(launch_x3_update(m_, d_, incz_, piz_, cfg_.kappa_z_upper, fast, shard_, &S_->stop,
                                 st_),
                "x3 update");
@@ -389,15 +390,15 @@ void Engine::enqueue_sharded_z(int it) {
     launches_ += 3;
   }
   enqueue_zlap(costs, t_lo_, t_hi_ - t_lo_, theta_, nullptr, S, st_);
-  nccl_check(ncclGroupStart(), "group");
+  nccl_check(nccl().GroupStart(), "group");
   for (int r = 0; r < world_; ++r) {
     const int c = shard_.tbase[r + 1] - shard_.tbase[r];
     if (c)
-      nccl_check(ncclBroadcast(theta_ + shard_.tbase[r], theta_ + shard_.tbase[r], c, ncclDouble,
+      nccl_check(nccl().Broadcast(theta_ + shard_.tbase[r], theta_ + shard_.tbase[r], c, ncclDouble,
                                r, comm_, st_),
                  "theta broadcast");
   }
-  nccl_check(ncclGroupEnd(), "group");
+  nccl_check(nccl().GroupEnd(), "group");
 }
 
 void Engine::plan_pipeline() {
@@ -601,7 +602,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   kbegin(QAPB_K_XSTAGE, st_);
   cuda_check(launch_xstage(xs, st_), "x-stage");
   if (world_ > 1)  // feasibility needs every rank's pi(z) tiles
-    nccl_check(ncclAllReduce(feas_bad_, feas_bad_, 1, ncclInt, ncclMax, comm_, st_), "allreduce");
+    nccl_check(nccl().AllReduce(feas_bad_, feas_bad_, 1, ncclInt, ncclMax, comm_, st_), "allreduce");
   cuda_check(launch_xfinish(xs, st_), "x-finish");
   kend(st_);
   launches_ += 2;

@@ -90,6 +90,7 @@ def shard_exchange_counts(n: int, world: int, rank: int):
 
 
 def nccl_unique_id() -> bytes:
+    import torch  # noqa: F401  (bind to the NCCL torch already loaded, see csrc/nccl_dyn.h)
     buf = (C.c_ubyte * 128)()
     _check(lib.qapb_nccl_unique_id(buf))
     return bytes(buf)
@@ -376,6 +377,7 @@ class AscentEngine:
                               world: int, nccl_id: bytes):
         """One rank of a z-sharded engine (one process per GPU).
         Every rank passes the same instance, cfg and NCCL id; cfg.device = its GPU."""
+        import torch  # noqa: F401  (bind to the NCCL torch already loaded)
         self = cls.__new__(cls)
         self.cfg = cfg or AscentConfig()
         self.m = inst.n
