@@ -249,9 +249,14 @@ def run_ours(args):
     launches = eng.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
     ktimes = eng.kernel_times(reset=True)
+    rank_times = None
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        rank_times = [None] * world
+        torch.distributed.all_gather_object(
+            rank_times, {"ms": ms, **{k: round(v[0] / max(1, v[1]), 4) for k, v in ktimes.items()
+                                     if v[1]}})
         ms = float(t.item())
     clocks = clk.summary()
 
@@ -354,6 +359,8 @@ def run_ours(args):
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         "parity": parity, "bound_after": final_bound,
     }
+    if rank_times:
+        line["per_rank_ms_per_launch"] = rank_times
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

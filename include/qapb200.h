@@ -4,7 +4,7 @@
  * This is the drop-in boundary for the reference's hot path
  * (`qap::AscentEngine` + the Hungarian LAP solver it calls).  Every entry
  * point takes plain pointers and sizes; no C++ or torch types cross it.
- * The C++ facade in include/qap/*.hpp rebuilds the reference API
+ * The C++ facade in include/qap/ (instance, lap, rlt2 .hpp) rebuilds the reference API
  * (same class names, signatures and exception types) on top of these
  * calls; Python reaches them through ctypes.
  *

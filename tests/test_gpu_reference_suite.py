@@ -1,0 +1,37 @@
+"""GPU: the reference's OWN unit tests (proj/tests/test_lap.cpp and
+test_rlt2.cpp), compiled unmodified against the B200 facade headers
+(include/qap/*.hpp) + libqapb200.so by `make -C oracle reftests`, must pass.
+The binaries are built where /root/reference exists and travel in-tree
+(build/reftests); fixtures are regenerated from tests/golden/golden.json."""
+import json
+import os
+import subprocess
+
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+pytestmark = pytest.mark.gpu
+BIN = os.path.join(ROOT, "build", "reftests")
+
+
+def _write_fixtures(dirpath):
+    with open(os.path.join(GOLDEN, "golden.json")) as fh:
+        g = json.load(fh)
+    for name in ("nug12", "zero", "nug5", "two"):
+        inst = g[name]
+        rows = lambda m: "\n".join(" ".join(str(int(x)) for x in r) for r in m)
+        with open(os.path.join(dirpath, f"{name}.dat"), "w") as fh:
+            fh.write(f"{inst['n']}\n\n{rows(inst['flow'])}\n\n{rows(inst['dist'])}\n")
+
+
+@pytest.mark.parametrize("name", ["test_lap_b200", "test_rlt2_b200"])
+def test_reference_unit_tests_pass_on_b200(name, tmp_path):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    _write_fixtures(str(tmp_path))
+    env = dict(os.environ, QAPB_FIXTURE_DIR=str(tmp_path))
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=1200, env=env)
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-4000:]
+    assert "| 0 failed" in out.stdout
