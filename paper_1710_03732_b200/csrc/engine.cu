@@ -12,16 +12,27 @@
 namespace qapb {
 
 std::vector<int> shard_plan(int n, int world) {
-  // contiguous first-facility ranges; a facility's work = its share of the
-  // fold (triples a<b<c: C(n-1-a,2)) and of the Z-LAPs (pairs: n-1-a),
-  // weighted by their measured split of an n=30 iteration (0.55 / 0.45)
+  // Contiguous first-facility ranges [s,e) chosen by DP to minimise the
+  // slowest rank's predicted time (constants: n=30 single-GPU measurements
+  // and NVLink peer bandwidth):
+  //   fold of its triples + Z-LAPs of its tiles
+  //   + cross families as X3 owner (sigma pack, X3 update, 8 B out / 8 B in)
+  //   + cross families as fold owner (gain pre-pass, 8 B out / 8 B in)
   const int F = n - 1;  // first facilities 0..n-2 own pairs
   if (world < 1 || world > F) throw std::invalid_argument("shard_plan: bad world size");
   auto c2 = [](double x) { return x >= 2 ? x * (x - 1) / 2 : 0.0; };
-  const double tri = std::max(1.0, c2(n) * (n - 2) / 3.0), pairs = std::max(1.0, c2(n));
-  std::vector<double> pre(F + 1, 0.0);
-  for (int a = 0; a < F; ++a)
-    pre[a + 1] = pre[a] + 0.55 * c2(n - 1 - a) / tri + 0.45 * (n - 1 - a) / pairs;
+  const double L = (double)n * (n - 1) * (n - 2), lp = (double)n * (n - 1);
+  const double a_fold = 33.3e-12, b_lap = 6.95e-9, g_xb = 11e-12 + 12.3e-12, d_xa = 15e-12;
+  auto cost = [&](int s, int e) {
+    double F3 = 0, T = 0, XB = 0;
+    for (int a = s; a < e; ++a) {
+      F3 += c2(n - 1 - a);
+      T += (n - 1 - a) * lp;
+      XB += (double)s * (n - 1 - a);  // families (a'<s, b=a, c>a)
+    }
+    const double XA = (e - s) * c2(n - e);  // families (a in range, b >= e)
+    return a_fold * L * F3 + b_lap * T + g_xb * L * XB + d_xa * L * XA;
+  };
   const double INF = std::numeric_limits<double>::infinity();
   std::vector<std::vector<double>> f(world + 1, std::vector<double>(F + 1, INF));
   std::vector<std::vector<int>> arg(world + 1, std::vector<int>(F + 1, -1));
@@ -29,19 +40,19 @@ std::vector<int> shard_plan(int n, int world) {
   for (int k = 1; k <= world; ++k)
     for (int i = k; i <= F; ++i)
       for (int j = k - 1; j < i; ++j) {
-        const double v = std::max(f[k - 1][j], pre[i] - pre[j]);
+        const double v = std::max(f[k - 1][j], cost(j, i));
         if (v < f[k][i]) {
           f[k][i] = v;
           arg[k][i] = j;
         }
       }
-  std::vector<int> b(world + 1);
-  b[world] = F;
+  std::vector<int> bnd(world + 1);
+  bnd[world] = F;
   for (int k = world, i = F; k > 0; --k) {
     i = arg[k][i];
-    b[k - 1] = i;
+    bnd[k - 1] = i;
   }
-  return b;
+  return bnd;
 }
 
 void shard_counts(int n, const std::vector<int>& ab, int rank, std::vector<long long>& send,
@@ -243,6 +254,11 @@ Engine::~Engine() {
   if (shard_dev_) cudaFree(shard_dev_);
   if (feas_bad_) cudaFree(feas_bad_);
   if (comm_) nccl().CommDestroy(comm_);
+  if (tri_local_) cudaFree(tri_local_);
+  if (tri_remote_) cudaFree(tri_remote_);
+  if (ev_pack_) cudaEventDestroy(ev_pack_);
+  if (ev_xchg_) cudaEventDestroy(ev_xchg_);
+  if (comm_st_) cudaStreamDestroy(comm_st_);
   for (auto e : stage_ev_) cudaEventDestroy(e);
   if (join_ev_) cudaEventDestroy(join_ev_);
   if (st2_) cudaStreamDestroy(st2_);
@@ -314,6 +330,28 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   tri_hi_ = tri_before(ab[rank_ + 1]);
   dalloc(&feas_bad_, 1);
   if (world_ == 1) return;
+  {  // owned triples split by where their X3 member lives
+    std::vector<int> loc, rem;
+    for (int a = ab[rank_]; a < ab[rank_ + 1]; ++a)
+      for (int b = a + 1; b < m; ++b)
+        for (int c = b + 1; c < m; ++c) {
+          auto& v = b < ab[rank_ + 1] ? loc : rem;
+          v.push_back(a);
+          v.push_back(b);
+          v.push_back(c);
+        }
+    n_local_ = (int)loc.size() / 3;
+    n_remote_ = (int)rem.size() / 3;
+    dalloc(&tri_local_, loc.size());
+    dalloc(&tri_remote_, rem.size());
+    if (!loc.empty())
+      cuda_check(cudaMemcpy(tri_local_, loc.data(), loc.size() * 4, cudaMemcpyHostToDevice), "H2D");
+    if (!rem.empty())
+      cuda_check(cudaMemcpy(tri_remote_, rem.data(), rem.size() * 4, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&ev_pack_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_xchg_, cudaEventDisableTiming), "event");
+  }
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
   nccl_check(nccl().CommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
@@ -346,8 +384,13 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   cuda_check(cudaMemcpy(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice), "H2D shard");
 }
 
-// Steady sharded Z stage: sigma out -> fold (owned triples) -> gain back ->
-// X3 update -> Z-LAPs of owned tiles -> theta re-assembled on every rank.
+// Steady sharded Z stage (one exchange per iteration):
+//   sigma of my X3 cells owned by lower ranks' families  -> send buffers
+//   gains of the X3 members of my cross-shard families   -> send buffers
+//   one grouped NCCL send/recv on comm_st_, overlapped with the fold of my
+//   purely local triples; then the X1/X2 updates of the cross-shard
+//   triples, the X3 updates the lower ranks' gains asked for, my Z-LAPs, and
+//   theta re-assembled on every rank.
 void Engine::enqueue_sharded_z(int it) {
   const bool fast = is_fast();
   double* costs = (fast && it > 0) ? incz_ : d_;
@@ -357,45 +400,55 @@ void Engine::enqueue_sharded_z(int it) {
     kbegin(QAPB_K_ZFOLD, st_);
     cuda_check(launch_sigma_pack(m_, piz_, push_, cfg_.kappa_z_upper, shard_, &S_->stop, st_),
                "sigma pack");
+    FoldParams fr = fold_params(-1);
+    fr.triples = tri_remote_;
+    fr.ntriples = n_remote_;
+    fr.shard = shard_dev_;
+    fr.mode = 1;
+    cuda_check(launch_zfold(fr, st_), "gain pass");
+    cuda_check(cudaEventRecord(ev_pack_, st_), "event");
+    cuda_check(cudaStreamWaitEvent(comm_st_, ev_pack_, 0), "wait");
     nccl_check(nccl().GroupStart(), "group");
     for (int p = 0; p < world_; ++p) {
-      if (xcount_[p])
-        nccl_check(nccl().Send(shard_.sig_send[p], xcount_[p], ncclDouble, p, comm_, st_), "send");
-      if (xcount_[world_ + p])
-        nccl_check(nccl().Recv(const_cast<double*>(shard_.sig_recv[p]), xcount_[world_ + p],
-                            ncclDouble, p, comm_, st_),
-                   "recv");
-    }
-    nccl_check(nccl().GroupEnd(), "group");
-    FoldParams f = fold_params(-1);
-    f.triples = triples_ + 3 * (size_t)tri_lo_;
-    f.ntriples = tri_hi_ - tri_lo_;
-    f.shard = shard_dev_;
-    cuda_check(launch_zfold(f, st_), "z-fold");
-    nccl_check(nccl().GroupStart(), "group");
-    for (int p = 0; p < world_; ++p) {
-      if (xcount_[world_ + p])
-        nccl_check(nccl().Send(shard_.gain_send[p], xcount_[world_ + p], ncclDouble, p, comm_, st_),
+      if (xcount_[p]) {  // lower peer: sigma out, gain in
+        nccl_check(nccl().Send(shard_.sig_send[p], xcount_[p], ncclDouble, p, comm_, comm_st_),
                    "send");
-      if (xcount_[p])
-        nccl_check(nccl().Recv(const_cast<double*>(shard_.gain_recv[p]), xcount_[p], ncclDouble, p,
-                            comm_, st_),
+        nccl_check(nccl().Recv(const_cast<double*>(shard_.gain_recv[p]), xcount_[p], ncclDouble,
+                               p, comm_, comm_st_),
                    "recv");
+      }
+      if (xcount_[world_ + p]) {  // higher peer: sigma in, gain out
+        nccl_check(nccl().Recv(const_cast<double*>(shard_.sig_recv[p]), xcount_[world_ + p],
+                               ncclDouble, p, comm_, comm_st_),
+                   "recv");
+        nccl_check(nccl().Send(shard_.gain_send[p], xcount_[world_ + p], ncclDouble, p, comm_,
+                               comm_st_),
+                   "send");
+      }
     }
     nccl_check(nccl().GroupEnd(), "group");
+    cuda_check(cudaEventRecord(ev_xchg_, comm_st_), "event");
+    FoldParams fl = fold_params(-1);  // local triples: no exchange needed
+    fl.triples = tri_local_;
+    fl.ntriples = n_local_;
+    fl.shard = shard_dev_;
+    cuda_check(launch_zfold(fl, st_), "z-fold local");
+    cuda_check(cudaStreamWaitEvent(st_, ev_xchg_, 0), "wait");
+    fr.mode = 2;
+    cuda_check(launch_zfold(fr, st_), "z-fold remote");
     cuda_check(launch_x3_update(m_, d_, incz_, piz_, cfg_.kappa_z_upper, fast, shard_, &S_->stop,
                                 st_),
                "x3 update");
     kend(st_);
-    launches_ += 3;
+    launches_ += 5;
   }
   enqueue_zlap(costs, t_lo_, t_hi_ - t_lo_, theta_, nullptr, S, st_);
   nccl_check(nccl().GroupStart(), "group");
   for (int r = 0; r < world_; ++r) {
     const int c = shard_.tbase[r + 1] - shard_.tbase[r];
     if (c)
-      nccl_check(nccl().Broadcast(theta_ + shard_.tbase[r], theta_ + shard_.tbase[r], c, ncclDouble,
-                               r, comm_, st_),
+      nccl_check(nccl().Broadcast(theta_ + shard_.tbase[r], theta_ + shard_.tbase[r], c,
+                                  ncclDouble, r, comm_, st_),
                  "theta broadcast");
   }
   nccl_check(nccl().GroupEnd(), "group");

@@ -260,17 +260,17 @@ struct FoldSmem {
 __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
                                              const double* __restrict__ piz,
                                              const double* __restrict__ vals, double* sm,
-                                             const FoldSmem& L) {
+                                             const FoldSmem& L, int mode = 0) {
   double* S = sm + L.pi_off();
   double* V = sm + L.val_off();
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
     double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
     if (mem == 2 && f.xr >= 0) {  // remote X3: its owner sent sigma (kz*pi + push)
-      cp_async8(sp, f.xsig + g);
+      if (mode != 1) cp_async8(sp, f.xsig + g);
       return;
     }
     cp_async8(sp, piz + g);
-    cp_async8(V + slot, vals + g);
+    if (mode != 1) cp_async8(V + slot, vals + g);
   });
 }
 
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   double* U3 = U2 + C * n;         // [n][n]  push of tile (b,c,pb,pc)
   const DIdx ix(n);
   const int tid = threadIdx.x, bd = blockDim.x;
-  stage_family(f, C, P.piz, P.d, sm, L);
+  const int mode = P.mode;
+  stage_family(f, C, P.piz, P.d, sm, L, mode);
   for (int e = tid; e < f.Pe * n; e += bd) {
     const int pa_l = e / n, q = e - pa_l * n, pa = f.pa0 + pa_l;
     if (q == pa) continue;
@@ -308,6 +309,13 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   const bool remote3 = f.xr >= 0;
   for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
     const int fi = (pa_l * n + pb) * L.np + pc;
+    if (mode == 1) {  // gain of the remote X3 member only: phi*sigma1 + phi*sigma2
+      if (mem != 2) return;
+      const double s1 = dadd(dmul(kz, S[fi]), U1[pa_l * n + pb]);
+      const double s2 = dadd(dmul(kz, S[L.cube + fi]), U2[pa_l * n + pc]);
+      f.xgain[g] = dadd(dmul(phi, s1), dmul(phi, s2));
+      return;
+    }
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
     const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
@@ -324,7 +332,7 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
     }
     if (mem == 2 && remote3) {  // the X3 owner applies it (x3_update_kernel)
-      f.xgain[g] = gain;
+      if (mode == 0) f.xgain[g] = gain;
       return;
     }
     d[g] = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292

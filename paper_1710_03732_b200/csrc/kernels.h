@@ -70,6 +70,10 @@ struct FoldParams {
   // phase 2 (rlt2.cpp:344-381): costs mutated in place from pi(z)
   double* costs;
   const ShardInfo* shard;  // null on one GPU
+  // multi-GPU passes over triples whose X3 member is remote (owner(b) != me):
+  // 0 whole fold, 1 gains of the X3 members only (before the exchange),
+  // 2 X1/X2 updates with the received sigma (after it)
+  int mode;
 };
 
 struct XYFoldParams {
