@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(128) ystage_kernel(YStageParams P, int warps_p
 // (rlt2.cpp:453-473) over the pi(z) tiles this rank holds; the flag is
 // all-reduced across ranks before xfinish_kernel.
 template <int CPL>
-__global__ void __launch_bounds__(256) xstage_kernel(XStageParams P) {
+__global__ void __launch_bounds__(1024) xstage_kernel(XStageParams P) {
   DevScalars* S = P.S;
   if (S->stop) return;
   extern __shared__ double xsm[];
@@ -770,7 +770,7 @@ cudaError_t launch_xstage_t(const XStageParams& p, cudaStream_t st) {
   const size_t smem = ((size_t)p.m * p.m + p.m + 1) * sizeof(double);
   cudaFuncSetAttribute(xstage_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
-  xstage_kernel<CPL><<<1, 256, smem, st>>>(p);
+  xstage_kernel<CPL><<<1, 1024, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,20 @@ __device__ __forceinline__ unsigned long long ordkey(double x) {
   return (unsigned long long)(b ^ ((b >> 63) | (long long)0x8000000000000000ull));
 }
 
+// The same key as two 32-bit halves in three integer ops (one shift, two
+// 3-input LOPs): khi = hi ^ (s | 0x80000000), klo = lo ^ s, s = hi >> 31.
+__device__ __forceinline__ void ordkey2(double x, unsigned& khi, unsigned& klo) {
+  const double c = dadd(x, 0.0);
+  asm("{\n\t.reg .b32 lo, hi, s, t;\n\t"
+      "mov.b64 {lo, hi}, %2;\n\t"
+      "shr.s32 s, hi, 31;\n\t"
+      "or.b32 t, s, 0x80000000;\n\t"
+      "xor.b32 %0, hi, t;\n\t"
+      "xor.b32 %1, lo, s;\n\t}"
+      : "=r"(khi), "=r"(klo)
+      : "d"(c));
+}
+
 template <int CPL>
 struct LapLane {
   int p[CPL];     // row matched to column s*32+lane, -1 when free   (lap.cpp:30)
@@ -56,7 +70,12 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   L.w[0] = 0.0;
   L.v[0] = 0.0;
   int way = 0;
-  for (int i = 0; i < m; ++i) {  // lap.cpp:33
+  // Non-finite (or overflow-prone) costs would let the search run forever
+  // (the reference is undefined there too): check the tile once and bail out.
+  bool ok = true;
+  for (int e = lane; e < m * m; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
+  const bool bad = !__all_sync(QAPB_FULL, ok);
+  for (int i = 0; i < m && !bad; ++i) {  // lap.cpp:33
     double minv = INF;
     if (lane == m) {  // p[m] = i; u[i] is still 0
       L.p[0] = i;
@@ -65,14 +84,7 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
     bool used = !real;  // padding lanes (and the virtual column m) never relax
     int j0 = m, i0 = i;
     double ui0 = 0.0;
-    // every step uses one more column, so a row takes at most m steps; more
-    // means non-finite costs (the reference is undefined there too): stop
-    for (int guard = 0;; ++guard) {  // lap.cpp:40-67
-      if (guard > m) {  // leave a valid permutation behind for the writers
-        L.p[0] = real ? lane : -1;
-        L.w[0] = L.v[0] = __longlong_as_double(0x7ff8000000000000ll);
-        return L.w[0];
-      }
+    while (true) {  // lap.cpp:40-67 (at most m+1 steps: finite costs, checked above)
       // a used column's minv is never read again in this row (lap.cpp:47,58-64):
       // park it at +inf so the order key needs no activity mask
       if (lane == j0) {
@@ -84,14 +96,14 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
         minv = cur;
         way = j0;
       }
-      const unsigned long long k = ordkey(minv);  // +inf for used / padding lanes
-      const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+      unsigned hi, lo;  // order key of minv (+inf for used / padding lanes)
+      ordkey2(minv, hi, lo);
       const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
       const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
-      const int j1 = (__ffs(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin)) - 1) & 31;
+      const int j1 = __ffs(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin)) - 1;
       const double delta = __shfl_sync(QAPB_FULL, minv, j1);
-      minv = dsub(minv, delta);  // lap.cpp:63 (inf stays inf for used lanes)
-      if (used) {                // lap.cpp:60-61
+      minv = dsub(minv, delta);                    // lap.cpp:63 (inf stays inf when used)
+      if (used) {  // lap.cpp:60-61
         L.w[0] = dadd(L.w[0], delta);
         L.v[0] = dsub(L.v[0], delta);
       }
@@ -102,7 +114,7 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
       i0 = pj;
       ui0 = wj;
     }
-    for (int g2 = 0; j0 != m && g2 <= m; ++g2) {  // augment, lap.cpp:68-72
+    while (j0 != m) {  // augment, lap.cpp:68-72
       const int jw = __shfl_sync(QAPB_FULL, way, j0);
       const int pw = __shfl_sync(QAPB_FULL, L.p[0], jw);
       const double ww = __shfl_sync(QAPB_FULL, L.w[0], jw);
@@ -112,6 +124,11 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
       }
       j0 = jw;
     }
+  }
+  if (bad) {  // non-finite input: leave a valid permutation for the writers
+    L.p[0] = real ? lane : -1;
+    L.w[0] = L.v[0] = __longlong_as_double(0x7ff8000000000000ll);
+    return L.w[0];
   }
   const double term = real ? cost[(size_t)L.p[0] * m + lane] : 0.0;
   double value = 0.0;  // lap.cpp:75-80
@@ -138,7 +155,17 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
     way[s] = 0;
   }
   const int vs = m >> 5, vl = m & 31;  // owner of the virtual column m
-  for (int i = 0; i < m; ++i) {        // lap.cpp:33
+  bool ok = true;  // finite costs bound every row to m+1 steps (see warp_lap_solve_1)
+  for (int e = lane; e < m * m; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
+  if (!__all_sync(QAPB_FULL, ok)) {
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      L.p[s] = (s * 32 + lane < m) ? s * 32 + lane : -1;
+      L.w[s] = L.v[s] = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    return L.w[0];
+  }
+  for (int i = 0; i < m; ++i) {  // lap.cpp:33
 #pragma unroll
     for (int s = 0; s < CPL; ++s) {
       minv[s] = INF;
@@ -150,15 +177,7 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
     unsigned used = 0;
     int j0 = m, i0 = i;
     double ui0 = 0.0;
-    for (int guard = 0;; ++guard) {  // Dijkstra step, lap.cpp:40-67
-      if (guard > m) {  // non-finite input: leave a valid permutation behind
-#pragma unroll
-        for (int s = 0; s < CPL; ++s) {
-          L.p[s] = (s * 32 + lane < m) ? s * 32 + lane : -1;
-          L.w[s] = L.v[s] = __longlong_as_double(0x7ff8000000000000ll);
-        }
-        return L.w[0];
-      }
+    while (true) {  // Dijkstra step, lap.cpp:40-67
       if ((j0 & 31) == lane) used |= 1u << (j0 >> 5);
       const double* row = cost + (size_t)i0 * m;
       unsigned long long bkey = ~0ull;
@@ -212,7 +231,7 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
       i0 = pj;
       ui0 = wj;
     }
-    for (int g2 = 0; j0 != m && g2 <= m; ++g2) {  // augment, lap.cpp:68-72
+    while (j0 != m) {  // augment, lap.cpp:68-72
       const int s0 = j0 >> 5, l0 = j0 & 31;
       const int jw = __shfl_sync(QAPB_FULL, pick<CPL>(way, s0), l0);
       const int sw = jw >> 5, lw = jw & 31;
