@@ -245,17 +245,17 @@ QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms,
                                               long long* launches, int reset);
 
 /* ---- multi-GPU: one process per GPU, z state sharded -----
- * Rank r owns the facility pairs (a, b>a) with a in [a_bounds[r],
- * a_bounds[r+1]) -- a contiguous range of half-Z tiles -- and folds the
- * triples whose first facility it owns.  In a family (a<b<c) the X3 member
- * T(b,c)[a] belongs to owner(b): each iteration owner(b) sends
- * sigma = kz*pi + push of those cells to owner(a) and receives their gain
- * back (NCCL grouped send/recv); theta is re-assembled with broadcasts and
- * the O(n^4) Y/X stages run replicated, so every rank holds the same bound.
- * Results are bitwise those of the single-GPU engine. */
-/* Facility ranges per rank (a_bounds has world+1 entries), balanced over the
- * fold and Z-LAP work of each first facility. */
-QAPB_API qapb_status qapb_shard_plan(int n, int world, int* a_bounds);
+ * Rank r owns the half-Z tiles whose first location lies in
+ * [p_bounds[r], p_bounds[r+1]) -- equal shares of tiles, fold work and
+ * exchange volume -- and folds every facility triple for its own locations.
+ * In a family the X3 member T(b,c,pb,pc)[a,pa] belongs to owner(pb): each
+ * iteration owner(pb) sends sigma = kz*pi + push of those cells to owner(pa)
+ * and receives their gain back (two NCCL grouped send/recv rounds); theta is
+ * re-assembled with broadcasts and the O(n^4) Y/X stages run replicated, so
+ * every rank holds the same bound.  Results are bitwise those of the
+ * single-GPU engine. */
+/* Location ranges per rank (p_bounds has world+1 entries). */
+QAPB_API qapb_status qapb_shard_plan(int n, int world, int* p_bounds);
 /* Doubles rank `rank` sends (send[p]) to / receives (recv[p]) from every
  * peer p in ONE of the two per-iteration exchanges (both exchanges move the
  * same amounts in opposite directions). */

@@ -512,11 +512,11 @@ QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms, long l
   return guard([&] { e->e->kernel_times(ms, launches, reset != 0); });
 }
 
-QAPB_API qapb_status qapb_shard_plan(int n, int world, int* a_bounds) {
+QAPB_API qapb_status qapb_shard_plan(int n, int world, int* p_bounds) {
   return guard([&] {
     need(n >= 3, "shard_plan: n >= 3 required");
     auto b = qapb::shard_plan(n, world);
-    std::copy(b.begin(), b.end(), a_bounds);
+    std::copy(b.begin(), b.end(), p_bounds);
   });
 }
 

@@ -11,62 +11,31 @@
 
 namespace qapb {
 
+// Location ranges per rank: every first location owns the same
+// n(n-1)^2/2 tiles and the same share of fold work, so contiguous, near-equal
+// ranges balance the Z-LAPs, the fold and the exchange volume at once.
 std::vector<int> shard_plan(int n, int world) {
-  // Contiguous first-facility ranges [s,e) chosen by DP to minimise the
-  // slowest rank's predicted time (constants: n=30 single-GPU measurements
-  // and NVLink peer bandwidth):
-  //   fold of its triples + Z-LAPs of its tiles
-  //   + cross families as X3 owner (sigma pack, X3 update, 8 B out / 8 B in)
-  //   + cross families as fold owner (gain pre-pass, 8 B out / 8 B in)
-  const int F = n - 1;  // first facilities 0..n-2 own pairs
-  if (world < 1 || world > F) throw std::invalid_argument("shard_plan: bad world size");
-  auto c2 = [](double x) { return x >= 2 ? x * (x - 1) / 2 : 0.0; };
-  const double L = (double)n * (n - 1) * (n - 2), lp = (double)n * (n - 1);
-  const double a_fold = 33.3e-12, b_lap = 6.95e-9, g_xb = 11e-12 + 12.3e-12, d_xa = 15e-12;
-  auto cost = [&](int s, int e) {
-    double F3 = 0, T = 0, XB = 0;
-    for (int a = s; a < e; ++a) {
-      F3 += c2(n - 1 - a);
-      T += (n - 1 - a) * lp;
-      XB += (double)s * (n - 1 - a);  // families (a'<s, b=a, c>a)
-    }
-    const double XA = (e - s) * c2(n - e);  // families (a in range, b >= e)
-    return a_fold * L * F3 + b_lap * T + g_xb * L * XB + d_xa * L * XA;
-  };
-  const double INF = std::numeric_limits<double>::infinity();
-  std::vector<std::vector<double>> f(world + 1, std::vector<double>(F + 1, INF));
-  std::vector<std::vector<int>> arg(world + 1, std::vector<int>(F + 1, -1));
-  f[0][0] = 0;
-  for (int k = 1; k <= world; ++k)
-    for (int i = k; i <= F; ++i)
-      for (int j = k - 1; j < i; ++j) {
-        const double v = std::max(f[k - 1][j], cost(j, i));
-        if (v < f[k][i]) {
-          f[k][i] = v;
-          arg[k][i] = j;
-        }
-      }
-  std::vector<int> bnd(world + 1);
-  bnd[world] = F;
-  for (int k = world, i = F; k > 0; --k) {
-    i = arg[k][i];
-    bnd[k - 1] = i;
-  }
-  return bnd;
+  if (world < 1 || world > n) throw std::invalid_argument("shard_plan: bad world size");
+  std::vector<int> b(world + 1);
+  for (int r = 0; r <= world; ++r) b[r] = (int)(((long long)r * n) / world);
+  return b;
 }
 
-void shard_counts(int n, const std::vector<int>& ab, int rank, std::vector<long long>& send,
+// doubles rank `rank` sends to (send[p]) / receives from (recv[p]) each peer in
+// the sigma exchange; the gain exchange moves the same amounts back.
+void shard_counts(int n, const std::vector<int>& pb, int rank, std::vector<long long>& send,
                   std::vector<long long>& recv) {
-  const int world = (int)ab.size() - 1;
-  const long long lp = (long long)n * (n - 1), nm2 = n - 2;
-  auto fpf = [&](int i) { return (long long)i * n - (long long)i * (i + 1) / 2; };
-  auto tiles = [&](int r) { return (fpf(ab[r + 1]) - fpf(ab[r])) * lp; };
-  auto rows = [&](int r) { return (long long)(ab[r + 1] - ab[r]); };
+  const int world = (int)pb.size() - 1;
+  long long rows = 0;  // sum over pairs b<c of b
+  for (int b = 0; b < n; ++b) rows += (long long)b * (n - 1 - b);
+  auto rl = [&](int r) { return (long long)(pb[r + 1] - pb[r]) * (n - 1); };
+  auto nl = [&](int r) { return (long long)(pb[r + 1] - pb[r]); };
   send.assign(world, 0);
   recv.assign(world, 0);
   for (int p = 0; p < world; ++p) {
-    if (p < rank) send[p] = tiles(rank) * rows(p) * nm2;  // sigma of my rows a in p's range
-    if (p > rank) recv[p] = tiles(p) * rows(rank) * nm2;
+    if (p == rank) continue;
+    send[p] = rl(rank) * rows * nl(p);  // sigma of my X3 cells for p's pa
+    recv[p] = rl(p) * rows * nl(rank);  // sigma of p's X3 cells for my pa
   }
 }
 
@@ -129,8 +98,7 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
     throw std::invalid_argument("AscentEngine: bad rank/world");
   if (world_ > 1 && (is_two_phase() || cfg.sa_enabled))
     throw std::invalid_argument("sharded engine: F1/S1 without SA only (round 1)");
-  if (world_ > std::max(1, n - 2))
-    throw std::invalid_argument("sharded engine: more ranks than first facilities");
+  if (world_ > n) throw std::invalid_argument("sharded engine: more ranks than locations");
   alloc();
   setup_shards(nccl_id);
   init_state();
@@ -254,11 +222,8 @@ Engine::~Engine() {
   if (shard_dev_) cudaFree(shard_dev_);
   if (feas_bad_) cudaFree(feas_bad_);
   if (comm_) nccl().CommDestroy(comm_);
-  if (tri_local_) cudaFree(tri_local_);
-  if (tri_remote_) cudaFree(tri_remote_);
-  if (ev_pack_) cudaEventDestroy(ev_pack_);
-  if (ev_xchg_) cudaEventDestroy(ev_xchg_);
-  if (comm_st_) cudaStreamDestroy(comm_st_);
+  if (rows_before_) cudaFree(rows_before_);
+  if (theta_buf_) cudaFree(theta_buf_);
   for (auto e : stage_ev_) cudaEventDestroy(e);
   if (join_ev_) cudaEventDestroy(join_ev_);
   if (st2_) cudaStreamDestroy(st2_);
@@ -309,88 +274,70 @@ void Engine::nccl_check(ncclResult_t r, const char* what) const {
 
 void Engine::setup_shards(const unsigned char* nccl_id) {
   const int m = m_;
-  std::vector<int> ab = world_ > 1 ? shard_plan(m, world_) : std::vector<int>{0, m - 1};
-  auto fpf = [&](int i) { return i * m - i * (i + 1) / 2; };
-  auto c2 = [](int x) { return x >= 2 ? x * (x - 1) / 2 : 0; };
-  auto tri_before = [&](int a) {
-    int t = 0;
-    for (int x = 0; x < a; ++x) t += c2(m - 1 - x);
-    return t;
-  };
+  std::vector<int> pb = world_ > 1 ? shard_plan(m, world_) : std::vector<int>{0, m};
   shard_ = ShardInfo{};
   shard_.world = world_;
   shard_.rank = rank_;
-  for (int r = 0; r <= world_; ++r) {
-    shard_.abound[r] = ab[r];
-    shard_.tbase[r] = fpf(ab[r]) * lpairs_;
-  }
-  t_lo_ = shard_.tbase[rank_];
-  t_hi_ = shard_.tbase[rank_ + 1];
-  tri_lo_ = tri_before(ab[rank_]);
-  tri_hi_ = tri_before(ab[rank_ + 1]);
+  for (int r = 0; r <= world_; ++r) shard_.pbound[r] = pb[r];
+  p_lo_ = pb[rank_];
+  p_hi_ = pb[rank_ + 1];
   dalloc(&feas_bad_, 1);
   if (world_ == 1) return;
-  {  // owned triples split by where their X3 member lives
-    std::vector<int> loc, rem;
-    for (int a = ab[rank_]; a < ab[rank_ + 1]; ++a)
-      for (int b = a + 1; b < m; ++b)
-        for (int c = b + 1; c < m; ++c) {
-          auto& v = b < ab[rank_ + 1] ? loc : rem;
-          v.push_back(a);
-          v.push_back(b);
-          v.push_back(c);
-        }
-    n_local_ = (int)loc.size() / 3;
-    n_remote_ = (int)rem.size() / 3;
-    dalloc(&tri_local_, loc.size());
-    dalloc(&tri_remote_, rem.size());
-    if (!loc.empty())
-      cuda_check(cudaMemcpy(tri_local_, loc.data(), loc.size() * 4, cudaMemcpyHostToDevice), "H2D");
-    if (!rem.empty())
-      cuda_check(cudaMemcpy(tri_remote_, rem.data(), rem.size() * 4, cudaMemcpyHostToDevice), "H2D");
-    cuda_check(cudaStreamCreateWithFlags(&comm_st_, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaEventCreateWithFlags(&ev_pack_, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&ev_xchg_, cudaEventDisableTiming), "event");
-  }
+  // fold chunks of my locations
+  chunks_me_ = (p_hi_ - p_lo_ + chunk_ - 1) / chunk_;
+  // rows_before[f] = sum over pairs f' < f of b(f')
+  std::vector<int> rb(fpairs_ + 1, 0);
+  for (int i = 0, f = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j, ++f) rb[f + 1] = rb[f] + i;
+  dalloc(&rows_before_, rb.size());
+  cuda_check(cudaMemcpy(rows_before_, rb.data(), rb.size() * 4, cudaMemcpyHostToDevice), "H2D");
+  shard_.rows_before = rows_before_;
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
   nccl_check(nccl().CommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
   std::vector<long long> send, recv;
-  shard_counts(m, ab, rank_, send, recv);
+  shard_counts(m, pb, rank_, send, recv);
   xcount_.assign(2 * world_, 0);
   for (int p = 0; p < world_; ++p) {
-    if (send[p]) {  // lower peer: sigma out, gain in
-      double *a = nullptr, *b = nullptr;
-      dalloc(&a, send[p]);
-      dalloc(&b, send[p]);
-      xbufs_.push_back(a);
-      xbufs_.push_back(b);
-      shard_.sig_send[p] = a;
-      shard_.gain_recv[p] = b;
-      xcount_[p] = send[p];
-    }
-    if (recv[p]) {  // higher peer: sigma in, gain out
-      double *a = nullptr, *b = nullptr;
-      dalloc(&a, recv[p]);
-      dalloc(&b, recv[p]);
-      xbufs_.push_back(a);
-      xbufs_.push_back(b);
-      shard_.sig_recv[p] = a;
-      shard_.gain_send[p] = b;
-      xcount_[world_ + p] = recv[p];
-    }
+    if (p == rank_) continue;
+    double *ss = nullptr, *gr = nullptr, *sr = nullptr, *gs = nullptr;
+    dalloc(&ss, send[p]);  // sigma out / gain in: my X3 cells, p's pa
+    dalloc(&gr, send[p]);
+    dalloc(&sr, recv[p]);  // sigma in / gain out: p's X3 cells, my pa
+    dalloc(&gs, recv[p]);
+    for (double* x : {ss, gr, sr, gs}) xbufs_.push_back(x);
+    shard_.sig_send[p] = ss;
+    shard_.gain_recv[p] = gr;
+    shard_.sig_recv[p] = sr;
+    shard_.gain_send[p] = gs;
+    xcount_[p] = send[p];
+    xcount_[world_ + p] = recv[p];
   }
+  dalloc(&theta_buf_, tiles_);
   dalloc(&shard_dev_, 1);
   cuda_check(cudaMemcpy(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice), "H2D shard");
 }
 
-// Steady sharded Z stage (one exchange per iteration):
-//   sigma of my X3 cells owned by lower ranks' families  -> send buffers
-//   gains of the X3 members of my cross-shard families   -> send buffers
-//   one grouped NCCL send/recv on comm_st_, overlapped with the fold of my
-//   purely local triples; then the X1/X2 updates of the cross-shard
-//   triples, the X3 updates the lower ranks' gains asked for, my Z-LAPs, and
-//   theta re-assembled on every rank.
+// Steady sharded Z stage (location ownership, two exchanges):
+//   sigma of my X3 cells for every peer's pa  -> exchange 1
+//   fold of every triple for my pa chunks (remote X3: sigma in, gain out)
+//   gains for my X3 cells                     <- exchange 2 -> X3 update
+//   Z-LAPs of my tile runs; theta segments re-assembled on every rank.
+void Engine::exchange(bool sigma) {
+  nccl_check(nccl().GroupStart(), "group");
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) continue;
+    double* out = sigma ? shard_.sig_send[p] : shard_.gain_send[p];
+    double* in = sigma ? const_cast<double*>(shard_.sig_recv[p])
+                       : const_cast<double*>(shard_.gain_recv[p]);
+    const long long n_out = sigma ? xcount_[p] : xcount_[world_ + p];
+    const long long n_in = sigma ? xcount_[world_ + p] : xcount_[p];
+    if (n_out) nccl_check(nccl().Send(out, n_out, ncclDouble, p, comm_, st_), "send");
+    if (n_in) nccl_check(nccl().Recv(in, n_in, ncclDouble, p, comm_, st_), "recv");
+  }
+  nccl_check(nccl().GroupEnd(), "group");
+}
+
 void Engine::enqueue_sharded_z(int it) {
   const bool fast = is_fast();
   double* costs = (fast && it > 0) ? incz_ : d_;
@@ -398,60 +345,52 @@ void Engine::enqueue_sharded_z(int it) {
   cuda_check(cudaMemsetAsync(counter_, 0, (S + 2) * sizeof(int), st_), "memset counters");
   if (it > 0) {
     kbegin(QAPB_K_ZFOLD, st_);
-    cuda_check(launch_sigma_pack(m_, piz_, push_, cfg_.kappa_z_upper, shard_, &S_->stop, st_),
+    cuda_check(launch_sigma_pack(m_, piz_, push_, cfg_.kappa_z_upper, shard_, fpair_ij_,
+                                 &S_->stop, st_),
                "sigma pack");
-    FoldParams fr = fold_params(-1);
-    fr.triples = tri_remote_;
-    fr.ntriples = n_remote_;
-    fr.shard = shard_dev_;
-    fr.mode = 1;
-    cuda_check(launch_zfold(fr, st_), "gain pass");
-    cuda_check(cudaEventRecord(ev_pack_, st_), "event");
-    cuda_check(cudaStreamWaitEvent(comm_st_, ev_pack_, 0), "wait");
-    nccl_check(nccl().GroupStart(), "group");
-    for (int p = 0; p < world_; ++p) {
-      if (xcount_[p]) {  // lower peer: sigma out, gain in
-        nccl_check(nccl().Send(shard_.sig_send[p], xcount_[p], ncclDouble, p, comm_, comm_st_),
-                   "send");
-        nccl_check(nccl().Recv(const_cast<double*>(shard_.gain_recv[p]), xcount_[p], ncclDouble,
-                               p, comm_, comm_st_),
-                   "recv");
-      }
-      if (xcount_[world_ + p]) {  // higher peer: sigma in, gain out
-        nccl_check(nccl().Recv(const_cast<double*>(shard_.sig_recv[p]), xcount_[world_ + p],
-                               ncclDouble, p, comm_, comm_st_),
-                   "recv");
-        nccl_check(nccl().Send(shard_.gain_send[p], xcount_[world_ + p], ncclDouble, p, comm_,
-                               comm_st_),
-                   "send");
-      }
-    }
-    nccl_check(nccl().GroupEnd(), "group");
-    cuda_check(cudaEventRecord(ev_xchg_, comm_st_), "event");
-    FoldParams fl = fold_params(-1);  // local triples: no exchange needed
-    fl.triples = tri_local_;
-    fl.ntriples = n_local_;
-    fl.shard = shard_dev_;
-    cuda_check(launch_zfold(fl, st_), "z-fold local");
-    cuda_check(cudaStreamWaitEvent(st_, ev_xchg_, 0), "wait");
-    fr.mode = 2;
-    cuda_check(launch_zfold(fr, st_), "z-fold remote");
-    cuda_check(launch_x3_update(m_, d_, incz_, piz_, cfg_.kappa_z_upper, fast, shard_, &S_->stop,
-                                st_),
+    exchange(true);
+    FoldParams f = fold_params(-1);
+    f.nchunks = chunks_me_;
+    f.shard = shard_dev_;
+    cuda_check(launch_zfold(f, st_), "z-fold");
+    exchange(false);
+    cuda_check(launch_x3_update(m_, d_, incz_, piz_, cfg_.kappa_z_upper, fast, shard_,
+                                fpair_ij_, &S_->stop, st_),
                "x3 update");
     kend(st_);
-    launches_ += 5;
+    launches_ += 3;
   }
-  enqueue_zlap(costs, t_lo_, t_hi_ - t_lo_, theta_, nullptr, S, st_);
+  {  // Z-LAPs of my runs: one run of rl tiles per facility-pair block
+    const int rl = (p_hi_ - p_lo_) * (m_ - 1);
+    BatchLapParams p{};
+    p.costs = costs;
+    p.m = m_ - 2;
+    p.count = fpairs_ * rl;
+    p.counter = counter_ + S;
+    p.stop = &S_->stop;
+    p.stop_w = &S_->stop;
+    p.values = theta_;
+    p.pi = piz_;
+    p.err_tile = &S_->err_tile;
+    p.run_len = rl;
+    p.run_stride = lpairs_;
+    p.run_off = p_lo_ * (m_ - 1);
+    kbegin(QAPB_K_ZLAP, st_);
+    cuda_check(launch_lap_batch(p, st_), "z-stage");
+    kend(st_);
+    ++launches_;
+  }
+  cuda_check(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 1, st_), "theta pack");
   nccl_check(nccl().GroupStart(), "group");
-  for (int r = 0; r < world_; ++r) {
-    const int c = shard_.tbase[r + 1] - shard_.tbase[r];
-    if (c)
-      nccl_check(nccl().Broadcast(theta_ + shard_.tbase[r], theta_ + shard_.tbase[r], c,
-                                  ncclDouble, r, comm_, st_),
-                 "theta broadcast");
+  for (int r = 0, seg = 0; r < world_; ++r) {
+    const int c = fpairs_ * (shard_.pbound[r + 1] - shard_.pbound[r]) * (m_ - 1);
+    nccl_check(nccl().Broadcast(theta_buf_ + seg, theta_buf_ + seg, c, ncclDouble, r, comm_, st_),
+               "theta broadcast");
+    seg += c;
   }
   nccl_check(nccl().GroupEnd(), "group");
+  cuda_check(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 0, st_), "theta unpack");
+  launches_ += 2;
 }
 
 void Engine::plan_pipeline() {
@@ -650,8 +589,8 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   xs.es_window = cfg_.early_stop_window;
   xs.iter_limit = cfg_.iter_limit;
   xs.feas_bad = feas_bad_;
-  xs.zt_lo = t_lo_;
-  xs.zt_hi = t_hi_;
+  xs.zp_lo = p_lo_;
+  xs.zp_hi = p_hi_;
   kbegin(QAPB_K_XSTAGE, st_);
   cuda_check(launch_xstage(xs, st_), "x-stage");
   if (world_ > 1)  // feasibility needs every rank's pi(z) tiles

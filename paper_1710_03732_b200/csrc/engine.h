@@ -115,12 +115,10 @@ class Engine {
   std::vector<double*> xbufs_;  // all exchange buffers (owned)
   std::vector<long long> xcount_;  // doubles per peer in one exchange
   int* feas_bad_ = nullptr;
-  int t_lo_ = 0, t_hi_ = 0, tri_lo_ = 0, tri_hi_ = 0;
-  int* tri_local_ = nullptr;   // owned triples whose X3 member is local
-  int* tri_remote_ = nullptr;  // owned triples whose X3 member lives on a higher rank
-  int n_local_ = 0, n_remote_ = 0;
-  cudaStream_t comm_st_ = nullptr;
-  cudaEvent_t ev_pack_ = nullptr, ev_xchg_ = nullptr;
+  int p_lo_ = 0, p_hi_ = 0, chunks_me_ = 0;  // my first locations / fold chunks
+  int* rows_before_ = nullptr;
+  double* theta_buf_ = nullptr;
+  void exchange(bool sigma);
   void setup_shards(const unsigned char* nccl_id);
   void enqueue_sharded_z(int it);
   void nccl_check(ncclResult_t r, const char* what) const;

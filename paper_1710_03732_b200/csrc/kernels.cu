@@ -115,11 +115,7 @@ struct FamilyCtx {
   int n, nm1, nm2, a, b, c, pa0, Pe, fab, fac, fbc;
   size_t esz;
   int lpairs;
-  // multi-GPU: X3 = T(b,c)[a] lives on rank xr != this rank
-  int xr;                 // -1 when local
-  const double* xsig;     // sigma of the X3 cells, (tile - tbase[xr]) * rows * nm2 + ...
-  double* xgain;          // gain of the X3 cells, same index
-  int xrows, xa0, xtb;    // rows per tile (my facility count), my first facility, tbase[xr]
+  const ShardInfo* sh;  // multi-GPU: X3 members owned by other ranks (null on one GPU)
 };
 
 __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
@@ -131,37 +127,29 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
   f.a = P.triples[3 * T];
   f.b = P.triples[3 * T + 1];
   f.c = P.triples[3 * T + 2];
-  f.pa0 = ch * P.chunk;
-  f.Pe = min(P.chunk, f.n - f.pa0);
+  f.sh = P.shard;
+  const int p_lo = f.sh ? f.sh->pbound[f.sh->rank] : 0;
+  const int p_hi = f.sh ? f.sh->pbound[f.sh->rank + 1] : f.n;
+  f.pa0 = p_lo + ch * P.chunk;
+  f.Pe = min(P.chunk, p_hi - f.pa0);
   const DIdx ix(f.n);
   f.fab = ix.fpair(f.a, f.b);
   f.fac = ix.fpair(f.a, f.c);
   f.fbc = ix.fpair(f.b, f.c);
   f.esz = (size_t)ix.esz;
   f.lpairs = ix.lpairs;
-  f.xr = -1;
-  f.xsig = nullptr;
-  f.xgain = nullptr;
-  f.xrows = f.xa0 = f.xtb = 0;
-  if (P.shard) {
-    const ShardInfo& sh = *P.shard;
-    int r = sh.world - 1;
-    while (r > 0 && f.b < sh.abound[r]) --r;
-    if (r != sh.rank) {
-      f.xr = r;
-      f.xsig = sh.sig_recv[r];
-      f.xgain = sh.gain_send[r];
-      f.xrows = sh.abound[sh.rank + 1] - sh.abound[sh.rank];
-      f.xa0 = sh.abound[sh.rank];
-      f.xtb = sh.tbase[r];
-    }
-  }
   return f;
 }
 
-// exchange-buffer index of X3 cell (tile t, row a, column col) on a remote rank
-__device__ __forceinline__ size_t x3_xindex(const FamilyCtx& f, size_t tile, int col) {
-  return ((tile - (size_t)f.xtb) * f.xrows + (size_t)(f.a - f.xa0)) * f.nm2 + col;
+// exchange-buffer index of X3 cell (row a, location pa) of tile (b,c,pb,pc),
+// owned by rank xb, folded by rank xa (ShardInfo comment)
+__device__ __forceinline__ size_t x3_xindex(const ShardInfo& sh, int n, int fbc, int b, int pb,
+                                            int pc, int a, int pa, int xb, int xa) {
+  const int nm1 = n - 1;
+  const size_t rlB = (size_t)(sh.pbound[xb + 1] - sh.pbound[xb]) * nm1;
+  const int lp_local = pb * nm1 + pc - (pc > pb) - sh.pbound[xb] * nm1;
+  const int nA = sh.pbound[xa + 1] - sh.pbound[xa];
+  return ((rlB * sh.rows_before[fbc] + (size_t)lp_local * b + a) * nA) + (pa - sh.pbound[xa]);
 }
 
 // Visit every member cell of the CTA's families: fn(member, pa_l, pb, pc, g, slot)
@@ -192,9 +180,9 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
       const int other = skip2(r, min(pa, q), max(pa, q));
       const size_t g = (size_t)(fpr * f.lpairs + ix.lpair(pa, q)) * f.esz + rowoff + r;
       if (mem == 0)
-        fn(0, pa_l, q, other, g, e);
+        fn(0, pa_l, q, other, g, e, -1);
       else
-        fn(1, pa_l, other, q, g, base2 + e);
+        fn(1, pa_l, other, q, g, base2 + e, -1);
       r += dr;
       int inc = dsg;
       if (r >= nm2) {
@@ -218,12 +206,19 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
     const int pc = pci + (pci >= pb);
     const int pa = f.pa0 + pa_l;
     if (pa != pb && pa != pc) {
-      const int lo = min(pb, pc), hi = max(pb, pc);
-      const int col = pa - (pa > lo) - (pa > hi);
-      const size_t tile = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc));
-      // local: offset in the z arrays; remote: index in the exchange buffers
-      const size_t g = f.xr < 0 ? tile * f.esz + (size_t)f.a * nm2 + col : x3_xindex(f, tile, col);
-      fn(2, pa_l, pb, pc, g, base3 + e);
+      // X3 lives with owner(pb): local -> offset in the z arrays, remote -> index
+      // in the exchange buffers shared with that rank
+      const int xb = f.sh ? shard_owner(*f.sh, pb) : 0;
+      if (!f.sh || xb == f.sh->rank) {
+        const int lo = min(pb, pc), hi = max(pb, pc);
+        const int col = pa - (pa > lo) - (pa > hi);
+        const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
+                         (size_t)f.a * nm2 + col;
+        fn(2, pa_l, pb, pc, g, base3 + e, -1);
+      } else {
+        fn(2, pa_l, pb, pc, x3_xindex(*f.sh, f.n, f.fbc, f.b, pb, pc, f.a, pa, xb, f.sh->rank),
+           base3 + e, xb);
+      }
     }
     pa_l += dpl;
     int inc = dpr;
@@ -260,17 +255,17 @@ struct FoldSmem {
 __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
                                              const double* __restrict__ piz,
                                              const double* __restrict__ vals, double* sm,
-                                             const FoldSmem& L, int mode = 0) {
+                                             const FoldSmem& L) {
   double* S = sm + L.pi_off();
   double* V = sm + L.val_off();
-  for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
+  for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
     double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
-    if (mem == 2 && f.xr >= 0) {  // remote X3: its owner sent sigma (kz*pi + push)
-      if (mode != 1) cp_async8(sp, f.xsig + g);
+    if (xr >= 0) {  // remote X3: its owner sent sigma (kz*pi + push)
+      cp_async8(sp, f.sh->sig_recv[xr] + g);
       return;
     }
     cp_async8(sp, piz + g);
-    if (mode != 1) cp_async8(V + slot, vals + g);
+    cp_async8(V + slot, vals + g);
   });
 }
 
@@ -288,8 +283,7 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   double* U3 = U2 + C * n;         // [n][n]  push of tile (b,c,pb,pc)
   const DIdx ix(n);
   const int tid = threadIdx.x, bd = blockDim.x;
-  const int mode = P.mode;
-  stage_family(f, C, P.piz, P.d, sm, L, mode);
+  stage_family(f, C, P.piz, P.d, sm, L);
   for (int e = tid; e < f.Pe * n; e += bd) {
     const int pa_l = e / n, q = e - pa_l * n, pa = f.pa0 + pa_l;
     if (q == pa) continue;
@@ -306,20 +300,15 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   double* __restrict__ d = P.d;
   double* __restrict__ incz = P.incz;
   const int fast = P.fast;
-  const bool remote3 = f.xr >= 0;
-  for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
+  for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
     const int fi = (pa_l * n + pb) * L.np + pc;
-    if (mode == 1) {  // gain of the remote X3 member only: phi*sigma1 + phi*sigma2
-      if (mem != 2) return;
-      const double s1 = dadd(dmul(kz, S[fi]), U1[pa_l * n + pb]);
-      const double s2 = dadd(dmul(kz, S[L.cube + fi]), U2[pa_l * n + pc]);
-      f.xgain[g] = dadd(dmul(phi, s1), dmul(phi, s2));
-      return;
-    }
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
     const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
-    const double s3 = remote3 ? p3 : dadd(dmul(kz, p3), U3[pb * n + pc]);
+    // a remote X3 slot holds its owner's sigma; the owner of pb is local iff
+    // the X3 slot is local (this family's X1/X2 use s3 either way)
+    const bool x3_remote = f.sh && shard_owner(*f.sh, pb) != f.sh->rank;
+    const double s3 = x3_remote ? p3 : dadd(dmul(kz, p3), U3[pb * n + pc]);
     double own, gain;  // partners in ascending member order (B, C of rlt2.cpp:280-288)
     if (mem == 0) {
       own = p1;
@@ -331,8 +320,8 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
       own = p3;
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
     }
-    if (mem == 2 && remote3) {  // the X3 owner applies it (x3_update_kernel)
-      if (mode == 0) f.xgain[g] = gain;
+    if (xr >= 0) {  // remote X3: its owner applies the gain (x3_update_kernel)
+      f.sh->gain_send[xr][g] = gain;
       return;
     }
     d[g] = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
@@ -359,7 +348,7 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
   __syncthreads();
   double* __restrict__ costs = P.costs;
   const double tol = 1e-9;
-  for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot) {
+  for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int) {
     const int fi = (pa_l * n + pb) * L.np + pc;
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     double total = 0.0;
@@ -398,10 +387,13 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
     if (lane == 0) x = atomicAdd(P.counter, 1);
     return __shfl_sync(QAPB_FULL, x, 0);
   };
+  auto gtile = [&](int t) {  // launch tile -> global tile (run mapping, multi-GPU)
+    return P.run_len ? (t / P.run_len) * P.run_stride + P.run_off + t % P.run_len : t;
+  };
   auto issue = [&](double* dst, int tile, uint64_t* b) {  // lane 0 only
     fence_proxy_async();
     mbar_expect_tx(b, bytes);
-    bulk_g2s(dst, P.costs + (size_t)tile * esz, bytes, b);
+    bulk_g2s(dst, P.costs + (size_t)gtile(tile) * esz, bytes, b);
   };
   if (use_bulk && lane == 0) {
     mbar_init(&bar[0], 1);
@@ -419,11 +411,12 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
   unsigned phases = 0;
   while (t < P.count) {
     double* cb = cur ? buf1 : buf0;
+    const int tg = gtile(t);  // global tile of launch tile t
     if (use_bulk) {
       mbar_wait(cur ? &bar[1] : &bar[0], (phases >> cur) & 1u);
       phases ^= 1u << cur;
     } else {
-      const double* src = P.costs + (size_t)t * esz;
+      const double* src = P.costs + (size_t)tg * esz;
       for (int e = lane; e < (int)esz; e += 32) cb[e] = src[e];
       __syncwarp();
     }
@@ -431,17 +424,17 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
     LapLane<CPL> L;
     const double value = warp_lap_solve<CPL>(cb, m, lane, L);
     if (lane == 0) {
-      if (P.values) P.values[t] = value;
-      if (P.theta_ref && value < dsub(P.theta_ref[t], 1e-7)) {  // rlt2.cpp:332-335
-        atomicMin(P.err_tile, P.tile_base + t);
+      if (P.values) P.values[tg] = value;
+      if (P.theta_ref && value < dsub(P.theta_ref[tg], 1e-7)) {  // rlt2.cpp:332-335
+        atomicMin(P.err_tile, P.tile_base + tg);
         if (P.stop_w) atomicExch(P.stop_w, 1);
       }
     }
-    warp_lap_write_duals<CPL>(m, lane, L, P.r2c ? P.r2c + (size_t)t * m : nullptr,
-                              P.c2r ? P.c2r + (size_t)t * m : nullptr,
-                              P.u ? P.u + (size_t)t * m : nullptr,
-                              P.v ? P.v + (size_t)t * m : nullptr);
-    if (P.pi) warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)t * esz);
+    warp_lap_write_duals<CPL>(m, lane, L, P.r2c ? P.r2c + (size_t)tg * m : nullptr,
+                              P.c2r ? P.c2r + (size_t)tg * m : nullptr,
+                              P.u ? P.u + (size_t)tg * m : nullptr,
+                              P.v ? P.v + (size_t)tg * m : nullptr);
+    if (P.pi) warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
     __syncwarp();
     if (use_bulk && lane == 0) {  // buffer `cur` is free again
       if (nbuf == 2) {
@@ -546,8 +539,8 @@ __global__ void __launch_bounds__(1024) xstage_kernel(XStageParams P) {
     for (int e = tid; e < m * m * m; e += blockDim.x) {
       const int i = e / (m * m), rem = e - i * m * m, j = rem / m, k = rem - j * m;
       if (!(i < j) || k == i || k == j) continue;
+      if (sx[i] < P.zp_lo || sx[i] >= P.zp_hi) continue;  // tile held by another rank
       const int t = ix.tile(i, j, sx[i], sx[j]);
-      if (t < P.zt_lo || t >= P.zt_hi) continue;
       if (P.piz[(size_t)t * esz + ix.cell(i, j, sx[i], sx[j], k, sx[k])] > tol) feas_bad = 1;
     }
   }
@@ -604,53 +597,72 @@ __global__ void xfinish_kernel(XStageParams P) {
 }
 
 // ---------------------------------------------------------------------------
-// Multi-GPU exchange kernels.  For every lower rank A, the rows a in A's
-// facility range of each tile this rank owns are the X3 members of families
-// A folds.  The rows are contiguous ([abound[A], abound[A+1]) x (n-2) doubles
-// per tile), so both kernels stream them in order.
-__global__ void __launch_bounds__(256) sigma_pack_kernel(int m, const double* __restrict__ piz,
-                                                         const double* __restrict__ push,
-                                                         double kz, ShardInfo sh,
-                                                         const int* stop) {
+// Multi-GPU exchange kernels.  For every other rank A, this rank (the X3
+// owner B) streams, pair block by pair block (one CTA per facility pair
+// f=(b,c)), the rows a<b of its tiles at A's pa columns -- exactly the
+// layout of the exchange buffers, so the buffer side is contiguous.
+template <bool PACK>
+__global__ void __launch_bounds__(256) x3_exchange_kernel(int m, double* __restrict__ d,
+                                                          double* __restrict__ incz,
+                                                          const double* __restrict__ piz,
+                                                          const double* __restrict__ push,
+                                                          double kz, int fast, ShardInfo sh,
+                                                          const int* fpair_ij, const int* stop) {
   if (stop && *stop) return;
-  const int nm2 = m - 2;
+  const int n = m, nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
   const size_t esz = (size_t)nm2 * nm2;
-  const int me = sh.rank, T = sh.tbase[me + 1] - sh.tbase[me];
-  for (int A = 0; A < me; ++A) {
-    const int rows = sh.abound[A + 1] - sh.abound[A];
-    const size_t blk = (size_t)rows * nm2, total = (size_t)T * blk;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
-         e += (size_t)gridDim.x * blockDim.x) {
-      const size_t tl = e / blk, rem = e - tl * blk;
-      const size_t t = (size_t)sh.tbase[me] + tl;
-      const size_t g = t * esz + (size_t)sh.abound[A] * nm2 + rem;
-      sh.sig_send[A][e] = dadd(dmul(kz, piz[g]), push[t]);  // sigma, rlt2.cpp:289-290
+  const double omk = dsub(1.0, kz);
+  const int me = sh.rank, f = blockIdx.x;
+  const int ij = fpair_ij[f], b = ij >> 16;
+  const int p_lo = sh.pbound[me], rl = (sh.pbound[me + 1] - p_lo) * nm1;
+  for (int A = 0; A < sh.world; ++A) {
+    if (A == me) continue;
+    const int a_lo = sh.pbound[A], nA = sh.pbound[A + 1] - a_lo;
+    const size_t base = ((size_t)rl * sh.rows_before[f]) * nA;
+    const int blk = b * nA, total = rl * blk;
+    for (int k = threadIdx.x; k < total; k += blockDim.x) {
+      const int lpl = k / blk, rem = k - lpl * blk, a = rem / nA, pa = a_lo + rem - a * nA;
+      const int lp = p_lo * nm1 + lpl, pb = lp / nm1, qq = lp - pb * nm1;
+      const int pc = qq + (qq >= pb);
+      const size_t xi = base + k;
+      if (pa == pc) {  // hole: location pc cannot host facility a too
+        if (PACK) sh.sig_send[A][xi] = 0.0;
+        continue;
+      }
+      const int lo = min(pb, pc), hi = max(pb, pc);
+      const int col = pa - (pa > lo) - (pa > hi);
+      const size_t t = (size_t)f * lpairs + lp;
+      const size_t g = t * esz + (size_t)a * nm2 + col;
+      if (PACK) {
+        sh.sig_send[A][xi] = dadd(dmul(kz, piz[g]), push[t]);  // sigma, rlt2.cpp:289-290
+      } else {
+        const double gain = sh.gain_recv[A][xi], own = piz[g];
+        d[g] = dadd(d[g], dsub(gain, dmul(kz, own)));     // rlt2.cpp:292
+        if (fast) incz[g] = dadd(dmul(omk, own), gain);  // rlt2.cpp:293
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(256) x3_update_kernel(int m, double* __restrict__ d,
-                                                        double* __restrict__ incz,
-                                                        const double* __restrict__ piz,
-                                                        double kz, int fast, ShardInfo sh,
-                                                        const int* stop) {
-  if (stop && *stop) return;
-  const int nm2 = m - 2;
-  const size_t esz = (size_t)nm2 * nm2;
-  const double omk = dsub(1.0, kz);
-  const int me = sh.rank, T = sh.tbase[me + 1] - sh.tbase[me];
-  for (int A = 0; A < me; ++A) {
-    const int rows = sh.abound[A + 1] - sh.abound[A];
-    const size_t blk = (size_t)rows * nm2, total = (size_t)T * blk;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
-         e += (size_t)gridDim.x * blockDim.x) {
-      const size_t tl = e / blk, rem = e - tl * blk;
-      const size_t g = ((size_t)sh.tbase[me] + tl) * esz + (size_t)sh.abound[A] * nm2 + rem;
-      const double gain = sh.gain_recv[A][e];
-      const double own = piz[g];
-      d[g] = dadd(d[g], dsub(gain, dmul(kz, own)));     // rlt2.cpp:292
-      if (fast) incz[g] = dadd(dmul(omk, own), gain);  // rlt2.cpp:293
+// theta of every rank's tile runs <-> one buffer of rank segments
+__global__ void theta_xfer_kernel(int m, double* theta, double* buf, ShardInfo sh, int pack) {
+  const int nm1 = m - 1, lpairs = m * nm1, fpairs = m * nm1 / 2;
+  size_t seg = 0;
+  for (int r = 0; r < sh.world; ++r) {
+    const int rl = (sh.pbound[r + 1] - sh.pbound[r]) * nm1;
+    const size_t cnt = (size_t)fpairs * rl;
+    if (!pack || r == sh.rank) {
+      for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < cnt;
+           k += (size_t)gridDim.x * blockDim.x) {
+        const size_t f = k / rl, o = k - f * rl;
+        const size_t t = f * lpairs + (size_t)sh.pbound[r] * nm1 + o;
+        if (pack)
+          buf[seg + k] = theta[t];
+        else
+          theta[t] = buf[seg + k];
+      }
     }
+    seg += cnt;
   }
 }
 
@@ -811,16 +823,24 @@ cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
-                              const ShardInfo& sh, const int* stop, cudaStream_t st) {
-  if (sh.rank == 0) return cudaSuccess;
-  sigma_pack_kernel<<<num_sms() * 4, 256, 0, st>>>(m, piz, push, kz, sh, stop);
+                              const ShardInfo& sh, const int* fpair_ij, const int* stop,
+                              cudaStream_t st) {
+  x3_exchange_kernel<true><<<m * (m - 1) / 2, 256, 0, st>>>(
+      m, nullptr, nullptr, piz, push, kz, 0, sh, fpair_ij, stop);
   return cudaGetLastError();
 }
 
 cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
-                             int fast, const ShardInfo& sh, const int* stop, cudaStream_t st) {
-  if (sh.rank == 0) return cudaSuccess;
-  x3_update_kernel<<<num_sms() * 4, 256, 0, st>>>(m, d, incz, piz, kz, fast, sh, stop);
+                             int fast, const ShardInfo& sh, const int* fpair_ij, const int* stop,
+                             cudaStream_t st) {
+  x3_exchange_kernel<false><<<m * (m - 1) / 2, 256, 0, st>>>(
+      m, d, incz, piz, nullptr, kz, fast, sh, fpair_ij, stop);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
+                              cudaStream_t st) {
+  theta_xfer_kernel<<<num_sms(), 256, 0, st>>>(m, theta, buf, sh, pack);
   return cudaGetLastError();
 }
 

@@ -37,22 +37,36 @@ struct BatchLapParams {
   const double* theta_ref;  // optional: phase-2 regression check (rlt2.cpp:332-335)
   int* err_tile;
   int tile_base;            // global index of tile 0 of this launch (error reports)
+  // optional run mapping (multi-GPU): launch tile t is global tile
+  // (t / run_len) * run_stride + run_off + t % run_len
+  int run_len, run_stride, run_off;
 };
 
 constexpr int kMaxRanks = 8;
 
-// Shard description (multi-GPU).  Rank r owns first facilities
-// [abound[r], abound[r+1]) and tiles [tbase[r], tbase[r+1]).
+// Shard description (multi-GPU).  Rank r owns the half-Z
+// tiles whose FIRST location lies in [pbound[r], pbound[r+1]): one run of
+// rl(r) = (pbound[r+1]-pbound[r])*(n-1) tiles inside every facility-pair
+// block.  It folds every facility triple for its own locations pa; in a
+// family the X3 member T(b,c,pb,pc)[a,pa] belongs to owner(pb).  Exchange
+// buffers between X3 owner B and fold owner A hold one double per
+// (pair f=(b,c), B's local location pair, row a<b, pa of A):
+//   index = ((rl(B)*rows_before[f] + lp_local*b + a) * n(A)) + (pa - pbound[A])
 struct ShardInfo {
   int world, rank;
-  int abound[kMaxRanks + 1];
-  int tbase[kMaxRanks + 1];
-  // exchange buffers indexed by peer rank (null where unused)
-  const double* sig_recv[kMaxRanks];   // from higher ranks: sigma of my X3 partners
-  double* gain_send[kMaxRanks];        // to higher ranks: gain of their X3 cells
-  double* sig_send[kMaxRanks];         // to lower ranks
-  const double* gain_recv[kMaxRanks];  // from lower ranks
+  int pbound[kMaxRanks + 1];
+  const int* rows_before;              // [fpairs+1], prefix sums of b over pairs (b<c)
+  const double* sig_recv[kMaxRanks];   // sigma of my families' X3 members, from their owners
+  double* gain_send[kMaxRanks];        // gains for those X3 members, to their owners
+  double* sig_send[kMaxRanks];         // sigma of my X3 cells, to the fold owners
+  const double* gain_recv[kMaxRanks];  // gains for my X3 cells, from the fold owners
 };
+
+__host__ __device__ inline int shard_owner(const ShardInfo& sh, int p) {
+  int r = sh.world - 1;
+  while (r > 0 && p < sh.pbound[r]) --r;
+  return r;
+}
 
 struct FoldParams {
   int m;
@@ -69,11 +83,7 @@ struct FoldParams {
   const int* stop;
   // phase 2 (rlt2.cpp:344-381): costs mutated in place from pi(z)
   double* costs;
-  const ShardInfo* shard;  // null on one GPU
-  // multi-GPU passes over triples whose X3 member is remote (owner(b) != me):
-  // 0 whole fold, 1 gains of the X3 members only (before the exchange),
-  // 2 X1/X2 updates with the received sigma (after it)
-  int mode;
+  const ShardInfo* shard;  // null on one GPU: the CTA's pa chunk comes from the rank's range
 };
 
 struct XYFoldParams {
@@ -121,7 +131,7 @@ struct XStageParams {
   double upper_bound, min_gap, fathom, es_delta;
   int es_window, iter_limit;
   int* feas_bad;           // device flag: 1 if any induced slack > 1e-7
-  int zt_lo, zt_hi;        // tiles whose pi(z) this rank checks (feasibility)
+  int zp_lo, zp_hi;        // first locations of the pi(z) tiles this rank checks
 };
 
 // ---- launches (all asynchronous on `st`) ----
@@ -137,9 +147,14 @@ cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st);
 cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
 // multi-GPU exchange kernels
 cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
-                              const ShardInfo& sh, const int* stop, cudaStream_t st);
+                              const ShardInfo& sh, const int* fpair_ij, const int* stop,
+                              cudaStream_t st);
 cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
-                             int fast, const ShardInfo& sh, const int* stop, cudaStream_t st);
+                             int fast, const ShardInfo& sh, const int* fpair_ij, const int* stop,
+                             cudaStream_t st);
+// theta of every rank's tile runs <-> one contiguous buffer (rank segments)
+cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
+                              cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
                             DevScalars* S, double drained, int fast, cudaStream_t st);
 

@@ -74,7 +74,7 @@ lib.qapb_engine_create_instance_sharded.argtypes = [C.c_int, _vp, _vp, _vp, _P(C
 
 
 def shard_plan(n: int, world: int) -> List[int]:
-    """First-facility boundaries per rank (world+1 entries), SURVEY.md §8(e)."""
+    """First-location boundaries per rank (world+1 entries), SURVEY.md §8(e)."""
     b = np.zeros(world + 1, np.int32)
     _check(lib.qapb_shard_plan(n, world, iptr(b)))
     return [int(x) for x in b]
