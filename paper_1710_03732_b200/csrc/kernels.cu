@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(256) x3_exchange_kernel(int m, double* __restr
   const size_t esz = (size_t)nm2 * nm2;
   const double omk = dsub(1.0, kz);
   const int me = sh.rank, f = blockIdx.x;
-  const int ij = fpair_ij[f], b = ij >> 16;
+  const int b = fpair_ij[f] & 0xffff;  // first facility of pair f = (b,c)
   const int p_lo = sh.pbound[me], rl = (sh.pbound[me + 1] - p_lo) * nm1;
   for (int A = 0; A < sh.world; ++A) {
     if (A == me) continue;
