@@ -615,12 +615,17 @@ __global__ void __launch_bounds__(256) x3_exchange_kernel(int m, double* __restr
   const int me = sh.rank, f = blockIdx.x;
   const int b = fpair_ij[f] & 0xffff;  // first facility of pair f = (b,c)
   const int p_lo = sh.pbound[me], rl = (sh.pbound[me + 1] - p_lo) * nm1;
+  // grid.y splits the pair block's rl location pairs (work grows with b)
+  const int lpb = (rl + gridDim.y - 1) / gridDim.y;
+  const int l0 = blockIdx.y * lpb, l1 = min(rl, l0 + lpb);
+  if (l0 >= l1 || b == 0) return;
   for (int A = 0; A < sh.world; ++A) {
     if (A == me) continue;
     const int a_lo = sh.pbound[A], nA = sh.pbound[A + 1] - a_lo;
     const size_t base = ((size_t)rl * sh.rows_before[f]) * nA;
-    const int blk = b * nA, total = rl * blk;
-    for (int k = threadIdx.x; k < total; k += blockDim.x) {
+    const int blk = b * nA, k0 = l0 * blk, total = (l1 - l0) * blk;
+    for (int kk = threadIdx.x; kk < total; kk += blockDim.x) {
+      const int k = k0 + kk;
       const int lpl = k / blk, rem = k - lpl * blk, a = rem / nA, pa = a_lo + rem - a * nA;
       const int lp = p_lo * nm1 + lpl, pb = lp / nm1, qq = lp - pb * nm1;
       const int pc = qq + (qq >= pb);
@@ -825,7 +830,7 @@ cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
 cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
                               const ShardInfo& sh, const int* fpair_ij, const int* stop,
                               cudaStream_t st) {
-  x3_exchange_kernel<true><<<m * (m - 1) / 2, 256, 0, st>>>(
+  x3_exchange_kernel<true><<<dim3(m * (m - 1) / 2, 16), 256, 0, st>>>(
       m, nullptr, nullptr, piz, push, kz, 0, sh, fpair_ij, stop);
   return cudaGetLastError();
 }
@@ -833,7 +838,7 @@ cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, doub
 cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
                              int fast, const ShardInfo& sh, const int* fpair_ij, const int* stop,
                              cudaStream_t st) {
-  x3_exchange_kernel<false><<<m * (m - 1) / 2, 256, 0, st>>>(
+  x3_exchange_kernel<false><<<dim3(m * (m - 1) / 2, 16), 256, 0, st>>>(
       m, d, incz, piz, nullptr, kz, fast, sh, fpair_ij, stop);
   return cudaGetLastError();
 }
