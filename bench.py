@@ -65,6 +65,7 @@ def kernel_bytes(n: int, variant: str):
         "ystage": ny * (8 + 8) + 8 * t,
         "phase2": nz * (8 + 16),
         "xstage": n * n * 8 * 4,
+        "xchg": 0,  # multi-GPU only: barrier + theta exchange (NCCL)
     }
 
 

@@ -225,7 +225,8 @@ enum {
   QAPB_K_PHASE2 = 3,  /* stage_z_second_phase,     rlt2.cpp:344-381 */
   QAPB_K_YSTAGE = 4,  /* stage_y,                  rlt2.cpp:383-426 */
   QAPB_K_XSTAGE = 5,  /* stage_x + feasibility,    rlt2.cpp:428-473 */
-  QAPB_K_COUNT = 6
+  QAPB_K_XCHG = 6,    /* multi-GPU: cross-rank barrier + theta segment exchange */
+  QAPB_K_COUNT = 7
 };
 QAPB_API qapb_status qapb_engine_enqueue(qapb_engine* e, int iters);
 QAPB_API qapb_status qapb_engine_synchronize(qapb_engine* e);

@@ -218,11 +218,17 @@ Engine::~Engine() {
   dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
   dfree(fpair_ij_); dfree(counter_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
   if (hSpin_) cudaFreeHost(hSpin_);
+  for (void* p : peer_maps_) cudaIpcCloseMemHandle(p);
+  if (comm_ && barrier_) {  // no peer may still map my receive buffers
+    barrier();
+    cudaStreamSynchronize(st_);
+  }
   for (auto* p : xbufs_) cudaFree(p);
   if (shard_dev_) cudaFree(shard_dev_);
   if (feas_bad_) cudaFree(feas_bad_);
   if (comm_) nccl().CommDestroy(comm_);
   if (rows_before_) cudaFree(rows_before_);
+  if (barrier_) cudaFree(barrier_);
   if (theta_buf_) cudaFree(theta_buf_);
   for (auto e : stage_ev_) cudaEventDestroy(e);
   if (join_ev_) cudaEventDestroy(join_ev_);
@@ -295,47 +301,73 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
   nccl_check(nccl().CommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
+  shard_.chunk = chunk_;
+  shard_.fence = env_int("QAPB_FENCE", 0);
+  // Receive buffers live here; peers write them directly over NVLink through
+  // CUDA IPC mappings (sigma from X3 owners, gains from fold owners).
   std::vector<long long> send, recv;
   shard_counts(m, pb, rank_, send, recv);
   xcount_.assign(2 * world_, 0);
+  std::vector<cudaIpcMemHandle_t> mine(2 * world_);
   for (int p = 0; p < world_; ++p) {
     if (p == rank_) continue;
-    double *ss = nullptr, *gr = nullptr, *sr = nullptr, *gs = nullptr;
-    dalloc(&ss, send[p]);  // sigma out / gain in: my X3 cells, p's pa
-    dalloc(&gr, send[p]);
-    dalloc(&sr, recv[p]);  // sigma in / gain out: p's X3 cells, my pa
-    dalloc(&gs, recv[p]);
-    for (double* x : {ss, gr, sr, gs}) xbufs_.push_back(x);
-    shard_.sig_send[p] = ss;
-    shard_.gain_recv[p] = gr;
+    double *sr = nullptr, *gr = nullptr;
+    dalloc(&sr, recv[p]);                                         // sigma from p
+    dalloc(&gr, shard_gain_count(shard_, m, p, rank_));           // gains from p
+    xbufs_.push_back(sr);
+    xbufs_.push_back(gr);
     shard_.sig_recv[p] = sr;
-    shard_.gain_send[p] = gs;
+    shard_.gain_recv[p] = gr;
+    cuda_check(cudaIpcGetMemHandle(&mine[2 * p], sr), "cudaIpcGetMemHandle");
+    cuda_check(cudaIpcGetMemHandle(&mine[2 * p + 1], gr), "cudaIpcGetMemHandle");
     xcount_[p] = send[p];
     xcount_[world_ + p] = recv[p];
   }
+  // all-gather every rank's handle table through NCCL
+  const size_t hb = sizeof(cudaIpcMemHandle_t) * 2 * world_;
+  unsigned char *dh = nullptr, *dall = nullptr;
+  dalloc(&dh, hb);
+  dalloc(&dall, hb * world_);
+  cuda_check(cudaMemcpy(dh, mine.data(), hb, cudaMemcpyHostToDevice), "H2D handles");
+  nccl_check(nccl().AllGather(dh, dall, hb, ncclUint8, comm_, st_), "allgather handles");
+  std::vector<cudaIpcMemHandle_t> all(2 * world_ * world_);
+  cuda_check(cudaMemcpyAsync(all.data(), dall, hb * world_, cudaMemcpyDeviceToHost, st_), "D2H");
+  cuda_check(cudaStreamSynchronize(st_), "handles");
+  cudaFree(dh);
+  cudaFree(dall);
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) continue;
+    void *sp = nullptr, *gp = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&sp, all[(size_t)p * 2 * world_ + 2 * rank_],
+                                    cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle");
+    cuda_check(cudaIpcOpenMemHandle(&gp, all[(size_t)p * 2 * world_ + 2 * rank_ + 1],
+                                    cudaIpcMemLazyEnablePeerAccess),
+               "cudaIpcOpenMemHandle");
+    shard_.sig_send[p] = static_cast<double*>(sp);   // p's sigma buffer for my X3 cells
+    shard_.gain_send[p] = static_cast<double*>(gp);  // p's gain buffer for my families
+    peer_maps_.push_back(sp);
+    peer_maps_.push_back(gp);
+  }
+  dalloc(&barrier_, 1);
   dalloc(&theta_buf_, tiles_);
   dalloc(&shard_dev_, 1);
   cuda_check(cudaMemcpy(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice), "H2D shard");
 }
 
-// Steady sharded Z stage (location ownership, two exchanges):
-//   sigma of my X3 cells for every peer's pa  -> exchange 1
-//   fold of every triple for my pa chunks (remote X3: sigma in, gain out)
-//   gains for my X3 cells                     <- exchange 2 -> X3 update
-//   Z-LAPs of my tile runs; theta segments re-assembled on every rank.
-void Engine::exchange(bool sigma) {
-  nccl_check(nccl().GroupStart(), "group");
-  for (int p = 0; p < world_; ++p) {
-    if (p == rank_) continue;
-    double* out = sigma ? shard_.sig_send[p] : shard_.gain_send[p];
-    double* in = sigma ? const_cast<double*>(shard_.sig_recv[p])
-                       : const_cast<double*>(shard_.gain_recv[p]);
-    const long long n_out = sigma ? xcount_[p] : xcount_[world_ + p];
-    const long long n_in = sigma ? xcount_[world_ + p] : xcount_[p];
-    if (n_out) nccl_check(nccl().Send(out, n_out, ncclDouble, p, comm_, st_), "send");
-    if (n_in) nccl_check(nccl().Recv(in, n_in, ncclDouble, p, comm_, st_), "recv");
-  }
-  nccl_check(nccl().GroupEnd(), "group");
+// Steady sharded Z stage (location ownership, transfers fused into kernels
+// over NVLink peer memory):
+//   fold of every triple for my pa chunks; remote X3 gains are stored into
+//   their owners' buffers; barrier;
+//   Z-LAPs of my tile runs: remote-folded X3 cells patched from the received
+//   gains before solving, kz * slack of those cells stored into the fold
+//   owners' sigma buffers after solving;
+//   theta segments re-assembled on every rank (this collective is also the
+//   barrier that orders those sigma stores before the next fold).
+// Cross-rank barrier on the engine stream: after it, every rank's earlier
+// kernels (and their fenced peer stores) are complete.
+void Engine::barrier() {
+  nccl_check(nccl().AllReduce(barrier_, barrier_, 1, ncclInt, ncclMax, comm_, st_), "barrier");
 }
 
 void Engine::enqueue_sharded_z(int it) {
@@ -344,21 +376,16 @@ void Engine::enqueue_sharded_z(int it) {
   const int S = (int)stage_ev_.size();
   cuda_check(cudaMemsetAsync(counter_, 0, (S + 2) * sizeof(int), st_), "memset counters");
   if (it > 0) {
-    kbegin(QAPB_K_ZFOLD, st_);
-    cuda_check(launch_sigma_pack(m_, piz_, push_, cfg_.kappa_z_upper, shard_, fpair_ij_,
-                                 &S_->stop, st_),
-               "sigma pack");
-    exchange(true);
     FoldParams f = fold_params(-1);
     f.nchunks = chunks_me_;
     f.shard = shard_dev_;
+    kbegin(QAPB_K_ZFOLD, st_);
     cuda_check(launch_zfold(f, st_), "z-fold");
-    exchange(false);
-    cuda_check(launch_x3_update(m_, d_, incz_, piz_, cfg_.kappa_z_upper, fast, shard_,
-                                fpair_ij_, &S_->stop, st_),
-               "x3 update");
     kend(st_);
-    launches_ += 3;
+    kbegin(QAPB_K_XCHG, st_);
+    barrier();  // gains have landed in every X3 owner's buffer
+    kend(st_);
+    ++launches_;
   }
   {  // Z-LAPs of my runs: one run of rl tiles per facility-pair block
     const int rl = (p_hi_ - p_lo_) * (m_ - 1);
@@ -375,11 +402,19 @@ void Engine::enqueue_sharded_z(int it) {
     p.run_len = rl;
     p.run_stride = lpairs_;
     p.run_off = p_lo_ * (m_ - 1);
+    p.sh = shard_dev_;
+    p.fpair_ij = fpair_ij_;
+    p.d = d_;
+    p.incz = incz_;
+    p.kz = cfg_.kappa_z_upper;
+    p.fast = fast ? 1 : 0;
+    p.patch = it > 0 ? 1 : 0;
     kbegin(QAPB_K_ZLAP, st_);
     cuda_check(launch_lap_batch(p, st_), "z-stage");
     kend(st_);
     ++launches_;
   }
+  kbegin(QAPB_K_XCHG, st_);
   cuda_check(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 1, st_), "theta pack");
   nccl_check(nccl().GroupStart(), "group");
   for (int r = 0, seg = 0; r < world_; ++r) {
@@ -390,6 +425,7 @@ void Engine::enqueue_sharded_z(int it) {
   }
   nccl_check(nccl().GroupEnd(), "group");
   cuda_check(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 0, st_), "theta unpack");
+  kend(st_);
   launches_ += 2;
 }
 

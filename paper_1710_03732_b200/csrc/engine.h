@@ -118,7 +118,9 @@ class Engine {
   int p_lo_ = 0, p_hi_ = 0, chunks_me_ = 0;  // my first locations / fold chunks
   int* rows_before_ = nullptr;
   double* theta_buf_ = nullptr;
-  void exchange(bool sigma);
+  void barrier();
+  std::vector<void*> peer_maps_;  // IPC-mapped peer receive buffers
+  int* barrier_ = nullptr;
   void setup_shards(const unsigned char* nccl_id);
   void enqueue_sharded_z(int it);
   void nccl_check(ncclResult_t r, const char* what) const;

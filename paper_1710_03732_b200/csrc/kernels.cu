@@ -260,7 +260,7 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
   double* V = sm + L.val_off();
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
     double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
-    if (xr >= 0) {  // remote X3: its owner sent sigma (kz*pi + push)
+    if (xr >= 0) {  // remote X3: its owner's Z-LAP stored kz*pi
       cp_async8(sp, f.sh->sig_recv[xr] + g);
       return;
     }
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
     // a remote X3 slot holds its owner's sigma; the owner of pb is local iff
     // the X3 slot is local (this family's X1/X2 use s3 either way)
     const bool x3_remote = f.sh && shard_owner(*f.sh, pb) != f.sh->rank;
-    const double s3 = x3_remote ? p3 : dadd(dmul(kz, p3), U3[pb * n + pc]);
+    const double s3 = dadd(x3_remote ? p3 : dmul(kz, p3), U3[pb * n + pc]);
     double own, gain;  // partners in ascending member order (B, C of rlt2.cpp:280-288)
     if (mem == 0) {
       own = p1;
@@ -320,13 +320,19 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
       own = p3;
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
     }
-    if (xr >= 0) {  // remote X3: its owner applies the gain (x3_update_kernel)
-      f.sh->gain_send[xr][g] = gain;
+    if (xr >= 0) {  // remote X3: store the gain straight into its owner's buffer (NVLink)
+      const ShardInfo& sh = *f.sh;
+      const int nB = sh.pbound[xr + 1] - sh.pbound[xr];
+      const int pci = pc - (pc > pb);
+      const size_t gi = (size_t)blockIdx.x * nB * (n - 1) * C +
+                        ((size_t)(pb - sh.pbound[xr]) * (n - 1) + pci) * C + pa_l;
+      sh.gain_send[xr][gi] = gain;
       return;
     }
     d[g] = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
     if (fast) incz[g] = dadd(dmul(omk, own), gain);   // rlt2.cpp:293
   });
+  if (P.shard && P.shard->fence) __threadfence_system();  // peer stores before the cross-rank barrier
   if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
     P.sa_fac[tid] = 0.0;
     P.sa_loc[tid] = 0.0;
@@ -368,8 +374,50 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
 // Persistent CTAs; each warp pulls tiles from a global counter and
 // double-buffers them in shared memory with TMA bulk copies
 // (cp.async.bulk + mbarrier), prefetching tile k+1 while solving tile k.
+// Per-tile view of a sharded Z tile (b,c,pb,pc) for the fused X3 exchange:
+// rows a < b are X3 members of families (a,b,c) whose fold owner is
+// owner(pa) of the column's location pa.
+struct X3Lane {
+  const double* gsrc = nullptr;  // gain of row a: gsrc[T(a,b,c) * gstride] (null: local column)
+  double* sdst = nullptr;        // sigma of row a: sdst[a * nA] (fold owner's buffer, peer)
+  size_t gstride = 0;
+  int nA = 0;
+};
+
 template <int CPL>
-__global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
+__device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_ij, int n, int tg,
+                                         int lane, X3Lane (&X)[CPL], int& b, long long& tb) {
+  const int nm1 = n - 1, m = n - 2, lpairs = n * nm1;
+  const int f = tg / lpairs, lp = tg - f * lpairs;
+  const int ij = fpair_ij[f];
+  b = ij & 0xffff;
+  const int c = ij >> 16;
+  const int pb = lp / nm1, qq = lp - pb * nm1, pc = qq + (qq >= pb);
+  const int lo = min(pb, pc), hi = max(pb, pc);
+  const int me = sh.rank, p_lo = sh.pbound[me], nB = sh.pbound[me + 1] - p_lo;
+  const int pci = pc - (pc > pb);
+  // T(a,b,c) = tri(a+1) - C(n-b,2) + (c-b-1), tri(x) = C(n,3) - C(n-x,3)
+  tb = (long long)n * (n - 1) * (n - 2) / 6 - (long long)(n - b) * (n - b - 1) / 2 + (c - b - 1);
+  const size_t rows_base = (size_t)nB * nm1 * sh.rows_before[f] + (size_t)(lp - p_lo * nm1) * b;
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = s * 32 + lane;
+    X[s].gsrc = nullptr;
+    if (j >= m) continue;
+    const int pa = skip2(j, lo, hi);
+    const int A = shard_owner(sh, pa);
+    if (A == me) continue;
+    const int a_lo = sh.pbound[A], po = pa - a_lo, ch = po / sh.chunk;
+    X[s].nA = sh.pbound[A + 1] - a_lo;
+    X[s].gstride = (size_t)shard_chunks(sh, A) * nB * nm1 * sh.chunk;
+    X[s].gsrc = sh.gain_recv[A] + (size_t)ch * nB * nm1 * sh.chunk +
+                ((size_t)(pb - p_lo) * nm1 + pci) * sh.chunk + (po - ch * sh.chunk);
+    X[s].sdst = sh.sig_send[A] + rows_base * X[s].nA + po;
+  }
+}
+
+template <int CPL, bool SH>
+__global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
                                                         int buf_elems, int use_bulk, int nbuf) {
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -421,6 +469,60 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
       __syncwarp();
     }
     const int tnn = grab();
+    X3Lane X[CPL];
+    int xb = 0;
+    long long tb = 0;
+    if constexpr (SH) {
+      const ShardInfo& sh = *P.sh;
+      const int n = m + 2;
+      x3_lanes<CPL>(sh, P.fpair_ij, n, tg, lane, X, xb, tb);
+      if (P.patch) {  // fold owners' gains -> D' / incremental costs (rlt2.cpp:292-293)
+        // rows in groups of 4 with all loads issued before any store: the
+        // patch is latency-bound, this keeps 12 loads per lane in flight
+        const double kz = P.kz, omk = dsub(1.0, P.kz);
+        double* __restrict__ dg = P.d + (size_t)tg * esz;
+        double* __restrict__ ig = P.incz + (size_t)tg * esz;
+        const double* __restrict__ pg = P.pi + (size_t)tg * esz;
+        for (int a0 = 0; a0 < xb; a0 += 4) {
+          double gn[4][CPL], ow[4][CPL], dv[4][CPL];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int a = a0 + u;
+            // T(a,b,c) = tb - C(n-a-1, 3)
+            const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
+#pragma unroll
+            for (int s = 0; s < CPL; ++s) {
+              const int j = s * 32 + lane;
+              if (a < xb && X[s].gsrc) {
+                gn[u][s] = __ldg(X[s].gsrc + (size_t)T * X[s].gstride);
+                ow[u][s] = pg[a * m + j];
+                dv[u][s] = dg[a * m + j];
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int a = a0 + u;
+#pragma unroll
+            for (int s = 0; s < CPL; ++s) {
+              const int j = s * 32 + lane;
+              if (a < xb && X[s].gsrc) {
+                const double dn = dadd(dv[u][s], dsub(gn[u][s], dmul(kz, ow[u][s])));
+                dg[a * m + j] = dn;
+                if (P.fast) {
+                  const double inc = dadd(dmul(omk, ow[u][s]), gn[u][s]);
+                  ig[a * m + j] = inc;
+                  cb[a * m + j] = inc;
+                } else {
+                  cb[a * m + j] = dn;
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
     LapLane<CPL> L;
     const double value = warp_lap_solve<CPL>(cb, m, lane, L);
     if (lane == 0) {
@@ -434,7 +536,22 @@ __global__ void __launch_bounds__(256) lap_batch_kernel(BatchLapParams P, unsign
                               P.c2r ? P.c2r + (size_t)tg * m : nullptr,
                               P.u ? P.u + (size_t)tg * m : nullptr,
                               P.v ? P.v + (size_t)tg * m : nullptr);
-    if (P.pi) warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
+    if constexpr (SH) {
+      warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
+      // sigma (without push) of my remote-folded X3 cells -> fold owners (rlt2.cpp:289)
+      for (int a = 0; a < xb; ++a) {
+        const double ua = urow[a];
+#pragma unroll
+        for (int s = 0; s < CPL; ++s) {
+          if (!X[s].gsrc) continue;
+          const int j = s * 32 + lane;
+          const double sl = dsub(dsub(cb[a * m + j], ua), L.v[s]);
+          X[s].sdst[(size_t)a * X[s].nA] = dmul(P.kz, sl);
+        }
+      }
+    } else if (P.pi) {
+      warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
+    }
     __syncwarp();
     if (use_bulk && lane == 0) {  // buffer `cur` is free again
       if (nbuf == 2) {
@@ -596,59 +713,6 @@ __global__ void xfinish_kernel(XStageParams P) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// Multi-GPU exchange kernels.  For every other rank A, this rank (the X3
-// owner B) streams, pair block by pair block (one CTA per facility pair
-// f=(b,c)), the rows a<b of its tiles at A's pa columns -- exactly the
-// layout of the exchange buffers, so the buffer side is contiguous.
-template <bool PACK>
-__global__ void __launch_bounds__(256) x3_exchange_kernel(int m, double* __restrict__ d,
-                                                          double* __restrict__ incz,
-                                                          const double* __restrict__ piz,
-                                                          const double* __restrict__ push,
-                                                          double kz, int fast, ShardInfo sh,
-                                                          const int* fpair_ij, const int* stop) {
-  if (stop && *stop) return;
-  const int n = m, nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
-  const size_t esz = (size_t)nm2 * nm2;
-  const double omk = dsub(1.0, kz);
-  const int me = sh.rank, f = blockIdx.x;
-  const int b = fpair_ij[f] & 0xffff;  // first facility of pair f = (b,c)
-  const int p_lo = sh.pbound[me], rl = (sh.pbound[me + 1] - p_lo) * nm1;
-  // grid.y splits the pair block's rl location pairs (work grows with b)
-  const int lpb = (rl + gridDim.y - 1) / gridDim.y;
-  const int l0 = blockIdx.y * lpb, l1 = min(rl, l0 + lpb);
-  if (l0 >= l1 || b == 0) return;
-  for (int A = 0; A < sh.world; ++A) {
-    if (A == me) continue;
-    const int a_lo = sh.pbound[A], nA = sh.pbound[A + 1] - a_lo;
-    const size_t base = ((size_t)rl * sh.rows_before[f]) * nA;
-    const int blk = b * nA, k0 = l0 * blk, total = (l1 - l0) * blk;
-    for (int kk = threadIdx.x; kk < total; kk += blockDim.x) {
-      const int k = k0 + kk;
-      const int lpl = k / blk, rem = k - lpl * blk, a = rem / nA, pa = a_lo + rem - a * nA;
-      const int lp = p_lo * nm1 + lpl, pb = lp / nm1, qq = lp - pb * nm1;
-      const int pc = qq + (qq >= pb);
-      const size_t xi = base + k;
-      if (pa == pc) {  // hole: location pc cannot host facility a too
-        if (PACK) sh.sig_send[A][xi] = 0.0;
-        continue;
-      }
-      const int lo = min(pb, pc), hi = max(pb, pc);
-      const int col = pa - (pa > lo) - (pa > hi);
-      const size_t t = (size_t)f * lpairs + lp;
-      const size_t g = t * esz + (size_t)a * nm2 + col;
-      if (PACK) {
-        sh.sig_send[A][xi] = dadd(dmul(kz, piz[g]), push[t]);  // sigma, rlt2.cpp:289-290
-      } else {
-        const double gain = sh.gain_recv[A][xi], own = piz[g];
-        d[g] = dadd(d[g], dsub(gain, dmul(kz, own)));     // rlt2.cpp:292
-        if (fast) incz[g] = dadd(dmul(omk, own), gain);  // rlt2.cpp:293
-      }
-    }
-  }
-}
-
 // theta of every rank's tile runs <-> one buffer of rank segments
 __global__ void theta_xfer_kernel(int m, double* theta, double* buf, ShardInfo sh, int pack) {
   const int nm1 = m - 1, lpairs = m * nm1, fpairs = m * nm1 / 2;
@@ -758,15 +822,16 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const int wmax = std::max(1, std::min(8, env_int("QAPB_LAP_WARPS", 8)));
   int W = (int)std::max<size_t>(1, std::min<size_t>(wmax, (110 * 1024) / warp_smem));
   const size_t smem = warp_smem * W;
-  cudaFuncSetAttribute(lap_batch_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = p.sh ? lap_batch_kernel<CPL, true> : lap_batch_kernel<CPL, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lap_batch_kernel<CPL>, 32 * W, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem);
   if (per_sm < 1) per_sm = 1;
   const int need = (p.count + W - 1) / W;
   const int blocks = std::max(1, std::min(need, per_sm * num_sms()));
-  lap_batch_kernel<CPL><<<blocks, 32 * W, smem, st>>>(p, (unsigned)warp_smem, (int)buf_elems,
-                                                       use_bulk ? 1 : 0, nbuf);
+  kern<<<blocks, 32 * W, smem, st>>>(p, (unsigned)warp_smem, (int)buf_elems, use_bulk ? 1 : 0,
+                                     nbuf);
   return cudaGetLastError();
 }
 
@@ -824,22 +889,6 @@ cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st) {
 
 cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
   xfinish_kernel<<<1, 64, 0, st>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
-                              const ShardInfo& sh, const int* fpair_ij, const int* stop,
-                              cudaStream_t st) {
-  x3_exchange_kernel<true><<<dim3(m * (m - 1) / 2, 16), 256, 0, st>>>(
-      m, nullptr, nullptr, piz, push, kz, 0, sh, fpair_ij, stop);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
-                             int fast, const ShardInfo& sh, const int* fpair_ij, const int* stop,
-                             cudaStream_t st) {
-  x3_exchange_kernel<false><<<dim3(m * (m - 1) / 2, 16), 256, 0, st>>>(
-      m, d, incz, piz, nullptr, kz, fast, sh, fpair_ij, stop);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,8 @@ struct DevScalars {
   int pad;
 };
 
+struct ShardInfo;
+
 struct BatchLapParams {
   const double* costs;  // count tiles of m*m, contiguous
   int m, count;
@@ -40,6 +42,15 @@ struct BatchLapParams {
   // optional run mapping (multi-GPU): launch tile t is global tile
   // (t / run_len) * run_stride + run_off + t % run_len
   int run_len, run_stride, run_off;
+  // multi-GPU Z stage (location sharding), null on one GPU: the LAP kernel
+  // applies the fold owners' gains to its remote-folded X3 cells before
+  // solving (patch) and stores kz * slack of those cells straight into the
+  // fold owners' sigma buffers after solving (NVLink peer stores)
+  const ShardInfo* sh;
+  const int* fpair_ij;
+  double *d, *incz;
+  double kz;
+  int fast, patch;
 };
 
 constexpr int kMaxRanks = 8;
@@ -52,15 +63,35 @@ constexpr int kMaxRanks = 8;
 // buffers between X3 owner B and fold owner A hold one double per
 // (pair f=(b,c), B's local location pair, row a<b, pa of A):
 //   index = ((rl(B)*rows_before[f] + lp_local*b + a) * n(A)) + (pa - pbound[A])
+//
+// The buffers live on the RECEIVING rank and are written by the sender
+// through CUDA IPC peer mappings over NVLink (no separate copy step):
+//   sigma (X3 owner B -> fold owner A): the layout above, so B's pack kernel
+//     stores whole row segments; A's fold reads it.
+//   gain (A -> B): fold order, so each fold CTA stores one contiguous block;
+//     slot = (T*nch(A) + chunk) * n(B)*(n-1)*chunk_cap
+//            + ((pb - pbound[B])*(n-1) + pci)*chunk_cap + pa_l,
+//     T = lexicographic triple index; B's X3 update reads it.
 struct ShardInfo {
   int world, rank;
   int pbound[kMaxRanks + 1];
+  int chunk;                           // fold chunk capacity (pa values per CTA)
+  int fence;                           // system fence after peer stores (QAPB_FENCE)
   const int* rows_before;              // [fpairs+1], prefix sums of b over pairs (b<c)
-  const double* sig_recv[kMaxRanks];   // sigma of my families' X3 members, from their owners
-  double* gain_send[kMaxRanks];        // gains for those X3 members, to their owners
-  double* sig_send[kMaxRanks];         // sigma of my X3 cells, to the fold owners
-  const double* gain_recv[kMaxRanks];  // gains for my X3 cells, from the fold owners
+  const double* sig_recv[kMaxRanks];   // local: sigma of my families' X3 members, from owner
+  double* gain_send[kMaxRanks];        // PEER: owner's gain buffer for my families
+  double* sig_send[kMaxRanks];         // PEER: fold owner's sigma buffer for my X3 cells
+  const double* gain_recv[kMaxRanks];  // local: gains for my X3 cells, from each fold owner
 };
+
+__host__ __device__ inline int shard_chunks(const ShardInfo& sh, int r) {
+  return (sh.pbound[r + 1] - sh.pbound[r] + sh.chunk - 1) / sh.chunk;
+}
+__host__ __device__ inline long long shard_gain_count(const ShardInfo& sh, int n, int A, int B) {
+  const long long tri = (long long)n * (n - 1) * (n - 2) / 6;
+  return tri * shard_chunks(sh, A) * (long long)(sh.pbound[B + 1] - sh.pbound[B]) * (n - 1) *
+         sh.chunk;
+}
 
 __host__ __device__ inline int shard_owner(const ShardInfo& sh, int p) {
   int r = sh.world - 1;
@@ -145,13 +176,6 @@ cudaError_t launch_lap_batch(const BatchLapParams& p, cudaStream_t st);
 cudaError_t launch_ystage(const YStageParams& p, cudaStream_t st);
 cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st);
 cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
-// multi-GPU exchange kernels
-cudaError_t launch_sigma_pack(int m, const double* piz, const double* push, double kz,
-                              const ShardInfo& sh, const int* fpair_ij, const int* stop,
-                              cudaStream_t st);
-cudaError_t launch_x3_update(int m, double* d, double* incz, const double* piz, double kz,
-                             int fast, const ShardInfo& sh, const int* fpair_ij, const int* stop,
-                             cudaStream_t st);
 // theta of every rank's tile runs <-> one contiguous buffer (rank segments)
 cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
                               cudaStream_t st);

@@ -95,7 +95,7 @@ def nccl_unique_id() -> bytes:
     _check(lib.qapb_nccl_unique_id(buf))
     return bytes(buf)
 
-KERNEL_NAMES = ["xyfold", "zfold", "zlap", "phase2", "ystage", "xstage"]
+KERNEL_NAMES = ["xyfold", "zfold", "zlap", "phase2", "ystage", "xstage", "xchg"]
 
 
 class QapbError(RuntimeError):
