@@ -21,8 +21,8 @@ std::vector<int> shard_plan(int n, int world) {
   return b;
 }
 
-// doubles rank `rank` sends to (send[p]) / receives from (recv[p]) each peer in
-// the sigma exchange; the gain exchange moves the same amounts back.
+// pi values rank `rank` stores into (send[p]) / receives from (recv[p]) each
+// peer per iteration; the cost stores move the same amounts back.
 void shard_counts(int n, const std::vector<int>& pb, int rank, std::vector<long long>& send,
                   std::vector<long long>& recv) {
   const int world = (int)pb.size() - 1;
@@ -34,8 +34,8 @@ void shard_counts(int n, const std::vector<int>& pb, int rank, std::vector<long 
   recv.assign(world, 0);
   for (int p = 0; p < world; ++p) {
     if (p == rank) continue;
-    send[p] = rl(rank) * rows * nl(p);  // sigma of my X3 cells for p's pa
-    recv[p] = rl(p) * rows * nl(rank);  // sigma of p's X3 cells for my pa
+    send[p] = rl(rank) * rows * nl(p);  // pi of my X3 cells folded by p
+    recv[p] = rl(p) * rows * nl(rank);  // pi of p's X3 cells folded here
   }
 }
 
@@ -304,7 +304,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   shard_.chunk = chunk_;
   shard_.fence = env_int("QAPB_FENCE", 0);
   // Receive buffers live here; peers write them directly over NVLink through
-  // CUDA IPC mappings (sigma from X3 owners, gains from fold owners).
+  // CUDA IPC mappings (pi from X3 owners, costs from fold owners).
   std::vector<long long> send, recv;
   shard_counts(m, pb, rank_, send, recv);
   xcount_.assign(2 * world_, 0);
@@ -312,12 +312,12 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   for (int p = 0; p < world_; ++p) {
     if (p == rank_) continue;
     double *sr = nullptr, *gr = nullptr;
-    dalloc(&sr, recv[p]);                                         // sigma from p
-    dalloc(&gr, shard_gain_count(shard_, m, p, rank_));           // gains from p
+    dalloc(&sr, recv[p]);                                         // pi from p
+    dalloc(&gr, shard_cost_count(shard_, m, p, rank_));           // costs from p
     xbufs_.push_back(sr);
     xbufs_.push_back(gr);
-    shard_.sig_recv[p] = sr;
-    shard_.gain_recv[p] = gr;
+    shard_.pi_recv[p] = sr;
+    shard_.cost_recv[p] = gr;
     cuda_check(cudaIpcGetMemHandle(&mine[2 * p], sr), "cudaIpcGetMemHandle");
     cuda_check(cudaIpcGetMemHandle(&mine[2 * p + 1], gr), "cudaIpcGetMemHandle");
     xcount_[p] = send[p];
@@ -344,8 +344,8 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
     cuda_check(cudaIpcOpenMemHandle(&gp, all[(size_t)p * 2 * world_ + 2 * rank_ + 1],
                                     cudaIpcMemLazyEnablePeerAccess),
                "cudaIpcOpenMemHandle");
-    shard_.sig_send[p] = static_cast<double*>(sp);   // p's sigma buffer for my X3 cells
-    shard_.gain_send[p] = static_cast<double*>(gp);  // p's gain buffer for my families
+    shard_.pi_send[p] = static_cast<double*>(sp);   // p's pi buffer for my X3 cells
+    shard_.cost_send[p] = static_cast<double*>(gp);  // p's cost buffer for my families
     peer_maps_.push_back(sp);
     peer_maps_.push_back(gp);
   }
@@ -355,21 +355,21 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   cuda_check(cudaMemcpy(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice), "H2D shard");
 }
 
-// Steady sharded Z stage (location ownership, transfers fused into kernels
-// over NVLink peer memory):
-//   fold of every triple for my pa chunks; remote X3 gains are stored into
-//   their owners' buffers; barrier;
-//   Z-LAPs of my tile runs: remote-folded X3 cells patched from the received
-//   gains before solving, kz * slack of those cells stored into the fold
-//   owners' sigma buffers after solving;
-//   theta segments re-assembled on every rank (this collective is also the
-//   barrier that orders those sigma stores before the next fold).
 // Cross-rank barrier on the engine stream: after it, every rank's earlier
-// kernels (and their fenced peer stores) are complete.
+// kernels, and with them their peer stores, are complete.
 void Engine::barrier() {
   nccl_check(nccl().AllReduce(barrier_, barrier_, 1, ncclInt, ncclMax, comm_, st_), "barrier");
 }
 
+// Steady sharded Z stage (location ownership, transfers fused into kernels
+// over NVLink peer memory, ShardInfo in kernels.h):
+//   fold of every triple for my pa chunks; the new cost of each remote X3
+//   cell is stored into its owner's buffer; barrier;
+//   Z-LAPs of my tile runs: remote-folded X3 cells take their cost from that
+//   buffer before solving; their slack is stored into the fold owners' pi
+//   buffers after solving;
+//   theta segments re-assembled on every rank (this collective is also the
+//   barrier that orders those pi stores before the next fold).
 void Engine::enqueue_sharded_z(int it) {
   const bool fast = is_fast();
   double* costs = (fast && it > 0) ? incz_ : d_;
@@ -383,7 +383,7 @@ void Engine::enqueue_sharded_z(int it) {
     cuda_check(launch_zfold(f, st_), "z-fold");
     kend(st_);
     kbegin(QAPB_K_XCHG, st_);
-    barrier();  // gains have landed in every X3 owner's buffer
+    barrier();  // costs have landed in every X3 owner's buffer
     kend(st_);
     ++launches_;
   }
@@ -404,10 +404,6 @@ void Engine::enqueue_sharded_z(int it) {
     p.run_off = p_lo_ * (m_ - 1);
     p.sh = shard_dev_;
     p.fpair_ij = fpair_ij_;
-    p.d = d_;
-    p.incz = incz_;
-    p.kz = cfg_.kappa_z_upper;
-    p.fast = fast ? 1 : 0;
     p.patch = it > 0 ? 1 : 0;
     kbegin(QAPB_K_ZLAP, st_);
     cuda_check(launch_lap_batch(p, st_), "z-stage");

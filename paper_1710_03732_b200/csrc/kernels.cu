@@ -206,19 +206,14 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
     const int pc = pci + (pci >= pb);
     const int pa = f.pa0 + pa_l;
     if (pa != pb && pa != pc) {
-      // X3 lives with owner(pb): local -> offset in the z arrays, remote -> index
-      // in the exchange buffers shared with that rank
+      // X3 lives with owner(pb); when that is another rank (xr >= 0) this
+      // rank still owns the cell's D' (its copy at g) and receives pi
+      const int lo = min(pb, pc), hi = max(pb, pc);
+      const int col = pa - (pa > lo) - (pa > hi);
+      const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
+                       (size_t)f.a * nm2 + col;
       const int xb = f.sh ? shard_owner(*f.sh, pb) : 0;
-      if (!f.sh || xb == f.sh->rank) {
-        const int lo = min(pb, pc), hi = max(pb, pc);
-        const int col = pa - (pa > lo) - (pa > hi);
-        const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
-                         (size_t)f.a * nm2 + col;
-        fn(2, pa_l, pb, pc, g, base3 + e, -1);
-      } else {
-        fn(2, pa_l, pb, pc, x3_xindex(*f.sh, f.n, f.fbc, f.b, pb, pc, f.a, pa, xb, f.sh->rank),
-           base3 + e, xb);
-      }
+      fn(2, pa_l, pb, pc, g, base3 + e, (!f.sh || xb == f.sh->rank) ? -1 : xb);
     }
     pa_l += dpl;
     int inc = dpr;
@@ -260,11 +255,11 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
   double* V = sm + L.val_off();
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
     double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
-    if (xr >= 0) {  // remote X3: its owner's Z-LAP stored kz*pi
-      cp_async8(sp, f.sh->sig_recv[xr] + g);
-      return;
-    }
-    cp_async8(sp, piz + g);
+    if (xr >= 0)  // remote X3: its owner's Z-LAP stored pi into my buffer
+      cp_async8(sp, f.sh->pi_recv[xr] + x3_xindex(*f.sh, f.n, f.fbc, f.b, pb, pc, f.a,
+                                                   f.pa0 + pa_l, xr, f.sh->rank));
+    else
+      cp_async8(sp, piz + g);
     cp_async8(V + slot, vals + g);
   });
 }
@@ -305,10 +300,7 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
     const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
-    // a remote X3 slot holds its owner's sigma; the owner of pb is local iff
-    // the X3 slot is local (this family's X1/X2 use s3 either way)
-    const bool x3_remote = f.sh && shard_owner(*f.sh, pb) != f.sh->rank;
-    const double s3 = dadd(x3_remote ? p3 : dmul(kz, p3), U3[pb * n + pc]);
+    const double s3 = dadd(dmul(kz, p3), U3[pb * n + pc]);
     double own, gain;  // partners in ascending member order (B, C of rlt2.cpp:280-288)
     if (mem == 0) {
       own = p1;
@@ -320,17 +312,21 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
       own = p3;
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
     }
-    if (xr >= 0) {  // remote X3: store the gain straight into its owner's buffer (NVLink)
+    const double dn = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
+    d[g] = dn;
+    const double inc = fast ? dadd(dmul(omk, own), gain) : dn;  // rlt2.cpp:293
+    if (xr >= 0) {
+      // remote X3: its owner's next Z-LAP needs this cell's cost; store it
+      // straight into the owner's buffer over NVLink (contiguous per CTA)
       const ShardInfo& sh = *f.sh;
       const int nB = sh.pbound[xr + 1] - sh.pbound[xr];
       const int pci = pc - (pc > pb);
       const size_t gi = (size_t)blockIdx.x * nB * (n - 1) * C +
                         ((size_t)(pb - sh.pbound[xr]) * (n - 1) + pci) * C + pa_l;
-      sh.gain_send[xr][gi] = gain;
-      return;
+      sh.cost_send[xr][gi] = inc;
+    } else if (fast) {
+      incz[g] = inc;
     }
-    d[g] = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
-    if (fast) incz[g] = dadd(dmul(omk, own), gain);   // rlt2.cpp:293
   });
   if (P.shard && P.shard->fence) __threadfence_system();  // peer stores before the cross-rank barrier
   if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
@@ -374,12 +370,12 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
 // Persistent CTAs; each warp pulls tiles from a global counter and
 // double-buffers them in shared memory with TMA bulk copies
 // (cp.async.bulk + mbarrier), prefetching tile k+1 while solving tile k.
-// Per-tile view of a sharded Z tile (b,c,pb,pc) for the fused X3 exchange:
+// Per-lane view of a sharded Z tile (b,c,pb,pc) for the fused X3 exchange:
 // rows a < b are X3 members of families (a,b,c) whose fold owner is
-// owner(pa) of the column's location pa.
+// owner(pa) of the column's location pa (ShardInfo, kernels.h).
 struct X3Lane {
-  const double* gsrc = nullptr;  // gain of row a: gsrc[T(a,b,c) * gstride] (null: local column)
-  double* sdst = nullptr;        // sigma of row a: sdst[a * nA] (fold owner's buffer, peer)
+  const double* gsrc = nullptr;  // cost of row a: gsrc[T(a,b,c) * gstride] (null: local column)
+  double* sdst = nullptr;        // pi of row a: sdst[a * nA] (fold owner's buffer, peer)
   size_t gstride = 0;
   int nA = 0;
 };
@@ -410,9 +406,9 @@ __device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_i
     const int a_lo = sh.pbound[A], po = pa - a_lo, ch = po / sh.chunk;
     X[s].nA = sh.pbound[A + 1] - a_lo;
     X[s].gstride = (size_t)shard_chunks(sh, A) * nB * nm1 * sh.chunk;
-    X[s].gsrc = sh.gain_recv[A] + (size_t)ch * nB * nm1 * sh.chunk +
+    X[s].gsrc = sh.cost_recv[A] + (size_t)ch * nB * nm1 * sh.chunk +
                 ((size_t)(pb - p_lo) * nm1 + pci) * sh.chunk + (po - ch * sh.chunk);
-    X[s].sdst = sh.sig_send[A] + rows_base * X[s].nA + po;
+    X[s].sdst = sh.pi_send[A] + rows_base * X[s].nA + po;
   }
 }
 
@@ -476,49 +472,13 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
       const ShardInfo& sh = *P.sh;
       const int n = m + 2;
       x3_lanes<CPL>(sh, P.fpair_ij, n, tg, lane, X, xb, tb);
-      if (P.patch) {  // fold owners' gains -> D' / incremental costs (rlt2.cpp:292-293)
-        // rows in groups of 4 with all loads issued before any store: the
-        // patch is latency-bound, this keeps 12 loads per lane in flight
-        const double kz = P.kz, omk = dsub(1.0, P.kz);
-        double* __restrict__ dg = P.d + (size_t)tg * esz;
-        double* __restrict__ ig = P.incz + (size_t)tg * esz;
-        const double* __restrict__ pg = P.pi + (size_t)tg * esz;
-        for (int a0 = 0; a0 < xb; a0 += 4) {
-          double gn[4][CPL], ow[4][CPL], dv[4][CPL];
+      if (P.patch) {  // remote-folded cells: the fold owner sent their new cost
+#pragma unroll 4
+        for (int a = 0; a < xb; ++a) {
+          const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int a = a0 + u;
-            // T(a,b,c) = tb - C(n-a-1, 3)
-            const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
-#pragma unroll
-            for (int s = 0; s < CPL; ++s) {
-              const int j = s * 32 + lane;
-              if (a < xb && X[s].gsrc) {
-                gn[u][s] = __ldg(X[s].gsrc + (size_t)T * X[s].gstride);
-                ow[u][s] = pg[a * m + j];
-                dv[u][s] = dg[a * m + j];
-              }
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int a = a0 + u;
-#pragma unroll
-            for (int s = 0; s < CPL; ++s) {
-              const int j = s * 32 + lane;
-              if (a < xb && X[s].gsrc) {
-                const double dn = dadd(dv[u][s], dsub(gn[u][s], dmul(kz, ow[u][s])));
-                dg[a * m + j] = dn;
-                if (P.fast) {
-                  const double inc = dadd(dmul(omk, ow[u][s]), gn[u][s]);
-                  ig[a * m + j] = inc;
-                  cb[a * m + j] = inc;
-                } else {
-                  cb[a * m + j] = dn;
-                }
-              }
-            }
-          }
+          for (int s = 0; s < CPL; ++s)
+            if (X[s].gsrc) cb[a * m + s * 32 + lane] = __ldg(X[s].gsrc + (size_t)T * X[s].gstride);
         }
         __syncwarp();
       }
@@ -538,15 +498,14 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
                               P.v ? P.v + (size_t)tg * m : nullptr);
     if constexpr (SH) {
       warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
-      // sigma (without push) of my remote-folded X3 cells -> fold owners (rlt2.cpp:289)
+      // pi of my remote-folded X3 cells -> their fold owners (peer stores)
       for (int a = 0; a < xb; ++a) {
         const double ua = urow[a];
 #pragma unroll
         for (int s = 0; s < CPL; ++s) {
           if (!X[s].gsrc) continue;
           const int j = s * 32 + lane;
-          const double sl = dsub(dsub(cb[a * m + j], ua), L.v[s]);
-          X[s].sdst[(size_t)a * X[s].nA] = dmul(P.kz, sl);
+          X[s].sdst[(size_t)a * X[s].nA] = dsub(dsub(cb[a * m + j], ua), L.v[s]);
         }
       }
     } else if (P.pi) {

@@ -43,14 +43,12 @@ struct BatchLapParams {
   // (t / run_len) * run_stride + run_off + t % run_len
   int run_len, run_stride, run_off;
   // multi-GPU Z stage (location sharding), null on one GPU: the LAP kernel
-  // applies the fold owners' gains to its remote-folded X3 cells before
-  // solving (patch) and stores kz * slack of those cells straight into the
-  // fold owners' sigma buffers after solving (NVLink peer stores)
+  // takes the cost of its remote-folded X3 cells from the fold owners'
+  // stores (patch) and stores those cells' slack straight into the fold
+  // owners' pi buffers after solving (NVLink peer stores)
   const ShardInfo* sh;
   const int* fpair_ij;
-  double *d, *incz;
-  double kz;
-  int fast, patch;
+  int patch;
 };
 
 constexpr int kMaxRanks = 8;
@@ -58,36 +56,38 @@ constexpr int kMaxRanks = 8;
 // Shard description (multi-GPU).  Rank r owns the half-Z
 // tiles whose FIRST location lies in [pbound[r], pbound[r+1]): one run of
 // rl(r) = (pbound[r+1]-pbound[r])*(n-1) tiles inside every facility-pair
-// block.  It folds every facility triple for its own locations pa; in a
-// family the X3 member T(b,c,pb,pc)[a,pa] belongs to owner(pb).  Exchange
-// buffers between X3 owner B and fold owner A hold one double per
-// (pair f=(b,c), B's local location pair, row a<b, pa of A):
-//   index = ((rl(B)*rows_before[f] + lp_local*b + a) * n(A)) + (pa - pbound[A])
-//
-// The buffers live on the RECEIVING rank and are written by the sender
-// through CUDA IPC peer mappings over NVLink (no separate copy step):
-//   sigma (X3 owner B -> fold owner A): the layout above, so B's pack kernel
-//     stores whole row segments; A's fold reads it.
-//   gain (A -> B): fold order, so each fold CTA stores one contiguous block;
-//     slot = (T*nch(A) + chunk) * n(B)*(n-1)*chunk_cap
-//            + ((pb - pbound[B])*(n-1) + pci)*chunk_cap + pa_l,
-//     T = lexicographic triple index; B's X3 update reads it.
+// block, and solves their Z-LAPs.  It folds every facility triple for its
+// own locations pa; in a family the X3 member T(b,c,pb,pc)[a,pa] lies in a
+// tile of owner(pb).  When owner(pb) = B != A = owner(pa), A owns that
+// cell's D' (A's copy of it; B's is stale) and B owns its pi and its LAP.
+// Per iteration two values cross per such cell, both stored by the producing
+// kernel straight into a buffer on the consuming rank through CUDA IPC
+// mappings over NVLink (no copy step):
+//   pi   (B's Z-LAP -> A's next fold), layout per (pair f=(b,c), B's local
+//        location pair, row a<b, pa of A), so B stores whole row segments:
+//        index = ((rl(B)*rows_before[f] + lp_local*b + a) * n(A)) + (pa - pbound[A])
+//   cost (A's fold -> B's Z-LAP: the cell's new incremental cost, F variants,
+//        or new D', S variants), fold order, so each fold CTA stores one
+//        contiguous block:
+//        slot = (T*nch(A) + chunk) * n(B)*(n-1)*chunk_cap
+//               + ((pb - pbound[B])*(n-1) + pci)*chunk_cap + pa_l,
+//        T = lexicographic triple index.
 struct ShardInfo {
   int world, rank;
   int pbound[kMaxRanks + 1];
   int chunk;                           // fold chunk capacity (pa values per CTA)
   int fence;                           // system fence after peer stores (QAPB_FENCE)
   const int* rows_before;              // [fpairs+1], prefix sums of b over pairs (b<c)
-  const double* sig_recv[kMaxRanks];   // local: sigma of my families' X3 members, from owner
-  double* gain_send[kMaxRanks];        // PEER: owner's gain buffer for my families
-  double* sig_send[kMaxRanks];         // PEER: fold owner's sigma buffer for my X3 cells
-  const double* gain_recv[kMaxRanks];  // local: gains for my X3 cells, from each fold owner
+  const double* pi_recv[kMaxRanks];    // local: pi of my families' remote X3 cells
+  double* cost_send[kMaxRanks];        // PEER: X3 owner's cost buffer for my families
+  double* pi_send[kMaxRanks];          // PEER: fold owner's pi buffer for my X3 cells
+  const double* cost_recv[kMaxRanks];  // local: costs of my remote-folded X3 cells
 };
 
 __host__ __device__ inline int shard_chunks(const ShardInfo& sh, int r) {
   return (sh.pbound[r + 1] - sh.pbound[r] + sh.chunk - 1) / sh.chunk;
 }
-__host__ __device__ inline long long shard_gain_count(const ShardInfo& sh, int n, int A, int B) {
+__host__ __device__ inline long long shard_cost_count(const ShardInfo& sh, int n, int A, int B) {
   const long long tri = (long long)n * (n - 1) * (n - 2) / 6;
   return tri * shard_chunks(sh, A) * (long long)(sh.pbound[B + 1] - sh.pbound[B]) * (n - 1) *
          sh.chunk;
