@@ -84,6 +84,7 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
                "H2D d");
   else
     cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
+  split_gather();
   hS_.offset = offset;
   push_scalars();
   cuda_check(cudaStreamSynchronize(st_), "engine create");
@@ -114,6 +115,7 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
   cuda_check(launch_init_store(n, df, dd, dl, b_, c_, st_), "init_store");
   ++launches_;
   cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
+  split_gather();
   hS_.offset = 0.0;
   push_scalars();
   cuda_check(cudaStreamSynchronize(st_), "engine create");
@@ -158,6 +160,14 @@ void Engine::alloc() {
   dalloc(&triples_, 3 * (size_t)ntriples_);
   dalloc(&fpair_ij_, fpairs_);
   plan_pipeline();
+  split_mode_ = env_int("QAPB_X3SPLIT", 2);
+  split_ = world_ == 1 && !is_two_phase() && !cfg_.sa_enabled && stage_ev_.size() == 1 &&
+           split_mode_ != 0;
+  if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
+    const size_t nx = (size_t)ntriples_ * nchunks_ * lpairs_ * chunk_;
+    dalloc(&x3buf_, nx);
+    dalloc(&d3_, nx);
+  }
   dalloc(&counter_, stage_ev_.size() + 2);
   dalloc(&S_, 1);
   cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hSpin_), sizeof(DevScalars)),
@@ -216,7 +226,7 @@ Engine::~Engine() {
   dfree(b_); dfree(c_); dfree(d_); dfree(piz_); dfree(incz_); dfree(piy_); dfree(pix_);
   dfree(theta_); dfree(theta1_); dfree(delta_); dfree(ybar_); dfree(dx_); dfree(push_);
   dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
-  dfree(fpair_ij_); dfree(counter_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
+  dfree(fpair_ij_); dfree(counter_); dfree(x3buf_); dfree(d3_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
   if (hSpin_) cudaFreeHost(hSpin_);
   for (void* p : peer_maps_) cudaIpcCloseMemHandle(p);
   if (comm_ && barrier_) {  // no peer may still map my receive buffers
@@ -466,6 +476,22 @@ void Engine::plan_pipeline() {
   cuda_check(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming), "event");
 }
 
+void Engine::split_gather() {
+  if (!split_) return;
+  cuda_check(launch_x3_sync(m_, chunk_, nchunks_, triples_, ntriples_, d_, d3_, 1, st_),
+             "x3 gather");
+  d_stale_ = false;
+}
+
+// the tile-layout D' of the X3 members is stale after a split fold
+void Engine::split_scatter() const {
+  if (!split_ || !d_stale_) return;
+  cuda_check(launch_x3_sync(m_, chunk_, nchunks_, triples_, ntriples_, d_, d3_, 0, st_),
+             "x3 scatter");
+  cuda_check(cudaStreamSynchronize(st_), "x3 scatter");
+  d_stale_ = false;
+}
+
 void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
                           const double* theta_ref, int slot, cudaStream_t st) {
   if (count <= 0) return;
@@ -482,6 +508,14 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
   p.theta_ref = theta_ref ? theta_ref + t0 : nullptr;
   p.err_tile = &S_->err_tile;
   p.tile_base = t0;
+  if (split_ && t0 == 0 && count == tiles_) {  // X3 split (FoldParams::x3buf)
+    p.x3buf = x3buf_;
+    p.costs_w = costs;
+    p.x3_chunk = chunk_;
+    p.x3_nchunks = nchunks_;
+    p.fpair_ij = fpair_ij_;
+    p.patch = (cur_iter_ > 0 && split_mode_ == 1) ? 1 : 0;
+  }
   kbegin(QAPB_K_ZLAP, st);
   cuda_check(launch_lap_batch(p, st), "z-stage");
   kend(st);
@@ -505,6 +539,11 @@ FoldParams Engine::fold_params(int stage) const {
   f.sa_fac = sa_fac_;
   f.sa_loc = sa_loc_;
   f.stop = &S_->stop;
+  if (split_) {
+    f.x3buf = x3buf_;
+    f.d3 = d3_;
+    f.x3mode = split_mode_;
+  }
   return f;
 }
 
@@ -548,6 +587,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   const bool inc = is_fast() && it > 0;
   const bool steady = it > 0;
   cur_iter_ = it;
+  if (split_ && steady) d_stale_ = true;  // graph replays skip enqueue_stage_z
   if (steady && graph_ && !profiling_) {
     cuda_check(cudaGraphLaunch(graph_, st_), "graph launch");
     launches_ += graph_launches_;
@@ -829,7 +869,10 @@ void Engine::get_array(int which, double* dst, size_t count) const {
     case QAPB_ARR_PI_X: src = pix_; break;
     case QAPB_ARR_STORE_B: src = b_; break;
     case QAPB_ARR_STORE_C: src = c_; break;
-    case QAPB_ARR_STORE_D: src = d_; break;
+    case QAPB_ARR_STORE_D:
+      split_scatter();
+      src = d_;
+      break;
     case QAPB_ARR_THETA: src = theta_; break;
     case QAPB_ARR_DELTA: src = delta_; break;
     case QAPB_ARR_INCZ: src = incz_; break;

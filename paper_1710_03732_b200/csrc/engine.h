@@ -119,6 +119,14 @@ class Engine {
   int* rows_before_ = nullptr;
   double* theta_buf_ = nullptr;
   void barrier();
+  // single-GPU X3 split (kernels.h FoldParams::x3buf)
+  void split_gather();
+  void split_scatter() const;
+  bool split_ = false;
+  int split_mode_ = 0;
+  mutable bool d_stale_ = false;
+  double* x3buf_ = nullptr;
+  double* d3_ = nullptr;
   std::vector<void*> peer_maps_;  // IPC-mapped peer receive buffers
   int* barrier_ = nullptr;
   void setup_shards(const unsigned char* nccl_id);

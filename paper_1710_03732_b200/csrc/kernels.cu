@@ -116,14 +116,24 @@ struct FamilyCtx {
   size_t esz;
   int lpairs;
   const ShardInfo* sh;  // multi-GPU: X3 members owned by other ranks (null on one GPU)
+  int unit, C;
+  double* x3buf;  // single-GPU X3 split (FoldParams::x3buf), else null
+  double* d3;
+  int x3mode;
 };
 
-__device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
+// fold-order slot of X3 cell (pa_l, pb, pc) of the CTA's unit (X3 split)
+__device__ __forceinline__ size_t x3_slot(const FamilyCtx& f, int pa_l, int pb, int pc) {
+  return ((size_t)f.unit * f.lpairs + pb * f.nm1 + pc - (pc > pb)) * f.C + pa_l;
+}
+
+// unit = triple * nchunks + chunk (one CTA's work item)
+__device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
   FamilyCtx f;
   f.n = P.m;
   f.nm1 = f.n - 1;
   f.nm2 = f.n - 2;
-  const int T = blockIdx.x / P.nchunks, ch = blockIdx.x - T * P.nchunks;
+  const int T = unit / P.nchunks, ch = unit - T * P.nchunks;
   f.a = P.triples[3 * T];
   f.b = P.triples[3 * T + 1];
   f.c = P.triples[3 * T + 2];
@@ -138,6 +148,11 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P) {
   f.fbc = ix.fpair(f.b, f.c);
   f.esz = (size_t)ix.esz;
   f.lpairs = ix.lpairs;
+  f.unit = unit;
+  f.C = P.chunk;
+  f.x3buf = P.x3buf;
+  f.d3 = P.d3;
+  f.x3mode = P.x3mode;
   return f;
 }
 
@@ -206,14 +221,22 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
     const int pc = pci + (pci >= pb);
     const int pa = f.pa0 + pa_l;
     if (pa != pb && pa != pc) {
-      // X3 lives with owner(pb); when that is another rank (xr >= 0) this
-      // rank still owns the cell's D' (its copy at g) and receives pi
-      const int lo = min(pb, pc), hi = max(pb, pc);
-      const int col = pa - (pa > lo) - (pa > hi);
-      const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
-                       (size_t)f.a * nm2 + col;
-      const int xb = f.sh ? shard_owner(*f.sh, pb) : 0;
-      fn(2, pa_l, pb, pc, g, base3 + e, (!f.sh || xb == f.sh->rank) ? -1 : xb);
+      if (f.x3buf) {  // X3 split: tile offset g; the fold-order slot follows from pb, pc, pa_l
+        const int lo = min(pb, pc), hi = max(pb, pc);
+        const int col = pa - (pa > lo) - (pa > hi);
+        fn(2, pa_l, pb, pc,
+           (size_t)(f.fbc * f.lpairs + pb * nm1 + pci) * f.esz + (size_t)f.a * nm2 + col,
+           base3 + e, -2);
+      } else {
+        // X3 lives with owner(pb); when that is another rank (xr >= 0) this
+        // rank still owns the cell's D' (its copy at g) and receives pi
+        const int lo = min(pb, pc), hi = max(pb, pc);
+        const int col = pa - (pa > lo) - (pa > hi);
+        const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
+                         (size_t)f.a * nm2 + col;
+        const int xb = f.sh ? shard_owner(*f.sh, pb) : 0;
+        fn(2, pa_l, pb, pc, g, base3 + e, (!f.sh || xb == f.sh->rank) ? -1 : xb);
+      }
     }
     pa_l += dpl;
     int inc = dpr;
@@ -255,6 +278,12 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
   double* V = sm + L.val_off();
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
     double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
+    if (xr == -2) {  // X3 split: pi and D' in fold order
+      const size_t ui = x3_slot(f, pa_l, pb, pc);
+      cp_async8(sp, f.x3buf + ui);
+      cp_async8(V + slot, f.d3 + ui);
+      return;
+    }
     if (xr >= 0)  // remote X3: its owner's Z-LAP stored pi into my buffer
       cp_async8(sp, f.sh->pi_recv[xr] + x3_xindex(*f.sh, f.n, f.fbc, f.b, pb, pc, f.a,
                                                    f.pa0 + pa_l, xr, f.sh->rank));
@@ -265,14 +294,12 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
 }
 
 // z-level fold, rlt2.cpp:269-298 (Type-1 rule with the half-Z phi split).
-__global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
-  if (P.stop && *P.stop) return;
-  extern __shared__ double sm[];
-  const FamilyCtx f = family_ctx(P);
+// One work unit = (triple, pa chunk).  Staging (every load of a unit as
+// cp.async into one shared-memory buffer) and the update are separate so the
+// persistent kernel can stage unit k+1 while it updates unit k.
+__device__ __forceinline__ void fold_stage(const FoldParams& P, const FamilyCtx& f, double* sm,
+                                           const FoldSmem& L) {
   const int n = f.n, C = P.chunk;
-  const FoldSmem L(n, C);
-  double* S = sm + L.pi_off();
-  double* V = sm + L.val_off();
   double* U1 = sm + L.push_off();  // [C][n]  push of tile (a,b,pa,pb)
   double* U2 = U1 + C * n;         // [C][n]  push of tile (a,c,pa,pc)
   double* U3 = U2 + C * n;         // [n][n]  push of tile (b,c,pb,pc)
@@ -282,15 +309,23 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   for (int e = tid; e < f.Pe * n; e += bd) {
     const int pa_l = e / n, q = e - pa_l * n, pa = f.pa0 + pa_l;
     if (q == pa) continue;
-    U1[e] = P.push[f.fab * f.lpairs + ix.lpair(pa, q)];
-    U2[e] = P.push[f.fac * f.lpairs + ix.lpair(pa, q)];
+    cp_async8(U1 + e, P.push + f.fab * f.lpairs + ix.lpair(pa, q));
+    cp_async8(U2 + e, P.push + f.fac * f.lpairs + ix.lpair(pa, q));
   }
   for (int e = tid; e < n * n; e += bd) {
     const int pb = e / n, pc = e - pb * n;
-    if (pb != pc) U3[e] = P.push[f.fbc * f.lpairs + ix.lpair(pb, pc)];
+    if (pb != pc) cp_async8(U3 + e, P.push + f.fbc * f.lpairs + ix.lpair(pb, pc));
   }
-  cp_async_wait_all();
-  __syncthreads();
+}
+
+__device__ __forceinline__ void fold_update(const FoldParams& P, const FamilyCtx& f,
+                                            const double* sm, const FoldSmem& L, int unit) {
+  const int n = f.n, C = P.chunk;
+  const double* S = sm + L.pi_off();
+  const double* V = sm + L.val_off();
+  const double* U1 = sm + L.push_off();
+  const double* U2 = U1 + C * n;
+  const double* U3 = U2 + C * n;
   const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
   double* __restrict__ d = P.d;
   double* __restrict__ incz = P.incz;
@@ -313,25 +348,78 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
       gain = dadd(dmul(phi, s1), dmul(phi, s2));
     }
     const double dn = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
-    d[g] = dn;
     const double inc = fast ? dadd(dmul(omk, own), gain) : dn;  // rlt2.cpp:293
+    if (xr == -2) {  // X3 split: D' stays in fold order
+      const size_t ui = x3_slot(f, pa_l, pb, pc);
+      f.d3[ui] = dn;
+      if (f.x3mode == 1) {  // the LAP patches its tile from x3buf
+        f.x3buf[ui] = inc;
+      } else {  // hybrid: the LAP's next cost goes to the tile (scattered store)
+        if (fast)
+          incz[g] = inc;
+        else
+          d[g] = dn;
+      }
+      return;
+    }
+    d[g] = dn;
     if (xr >= 0) {
       // remote X3: its owner's next Z-LAP needs this cell's cost; store it
       // straight into the owner's buffer over NVLink (contiguous per CTA)
       const ShardInfo& sh = *f.sh;
       const int nB = sh.pbound[xr + 1] - sh.pbound[xr];
       const int pci = pc - (pc > pb);
-      const size_t gi = (size_t)blockIdx.x * nB * (n - 1) * C +
+      const size_t gi = (size_t)unit * nB * (n - 1) * C +
                         ((size_t)(pb - sh.pbound[xr]) * (n - 1) + pci) * C + pa_l;
       sh.cost_send[xr][gi] = inc;
     } else if (fast) {
       incz[g] = inc;
     }
   });
-  if (P.shard && P.shard->fence) __threadfence_system();  // peer stores before the cross-rank barrier
-  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
-    P.sa_fac[tid] = 0.0;
-    P.sa_loc[tid] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ double sm[];
+  const FamilyCtx f = family_ctx(P, blockIdx.x);
+  const FoldSmem L(f.n, P.chunk);
+  fold_stage(P, f, sm, L);
+  cp_async_wait_all();
+  __syncthreads();
+  fold_update(P, f, sm, L, blockIdx.x);
+  if (P.shard && P.shard->fence) __threadfence_system();  // peer stores before the barrier
+  if (blockIdx.x == 0 && threadIdx.x < f.n) {  // rlt2.cpp:297-298
+    P.sa_fac[threadIdx.x] = 0.0;
+    P.sa_loc[threadIdx.x] = 0.0;
+  }
+}
+
+// Persistent form: one CTA per SM strides the units (siblings of a triple run
+// on neighbouring CTAs at the same time and share its X3 rows through L2) and
+// double-buffers them: unit k+1's loads are in flight while unit k updates.
+__global__ void __launch_bounds__(512, 1) zfold_persistent_kernel(FoldParams P) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ double sm[];
+  const FoldSmem L(P.m, P.chunk);
+  const size_t bufsz = (L.total(P.m, P.chunk) + 15) & ~(size_t)15;
+  const int units = P.ntriples * P.nchunks;
+  int u = blockIdx.x, cur = 0;
+  if (u < units) fold_stage(P, family_ctx(P, u), sm, L);
+  cp_async_commit();
+  for (; u < units; u += gridDim.x) {
+    const int un = u + gridDim.x;
+    if (un < units) fold_stage(P, family_ctx(P, un), sm + (cur ^ 1) * bufsz, L);
+    cp_async_commit();
+    cp_async_wait_group<1>();  // unit u has landed (only un may be in flight)
+    __syncthreads();
+    fold_update(P, family_ctx(P, u), sm + cur * bufsz, L, u);
+    __syncthreads();  // buffer cur is re-staged next round
+    cur ^= 1;
+  }
+  if (P.shard && P.shard->fence) __threadfence_system();
+  if (blockIdx.x == 0 && threadIdx.x < P.m) {  // rlt2.cpp:297-298
+    P.sa_fac[threadIdx.x] = 0.0;
+    P.sa_loc[threadIdx.x] = 0.0;
   }
 }
 
@@ -340,7 +428,7 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
 __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
-  const FamilyCtx f = family_ctx(P);
+  const FamilyCtx f = family_ctx(P, blockIdx.x);
   const int n = f.n, C = P.chunk;
   const FoldSmem L(n, C);
   double* S = sm + L.pi_off();
@@ -412,7 +500,34 @@ __device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_i
   }
 }
 
-template <int CPL, bool SH>
+// Single-GPU X3 split (kernels.h, BatchLapParams::x3buf): the lane's column
+// pa of tile (b,c,pb,pc) maps to slot ((T*nch + pa/C)*lpairs + lp)*C + pa%C.
+template <int CPL>
+__device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, int tg, int lane,
+                                               X3Lane (&X)[CPL], int& b, long long& tb) {
+  const int nm1 = n - 1, m = n - 2, lpairs = n * nm1;
+  const int f = tg / lpairs, lp = tg - f * lpairs;
+  const int ij = P.fpair_ij[f];
+  b = ij & 0xffff;
+  const int c = ij >> 16;
+  const int pb = lp / nm1, qq = lp - pb * nm1, pc = qq + (qq >= pb);
+  const int lo = min(pb, pc), hi = max(pb, pc);
+  tb = (long long)n * (n - 1) * (n - 2) / 6 - (long long)(n - b) * (n - b - 1) / 2 + (c - b - 1);
+  const int C = P.x3_chunk;
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = s * 32 + lane;
+    X[s].gsrc = nullptr;
+    if (j >= m) continue;
+    const int pa = skip2(j, lo, hi), ch = pa / C;
+    X[s].sdst = P.x3buf + ((size_t)ch * lpairs + lp) * C + (pa - ch * C);
+    X[s].gsrc = X[s].sdst;
+    X[s].gstride = (size_t)P.x3_nchunks * lpairs * C;
+  }
+}
+
+// MODE 0: plain batch; 1: sharded Z stage (ShardInfo); 2: single-GPU X3 split
+template <int CPL, int MODE>
 __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
                                                         int buf_elems, int use_bulk, int nbuf) {
   if (P.stop && *P.stop) return;
@@ -468,17 +583,28 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
     X3Lane X[CPL];
     int xb = 0;
     long long tb = 0;
-    if constexpr (SH) {
-      const ShardInfo& sh = *P.sh;
+    if constexpr (MODE != 0) {
       const int n = m + 2;
-      x3_lanes<CPL>(sh, P.fpair_ij, n, tg, lane, X, xb, tb);
-      if (P.patch) {  // remote-folded cells: the fold owner sent their new cost
+      if constexpr (MODE == 1)
+        x3_lanes<CPL>(*P.sh, P.fpair_ij, n, tg, lane, X, xb, tb);
+      else
+        x3_split_lanes<CPL>(P, n, tg, lane, X, xb, tb);
+      if (P.patch) {  // remote-folded / split cells: the fold stored their new cost
 #pragma unroll 4
         for (int a = 0; a < xb; ++a) {
           const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
 #pragma unroll
-          for (int s = 0; s < CPL; ++s)
-            if (X[s].gsrc) cb[a * m + s * 32 + lane] = __ldg(X[s].gsrc + (size_t)T * X[s].gstride);
+          for (int s = 0; s < CPL; ++s) {
+            if (!X[s].gsrc) continue;
+            const int j = s * 32 + lane;
+            if constexpr (MODE == 1) {
+              cb[a * m + j] = __ldg(X[s].gsrc + (size_t)T * X[s].gstride);
+            } else {  // keep the tile-layout cost array current as well
+              const double v = X[s].gsrc[(size_t)T * X[s].gstride];
+              cb[a * m + j] = v;
+              P.costs_w[(size_t)tg * esz + a * m + j] = v;
+            }
+          }
         }
         __syncwarp();
       }
@@ -496,16 +622,23 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
                               P.c2r ? P.c2r + (size_t)tg * m : nullptr,
                               P.u ? P.u + (size_t)tg * m : nullptr,
                               P.v ? P.v + (size_t)tg * m : nullptr);
-    if constexpr (SH) {
+    if constexpr (MODE != 0) {
       warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
-      // pi of my remote-folded X3 cells -> their fold owners (peer stores)
+      // pi of the X3 cells folded elsewhere -> their fold slots (peer stores
+      // when sharded, the split buffer on one GPU)
+      const int n = m + 2;
       for (int a = 0; a < xb; ++a) {
         const double ua = urow[a];
+        const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
 #pragma unroll
         for (int s = 0; s < CPL; ++s) {
           if (!X[s].gsrc) continue;
           const int j = s * 32 + lane;
-          X[s].sdst[(size_t)a * X[s].nA] = dsub(dsub(cb[a * m + j], ua), L.v[s]);
+          const double sl = dsub(dsub(cb[a * m + j], ua), L.v[s]);
+          if constexpr (MODE == 1)
+            X[s].sdst[(size_t)a * X[s].nA] = sl;
+          else
+            X[s].sdst[(size_t)T * X[s].gstride] = sl;
         }
       }
     } else if (P.pi) {
@@ -672,6 +805,31 @@ __global__ void xfinish_kernel(XStageParams P) {
   }
 }
 
+// Single-GPU X3 split: copy the X3 members' D' between the tile layout (d)
+// and fold order (d3): to_d3 at engine creation, back on a store download.
+__global__ void x3_sync_kernel(int n, int C, int nch, const int* __restrict__ triples,
+                               double* __restrict__ d, double* __restrict__ d3, size_t total,
+                               int to_d3) {
+  const int nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
+  const size_t esz = (size_t)nm2 * nm2;
+  const DIdx ix(n);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t u = i / ((size_t)lpairs * C);
+    const int rem = (int)(i - u * lpairs * C), pair = rem / C, pa_l = rem - pair * C;
+    const int T = (int)(u / nch), ch = (int)(u - (size_t)T * nch), pa = ch * C + pa_l;
+    const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
+    if (pa >= n || pa == pb || pa == pc) continue;
+    const int a = triples[3 * T], b = triples[3 * T + 1], c = triples[3 * T + 2];
+    const int lo = min(pb, pc), hi = max(pb, pc), col = pa - (pa > lo) - (pa > hi);
+    const size_t g = ((size_t)ix.fpair(b, c) * lpairs + pair) * esz + (size_t)a * nm2 + col;
+    if (to_d3)
+      d3[i] = d[g];
+    else
+      d[g] = d3[i];
+  }
+}
+
 // theta of every rank's tile runs <-> one buffer of rank segments
 __global__ void theta_xfer_kernel(int m, double* theta, double* buf, ShardInfo sh, int pack) {
   const int nm1 = m - 1, lpairs = m * nm1, fpairs = m * nm1 / 2;
@@ -724,7 +882,8 @@ cudaError_t launch_xyfold(const XYFoldParams& p, int tiles, cudaStream_t st) {
 }
 
 int fold_chunk(int m) {
-  // largest pa-chunk whose CTA plan fits ~96 KB (2 CTAs / SM), at least 1
+  // largest pa-chunk whose CTA plan fits ~96 KB (2 CTAs / SM, or two buffers
+  // of the persistent fold), at least 1
   int best = 1;
   for (int c = 1; c <= m; ++c) {
     const FoldSmem L(m, c);
@@ -743,6 +902,15 @@ size_t fold_smem_bytes(int m, int chunk) {
 cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   if (p.ntriples <= 0) return cudaSuccess;
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
+  const size_t smem2 = 2 * ((smem / sizeof(double) + 15) & ~(size_t)15) * sizeof(double);
+  if (env_int("QAPB_FOLD_PERSIST", 0) && smem2 <= 220 * 1024) {
+    cudaFuncSetAttribute(zfold_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem2);
+    const int threads = env_int("QAPB_FOLD_THREADS", 512);
+    const int units = p.ntriples * p.nchunks;
+    zfold_persistent_kernel<<<std::min(units, num_sms()), threads, smem2, st>>>(p);
+    return cudaGetLastError();
+  }
   cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
   zfold_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
@@ -781,7 +949,8 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const int wmax = std::max(1, std::min(8, env_int("QAPB_LAP_WARPS", 8)));
   int W = (int)std::max<size_t>(1, std::min<size_t>(wmax, (110 * 1024) / warp_smem));
   const size_t smem = warp_smem * W;
-  auto kern = p.sh ? lap_batch_kernel<CPL, true> : lap_batch_kernel<CPL, false>;
+  auto kern = p.sh ? lap_batch_kernel<CPL, 1>
+                    : (p.x3buf ? lap_batch_kernel<CPL, 2> : lap_batch_kernel<CPL, 0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(smem, 48 * 1024));
   int per_sm = 0;
@@ -848,6 +1017,13 @@ cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st) {
 
 cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
   xfinish_kernel<<<1, 64, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
+                           double* d, double* d3, int to_d3, cudaStream_t st) {
+  const size_t total = (size_t)ntriples * nchunks * n * (n - 1) * chunk;
+  x3_sync_kernel<<<4 * num_sms(), 256, 0, st>>>(n, chunk, nchunks, triples, d, d3, total, to_d3);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,14 @@ struct BatchLapParams {
   const ShardInfo* sh;
   const int* fpair_ij;
   int patch;
+  // single-GPU X3 split (1-phase variants): the X3 member of every family
+  // lives in fold order in x3buf (slot ((T*nch + chunk)*lpairs + lp)*C + pa_l,
+  // holding the fold's new cost, then the LAP's slack) so neither kernel
+  // touches it with 16-byte scattered accesses in the fold; the LAP patches
+  // rows a < b from it (and writes them to costs_w) and stores their slack
+  double* x3buf;
+  double* costs_w;
+  int x3_chunk, x3_nchunks;
 };
 
 constexpr int kMaxRanks = 8;
@@ -115,6 +123,11 @@ struct FoldParams {
   // phase 2 (rlt2.cpp:344-381): costs mutated in place from pi(z)
   double* costs;
   const ShardInfo* shard;  // null on one GPU: the CTA's pa chunk comes from the rank's range
+  // single-GPU X3 split (BatchLapParams::x3buf): X3 pi and new cost in
+  // x3buf, X3 D' in d3, both in fold order (unit * lpairs * chunk + pair * chunk + pa_l)
+  double* x3buf;
+  double* d3;
+  int x3mode;  // 1: split (LAP patches), 2: hybrid (fold stores the cost to the tile)
 };
 
 struct XYFoldParams {
@@ -177,6 +190,9 @@ cudaError_t launch_ystage(const YStageParams& p, cudaStream_t st);
 cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st);
 cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
 // theta of every rank's tile runs <-> one contiguous buffer (rank segments)
+// single-GPU X3 split: D' of the X3 members, tile layout <-> fold order
+cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
+                           double* d, double* d3, int to_d3, cudaStream_t st);
 cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
                               cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
