@@ -394,32 +394,170 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   }
 }
 
-// Persistent form: one CTA per SM strides the units (siblings of a triple run
-// on neighbouring CTAs at the same time and share its X3 rows through L2) and
-// double-buffers them: unit k+1's loads are in flight while unit k updates.
-__global__ void __launch_bounds__(512, 1) zfold_persistent_kernel(FoldParams P) {
+// Lean z fold for the single-GPU X3 split (same arithmetic as zfold_kernel,
+// rlt2.cpp:269-298).  A CTA folds a few triples (QAPB_FOLD_LEAN_TPC, default
+// 4) of one pa chunk: the chunk's per-thread cell pattern does not depend on
+// the triple, so each thread derives its cells' in-tile offsets, cube slots
+// and push slots once and keeps them in registers; per triple only three tile
+// bases change (3.4x fewer instructions than zfold_kernel).  Offsets are
+// 32-bit (the launcher requires N_z < 2^32).  Grid = chunks x R; the R CTAs
+// of a chunk stride the triples, so the siblings of a triple run together
+// (their X3 incremental-cost stores meet in L2).  Fully persistent CTAs
+// (TPC=0) lose the inter-CTA stage/update overlap: 3.25 vs 2.60 ms at n=30.
+constexpr int kFoldSlots = 7;  // cells per thread per member group (<= 7 * 256)
+
+__global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
-  const FoldSmem L(P.m, P.chunk);
-  const size_t bufsz = (L.total(P.m, P.chunk) + 15) & ~(size_t)15;
-  const int units = P.ntriples * P.nchunks;
-  int u = blockIdx.x, cur = 0;
-  if (u < units) fold_stage(P, family_ctx(P, u), sm, L);
-  cp_async_commit();
-  for (; u < units; u += gridDim.x) {
-    const int un = u + gridDim.x;
-    if (un < units) fold_stage(P, family_ctx(P, un), sm + (cur ^ 1) * bufsz, L);
-    cp_async_commit();
-    cp_async_wait_group<1>();  // unit u has landed (only un may be in flight)
-    __syncthreads();
-    fold_update(P, family_ctx(P, u), sm + cur * bufsz, L, u);
-    __syncthreads();  // buffer cur is re-staged next round
-    cur ^= 1;
+  const int n = P.m, nm1 = n - 1, nm2 = n - 2, np = n + 1, C = P.chunk;
+  const int lpairs = n * nm1;
+  const uint32_t esz = (uint32_t)(nm2 * nm2);
+  const int nch = P.nchunks, ch = blockIdx.x % nch, r0 = blockIdx.x / nch, R = gridDim.x / nch;
+  const int pa0 = ch * C, Pe = min(C, n - pa0);
+  const FoldSmem L(n, C);
+  const int cube = L.cube;
+  double* S = sm + L.pi_off();
+  double* V = sm + L.val_off();
+  double* U1 = sm + L.push_off();  // push of tiles (a,b,pa,*), lpair order from pa0
+  double* U2 = U1 + C * nm1;       // push of tiles (a,c,pa,*)
+  double* U3 = U2 + C * nm1;       // push of tiles (b,c,*,*), lpair order
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int base2 = C * nm1 * nm2, base3 = 2 * base2;
+  auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
+
+  // X1/X2 cell e = ((pa_l*nm1 + qi)*nm2 + r): tile (.,.,pa,q), column r -> other
+  uint32_t rel12[kFoldSlots], fi12[kFoldSlots], ju12[kFoldSlots], lu12[kFoldSlots];
+  const int cnt12 = Pe * nm1 * nm2;
+#pragma unroll
+  for (int k = 0; k < kFoldSlots; ++k) {
+    const int e = tid + k * bd;
+    rel12[k] = 0xffffffffu;
+    if (e < cnt12) {
+      const int pa_l = e / (nm1 * nm2), rem = e - pa_l * nm1 * nm2;
+      const int qi = rem / nm2, r = rem - qi * nm2;
+      const int pa = pa0 + pa_l, q = qi + (qi >= pa);
+      const int other = skip2(r, min(pa, q), max(pa, q));
+      rel12[k] = (uint32_t)lpair(pa, q) * esz + r;
+      fi12[k] = (uint32_t)((pa_l * n + q) * np + other) |
+                ((uint32_t)((pa_l * n + other) * np + q) << 16);
+      ju12[k] = (uint32_t)(pa_l * nm1 + qi) | ((uint32_t)(pa_l * nm1 + other - (other > pa)) << 16);
+      lu12[k] = (uint32_t)lpair(q, other) | ((uint32_t)lpair(other, q) << 16);
+    }
   }
-  if (P.shard && P.shard->fence) __threadfence_system();
-  if (blockIdx.x == 0 && threadIdx.x < P.m) {  // rlt2.cpp:297-298
-    P.sa_fac[threadIdx.x] = 0.0;
-    P.sa_loc[threadIdx.x] = 0.0;
+  // X3 cell e = (pair*Pe + pa_l): fold-order slot pair*C + pa_l; packed as
+  // A = fi | col << 12 | pair << 18, B = j1 | j2 << 8 | pa_l << 16
+  uint32_t x3a[kFoldSlots], x3b[kFoldSlots];
+  const int cnt3 = lpairs * Pe;
+#pragma unroll
+  for (int k = 0; k < kFoldSlots; ++k) {
+    const int e = tid + k * bd;
+    x3b[k] = 0xffffffffu;
+    if (e < cnt3) {
+      const int pair = e / Pe, pa_l = e - pair * Pe;
+      const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
+      const int pa = pa0 + pa_l;
+      if (pa != pb && pa != pc) {
+        const int lo = min(pb, pc), hi = max(pb, pc);
+        const int col = pa - (pa > lo) - (pa > hi);
+        x3a[k] = (uint32_t)((pa_l * n + pb) * np + pc) | ((uint32_t)col << 12) |
+                 ((uint32_t)pair << 18);
+        x3b[k] = (uint32_t)(pa_l * nm1 + pb - (pb > pa)) |
+                 ((uint32_t)(pa_l * nm1 + pc - (pc > pa)) << 8) | ((uint32_t)pa_l << 16);
+      }
+    }
+  }
+
+  const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
+  const double* __restrict__ piz = P.piz;
+  const double* __restrict__ push = P.push;
+  double* __restrict__ d = P.d;
+  double* __restrict__ incz = P.incz;
+  double* __restrict__ x3buf = P.x3buf;
+  double* __restrict__ d3 = P.d3;
+  const int fast = P.fast;
+  const DIdx ix(n);
+  for (int T = r0; T < P.ntriples; T += R) {
+    const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+    const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
+    const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
+    const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+    const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
+    const size_t ub = ((size_t)T * nch + ch) * lpairs * C;  // fold-order base of the unit
+    // ---- stage: every load of the unit in flight before one wait ----
+#pragma unroll
+    for (int k = 0; k < kFoldSlots; ++k) {
+      if (rel12[k] == 0xffffffffu) continue;
+      const int e = tid + k * bd;
+      const uint32_t o1 = tb1 + rel12[k], o2 = tb2 + rel12[k];
+      cp_async8(S + (fi12[k] & 0xffffu), piz + o1);
+      cp_async8(V + e, d + o1);
+      cp_async8(S + cube + (fi12[k] >> 16), piz + o2);
+      cp_async8(V + base2 + e, d + o2);
+    }
+#pragma unroll
+    for (int k = 0; k < kFoldSlots; ++k) {
+      if (x3b[k] == 0xffffffffu) continue;
+      const int e = tid + k * bd;
+      const size_t ui = ub + (x3a[k] >> 18) * C + (x3b[k] >> 16);
+      cp_async8(S + 2 * cube + (x3a[k] & 0xfffu), x3buf + ui);
+      cp_async8(V + base3 + e, d3 + ui);
+    }
+    for (int e = tid; e < Pe * nm1; e += bd) {
+      cp_async8(U1 + e, push + (size_t)fab * lpairs + pa0 * nm1 + e);
+      cp_async8(U2 + e, push + (size_t)fac * lpairs + pa0 * nm1 + e);
+    }
+    for (int e = tid; e < lpairs; e += bd) cp_async8(U3 + e, push + (size_t)fbc * lpairs + e);
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- update: rlt2.cpp:280-293 per member cell ----
+#pragma unroll
+    for (int k = 0; k < kFoldSlots; ++k) {
+      if (rel12[k] == 0xffffffffu) continue;
+      const int e = tid + k * bd;
+      const uint32_t jq = ju12[k] & 0xffffu, jo = ju12[k] >> 16;
+      {  // X1: (pb, pc) = (q, other)
+        const uint32_t fi = fi12[k] & 0xffffu;
+        const double p1 = S[fi], p2 = S[cube + fi], p3 = S[2 * cube + fi];
+        const double s2 = dadd(dmul(kz, p2), U2[jo]);
+        const double s3 = dadd(dmul(kz, p3), U3[lu12[k] & 0xffffu]);
+        const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
+        const uint32_t o = tb1 + rel12[k];
+        d[o] = dadd(V[e], dsub(gain, dmul(kz, p1)));
+        if (fast) incz[o] = dadd(dmul(omk, p1), gain);
+      }
+      {  // X2: (pb, pc) = (other, q)
+        const uint32_t fi = fi12[k] >> 16;
+        const double p1 = S[fi], p2 = S[cube + fi], p3 = S[2 * cube + fi];
+        const double s1 = dadd(dmul(kz, p1), U1[jo]);
+        const double s3 = dadd(dmul(kz, p3), U3[lu12[k] >> 16]);
+        const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
+        const uint32_t o = tb2 + rel12[k];
+        d[o] = dadd(V[base2 + e], dsub(gain, dmul(kz, p2)));
+        if (fast) incz[o] = dadd(dmul(omk, p2), gain);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kFoldSlots; ++k) {
+      if (x3b[k] == 0xffffffffu) continue;
+      const int e = tid + k * bd;
+      const uint32_t fi = x3a[k] & 0xfffu, pair = x3a[k] >> 18;
+      const double p1 = S[fi], p2 = S[cube + fi], p3 = S[2 * cube + fi];
+      const double s1 = dadd(dmul(kz, p1), U1[x3b[k] & 0xffu]);
+      const double s2 = dadd(dmul(kz, p2), U2[(x3b[k] >> 8) & 0xffu]);
+      const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
+      const double dn = dadd(V[base3 + e], dsub(gain, dmul(kz, p3)));
+      d3[ub + pair * C + (x3b[k] >> 16)] = dn;
+      const uint32_t o = tb3 + pair * esz + ((x3a[k] >> 12) & 63u);
+      if (fast)
+        incz[o] = dadd(dmul(omk, p3), gain);
+      else
+        d[o] = dn;
+    }
+    __syncthreads();  // the next triple's staging overwrites shared memory
+  }
+  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
+    P.sa_fac[tid] = 0.0;
+    P.sa_loc[tid] = 0.0;
   }
 }
 
@@ -902,13 +1040,21 @@ size_t fold_smem_bytes(int m, int chunk) {
 cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   if (p.ntriples <= 0) return cudaSuccess;
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
-  const size_t smem2 = 2 * ((smem / sizeof(double) + 15) & ~(size_t)15) * sizeof(double);
-  if (env_int("QAPB_FOLD_PERSIST", 0) && smem2 <= 220 * 1024) {
-    cudaFuncSetAttribute(zfold_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem2);
-    const int threads = env_int("QAPB_FOLD_THREADS", 512);
-    const int units = p.ntriples * p.nchunks;
-    zfold_persistent_kernel<<<std::min(units, num_sms()), threads, smem2, st>>>(p);
+  const int n = p.m;
+  const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
+  if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_LEAN", 1) &&
+      nz < 4294967295.0 && p.chunk * (n - 1) * (n - 2) <= kFoldSlots * 256 &&
+      p.chunk * n * (n - 1) <= kFoldSlots * 256 && p.chunk * n * (n + 1) < 4096 && n < 64 &&
+      p.chunk * (n - 1) < 256 && n * (n - 1) < 16384) {
+    cudaFuncSetAttribute(zfold_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(smem, 48 * 1024));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zfold_lean_kernel, 256, smem);
+    const int slots = std::max(1, per_sm) * num_sms();
+    const int tpc = env_int("QAPB_FOLD_LEAN_TPC", 4);  // triples per CTA (0: persistent)
+    const int R = tpc > 0 ? (p.ntriples + tpc - 1) / tpc
+                          : std::max(1, std::min(p.ntriples, slots / p.nchunks));
+    zfold_lean_kernel<<<R * p.nchunks, 256, smem, st>>>(p);
     return cudaGetLastError();
   }
   cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
