@@ -7,6 +7,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 #include <limits>
 
 namespace qapb {
@@ -66,6 +69,25 @@ int env_int(const char* name, int dflt) {
 bool env_flag(const char* name) {
   const char* v = std::getenv(name);
   return v && *v && std::strcmp(v, "0") != 0;
+}
+
+// One NCCL communicator per (unique id, rank, device) for the process
+// lifetime: engines created again with the same id (a B&B bank, repeated
+// run_ascent calls) reuse it instead of paying ncclCommInitRank each time.
+ncclComm_t cached_comm(const ncclUniqueId& id, int world, int rank, int dev) {
+  static std::mutex mu;
+  static std::map<std::string, ncclComm_t> cache;
+  std::string key(reinterpret_cast<const char*>(&id), sizeof id);
+  key += ":" + std::to_string(world) + ":" + std::to_string(rank) + ":" + std::to_string(dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  ncclComm_t c = nullptr;
+  const ncclResult_t r = nccl().CommInitRank(&c, world, id, rank);
+  if (r != ncclSuccess)
+    throw CudaError(std::string("NCCL error in ncclCommInitRank: ") + nccl().GetErrorString(r));
+  cache.emplace(key, c);
+  return c;
 }
 }  // namespace
 
@@ -236,7 +258,6 @@ Engine::~Engine() {
   for (auto* p : xbufs_) cudaFree(p);
   if (shard_dev_) cudaFree(shard_dev_);
   if (feas_bad_) cudaFree(feas_bad_);
-  if (comm_) nccl().CommDestroy(comm_);
   if (rows_before_) cudaFree(rows_before_);
   if (barrier_) cudaFree(barrier_);
   if (theta_buf_) cudaFree(theta_buf_);
@@ -310,7 +331,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   shard_.rows_before = rows_before_;
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
-  nccl_check(nccl().CommInitRank(&comm_, world_, id, rank_), "ncclCommInitRank");
+  comm_ = cached_comm(id, world_, rank_, dev_);
   shard_.chunk = chunk_;
   shard_.fence = env_int("QAPB_FENCE", 0);
   // Receive buffers live here; peers write them directly over NVLink through
