@@ -342,13 +342,19 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   std::vector<cudaIpcMemHandle_t> mine(2 * world_);
   for (int p = 0; p < world_; ++p) {
     if (p == rank_) continue;
-    double *sr = nullptr, *gr = nullptr;
-    dalloc(&sr, recv[p]);                                         // pi from p
-    dalloc(&gr, shard_cost_count(shard_, m, p, rank_));           // costs from p
+    double *sr = nullptr, *gr = nullptr, *d3 = nullptr;
+    dalloc(&sr, recv[p]);                                // pi from p
+    dalloc(&gr, shard_cost_count(shard_, m, p, rank_));  // costs from p
+    dalloc(&d3, shard_cost_count(shard_, m, rank_, p));  // D' of my families' X3 cells in p
     xbufs_.push_back(sr);
     xbufs_.push_back(gr);
+    xbufs_.push_back(d3);
     shard_.pi_recv[p] = sr;
     shard_.cost_recv[p] = gr;
+    shard_.d3[p] = d3;
+    // sharded engines start from init_coefficients (D' = 0, rlt2.cpp:87)
+    cuda_check(cudaMemset(d3, 0, shard_cost_count(shard_, m, rank_, p) * sizeof(double)),
+               "memset d3");
     cuda_check(cudaIpcGetMemHandle(&mine[2 * p], sr), "cudaIpcGetMemHandle");
     cuda_check(cudaIpcGetMemHandle(&mine[2 * p + 1], gr), "cudaIpcGetMemHandle");
     xcount_[p] = send[p];

@@ -156,6 +156,16 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
   return f;
 }
 
+// slot of X3 cell (pa_l, pb, pc) of the CTA's unit in the cost / d3 buffers
+// shared with X3 owner xr (A's fold order, ShardInfo in kernels.h)
+__device__ __forceinline__ size_t shard_slot(const FamilyCtx& f, int xr, int pa_l, int pb,
+                                             int pc) {
+  const ShardInfo& sh = *f.sh;
+  const int nB = sh.pbound[xr + 1] - sh.pbound[xr];
+  return ((size_t)f.unit * nB * f.nm1 + (size_t)(pb - sh.pbound[xr]) * f.nm1 + pc - (pc > pb)) *
+             f.C + pa_l;
+}
+
 // exchange-buffer index of X3 cell (row a, location pa) of tile (b,c,pb,pc),
 // owned by rank xb, folded by rank xa (ShardInfo comment)
 __device__ __forceinline__ size_t x3_xindex(const ShardInfo& sh, int n, int fbc, int b, int pb,
@@ -284,11 +294,13 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
       cp_async8(V + slot, f.d3 + ui);
       return;
     }
-    if (xr >= 0)  // remote X3: its owner's Z-LAP stored pi into my buffer
+    if (xr >= 0) {  // remote X3: its owner's Z-LAP stored pi; its D' lives here
       cp_async8(sp, f.sh->pi_recv[xr] + x3_xindex(*f.sh, f.n, f.fbc, f.b, pb, pc, f.a,
                                                    f.pa0 + pa_l, xr, f.sh->rank));
-    else
-      cp_async8(sp, piz + g);
+      cp_async8(V + slot, f.sh->d3[xr] + shard_slot(f, xr, pa_l, pb, pc));
+      return;
+    }
+    cp_async8(sp, piz + g);
     cp_async8(V + slot, vals + g);
   });
 }
@@ -362,19 +374,16 @@ __device__ __forceinline__ void fold_update(const FoldParams& P, const FamilyCtx
       }
       return;
     }
-    d[g] = dn;
     if (xr >= 0) {
-      // remote X3: its owner's next Z-LAP needs this cell's cost; store it
-      // straight into the owner's buffer over NVLink (contiguous per CTA)
-      const ShardInfo& sh = *f.sh;
-      const int nB = sh.pbound[xr + 1] - sh.pbound[xr];
-      const int pci = pc - (pc > pb);
-      const size_t gi = (size_t)unit * nB * (n - 1) * C +
-                        ((size_t)(pb - sh.pbound[xr]) * (n - 1) + pci) * C + pa_l;
-      sh.cost_send[xr][gi] = inc;
-    } else if (fast) {
-      incz[g] = inc;
+      // remote X3: D' stays here in fold order; its owner's next Z-LAP takes
+      // the cost from its buffer (NVLink store, contiguous per CTA)
+      const size_t gi = shard_slot(f, xr, pa_l, pb, pc);
+      f.sh->d3[xr][gi] = dn;
+      f.sh->cost_send[xr][gi] = inc;
+      return;
     }
+    d[g] = dn;
+    if (fast) incz[g] = inc;
   });
 }
 

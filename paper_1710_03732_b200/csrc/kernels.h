@@ -67,7 +67,8 @@ constexpr int kMaxRanks = 8;
 // block, and solves their Z-LAPs.  It folds every facility triple for its
 // own locations pa; in a family the X3 member T(b,c,pb,pc)[a,pa] lies in a
 // tile of owner(pb).  When owner(pb) = B != A = owner(pa), A owns that
-// cell's D' (A's copy of it; B's is stale) and B owns its pi and its LAP.
+// cell's D' (in d3[B], in the cost layout below; B's copy is stale) and B
+// owns its pi and its LAP.
 // Per iteration two values cross per such cell, both stored by the producing
 // kernel straight into a buffer on the consuming rank through CUDA IPC
 // mappings over NVLink (no copy step):
@@ -90,6 +91,7 @@ struct ShardInfo {
   double* cost_send[kMaxRanks];        // PEER: X3 owner's cost buffer for my families
   double* pi_send[kMaxRanks];          // PEER: fold owner's pi buffer for my X3 cells
   const double* cost_recv[kMaxRanks];  // local: costs of my remote-folded X3 cells
+  double* d3[kMaxRanks];               // local: D' of my families' X3 cells in rank r (fold order)
 };
 
 __host__ __device__ inline int shard_chunks(const ShardInfo& sh, int r) {
