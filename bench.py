@@ -289,15 +289,24 @@ def run_ours(args):
                              "share": kms / max(1e-9, sum(v[0] for v in ktimes.values())),
                              "alg_bytes": kb[name], "achieved_gbs": gbs}
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_launch"] * kernels[k]["launches"])
-    traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    tdb = {}
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = _json.load(fh).get(f"n{args.n}_{args.variant}", {}).get(dom)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"],
-                "peak": peak, "unit": "GB/s", "frac": kernels[dom]["achieved_gbs"] / peak,
-                "traffic": traffic, "peak_source": peak_src,
-                "alg_bytes_per_launch": kb[dom]}
+            tdb = _json.load(fh).get(f"n{args.n}_{args.variant}", {})
+
+    def kernel_roofline(name):
+        return {"bound": "hbm", "kernel": name, "achieved": kernels[name]["achieved_gbs"],
+                "peak": peak, "unit": "GB/s", "frac": kernels[name]["achieved_gbs"] / peak,
+                "traffic": tdb.get(name), "peak_source": peak_src,
+                "alg_bytes_per_launch": kb[name]}
+    roofline = kernel_roofline(dom)
+    if dom == "zlap":
+        roofline["note"] = ("the Z-LAP batch is issue-bound (warp-per-LAP Hungarian, ~75% issue "
+                            "slots busy in ncu), not HBM-bound; its HBM fraction is reported as "
+                            "the contract asks; the HBM-bound fold is in roofline_fold")
+    if "zfold" in kernels and dom != "zfold":
+        roofline["roofline_fold"] = kernel_roofline("zfold")
     ib = iteration_bytes(args.n)
     per_gpu_its = its / world if not sharded else its  # sharded: bytes split over world GPUs
     agg_peak = peak * (world if sharded else 1)
@@ -324,9 +333,12 @@ def run_ours(args):
         e2e_s = float(tt.item())
     else:
         q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=2))  # warm context
-        t0 = time.perf_counter()
-        rep = q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters))
-        e2e_s = time.perf_counter() - t0
+        runs = []
+        for _ in range(3):  # best of 3 whole calls (the first can pay allocator warm-up)
+            t0 = time.perf_counter()
+            rep = q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters))
+            runs.append(time.perf_counter() - t0)
+        e2e_s = min(runs)
     rec_bytes = ctypes.sizeof(q.abi.Record)
     e2e = {"value": rep.iterations / e2e_s, "unit": "iterations/s",
            "h2d_bytes_per_step": 3 * args.n * args.n * 8 / rep.iterations,
@@ -336,6 +348,8 @@ def run_ours(args):
                     "qapb_run_ascent") + f"(nug{args.n}-shaped, {args.variant}, iter_limit=100): "
                    "engine build on device, 100 iterations, report + records to host",
            "seconds": e2e_s, "final_bound": rep.best_bound}
+    if not sharded:
+        e2e["all_seconds"] = runs
 
     if rank != 0:
         torch.distributed.destroy_process_group()
