@@ -257,9 +257,9 @@ QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms,
  * single-GPU engine. */
 /* Location ranges per rank (p_bounds has world+1 entries). */
 QAPB_API qapb_status qapb_shard_plan(int n, int world, int* p_bounds);
-/* Doubles rank `rank` sends (send[p]) to / receives (recv[p]) from every
- * peer p in ONE of the two per-iteration exchanges (both exchanges move the
- * same amounts in opposite directions). */
+/* Doubles rank `rank` stores into (send[p]) / receives from (recv[p]) every
+ * peer p per iteration in ONE direction of the X3 exchange (pi one way, the
+ * new costs the other; kernels.h ShardInfo). */
 QAPB_API qapb_status qapb_shard_exchange_counts(int n, int world, int rank,
                                                 long long* send, long long* recv);
 QAPB_API qapb_status qapb_nccl_unique_id(unsigned char id[128]);
@@ -278,6 +278,34 @@ QAPB_API qapb_status qapb_run_ascent(int n, const double* flow,
                                      const qapb_config* cfg, qapb_report* rep,
                                      qapb_record* records, int max_records,
                                      int* certificate);
+
+/* ---- Device-resident stores: branch-and-bound node evaluation ----
+ * A qapb_store is a CoefficientStore (rlt2.hpp:72-82) held in HBM.  The B&B
+ * flow of bnb.cpp:317-387 (parent snapshot -> collapse_store per child ->
+ * AscentEngine(child) -> run) runs without host round trips:
+ *   qapb_store_from_engine   AscentEngine::snapshot(), rlt2.cpp:537-542
+ *                            (S variants only: std::logic_error otherwise)
+ *   qapb_store_collapse      collapse_store(st, fac, loc), rlt2.cpp:109-182,
+ *                            bitwise identical to the host function
+ *   qapb_engine_create_from_store
+ *                            AscentEngine(CoefficientStore, cfg), rlt2.cpp:207,
+ *                            device-to-device
+ * Stores live on one device (cfg->device for engines built from them must
+ * match). */
+typedef struct qapb_store qapb_store;
+QAPB_API qapb_status qapb_store_upload(int m, const double* b, const double* c,
+                                       const double* d, double offset, int device,
+                                       qapb_store** out);
+QAPB_API qapb_status qapb_store_from_engine(qapb_engine* e, qapb_store** out);
+QAPB_API qapb_status qapb_store_collapse(const qapb_store* s, int fac, int loc,
+                                         qapb_store** out);
+QAPB_API qapb_status qapb_store_info(const qapb_store* s, int* m, double* offset);
+QAPB_API qapb_status qapb_store_download(const qapb_store* s, double* b, double* c,
+                                         double* d, double* offset);
+QAPB_API qapb_status qapb_store_destroy(qapb_store* s);
+QAPB_API qapb_status qapb_engine_create_from_store(const qapb_store* s,
+                                                   const qapb_config* cfg,
+                                                   qapb_engine** out);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,7 @@ from .abi import F1, F2, S1, S2, VARIANTS, VARIANT_NAMES  # noqa: F401
 from .instance import (QapInstance, evaluate_objective, generate_instance,  # noqa: F401
                        load_qaplib_file, parse_qaplib, parse_solution)
 from .engine import (AscentConfig, AscentEngine, BoundReport, CoefficientStore,  # noqa: F401
+                     DeviceStore,
                      IterationRecord, LapBatch, LapResult, QapbError, collapse_store,
                      init_coefficients, lib, library_path, redistribute_family, run_ascent,
                      run_ascent_warm, solve_batch, solve_batch_device, solve_batch_serial,

@@ -14,9 +14,15 @@
 #include "engine.h"
 #include "nccl_dyn.h"
 #include "kernels.h"
+#include "store.h"
 
 using qapb::CudaError;
 using qapb::Engine;
+using qapb::DeviceStore;
+using qapb::collapse_store_device;
+using qapb::store_nb;
+using qapb::store_nc;
+using qapb::store_nd;
 
 namespace qapb {
 std::vector<int> shard_plan(int n, int world);
@@ -26,6 +32,9 @@ void shard_counts(int n, const std::vector<int>& ab, int rank, std::vector<long 
 
 struct qapb_engine {
   std::unique_ptr<Engine> e;
+};
+struct qapb_store {
+  std::unique_ptr<qapb::DeviceStore> s;
 };
 
 namespace {
@@ -52,6 +61,10 @@ qapb_status guard(F&& f) {
     g_err = e.what();
     return QAPB_ERUNTIME;
   }
+}
+
+void cuda_check_set(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) throw CudaError("cudaSetDevice failed");
 }
 
 void need(bool ok, const char* msg) {
@@ -591,3 +604,97 @@ QAPB_API qapb_status qapb_run_ascent(int n, const double* flow, const double* di
 }
 
 }  // extern "C"
+
+// ---- device-resident stores (store.cu) -------------------
+QAPB_API qapb_status qapb_store_upload(int m, const double* b, const double* c,
+                                       const double* d, double offset, int device,
+                                       qapb_store** out) {
+  return guard([&] {
+    need(m >= 2, "store: m >= 2 required");
+    need(b && c && (m < 3 || d) && out, "store_upload: null pointer");
+    auto h = std::make_unique<qapb_store>();
+    h->s = std::make_unique<DeviceStore>(m, device);
+    auto up = [](double* dst, const double* src, size_t n) {
+      if (n && cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault) != cudaSuccess)
+        throw CudaError("store_upload: copy failed");
+    };
+    up(h->s->b, b, store_nb(m));
+    up(h->s->c, c, store_nc(m));
+    if (m >= 3) up(h->s->d, d, store_nd(m));
+    h->s->offset = offset;
+    *out = h.release();
+  });
+}
+
+// AscentEngine::snapshot() (rlt2.cpp:537-542) kept in HBM
+QAPB_API qapb_status qapb_store_from_engine(qapb_engine* e, qapb_store** out) {
+  return guard([&] {
+    need(e && out, "store_from_engine: null pointer");
+    if (e->e->is_fast())  // rlt2.cpp:538-540
+      throw std::logic_error("warm-start snapshots are only offered from S variants");
+    const int m = e->e->m();
+    auto h = std::make_unique<qapb_store>();
+    h->s = std::make_unique<DeviceStore>(m, e->e->device());
+    e->e->get_array(QAPB_ARR_STORE_B, h->s->b, e->e->array_size(QAPB_ARR_STORE_B));
+    e->e->get_array(QAPB_ARR_STORE_C, h->s->c, e->e->array_size(QAPB_ARR_STORE_C));
+    e->e->get_array(QAPB_ARR_STORE_D, h->s->d, e->e->array_size(QAPB_ARR_STORE_D));
+    h->s->offset = e->e->offset();
+    *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_store_collapse(const qapb_store* s, int fac, int loc,
+                                         qapb_store** out) {
+  return guard([&] {
+    need(s && out, "store_collapse: null pointer");
+    cuda_check_set(s->s->device);
+    auto h = std::make_unique<qapb_store>();
+    h->s = collapse_store_device(*s->s, fac, loc);
+    *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_store_info(const qapb_store* s, int* m, double* offset) {
+  return guard([&] {
+    need(s, "store_info: null store");
+    if (m) *m = s->s->m;
+    if (offset) *offset = s->s->offset;
+  });
+}
+
+QAPB_API qapb_status qapb_store_download(const qapb_store* s, double* b, double* c, double* d,
+                                         double* offset) {
+  return guard([&] {
+    need(s, "store_download: null store");
+    const int m = s->s->m;
+    auto down = [](double* dst, const double* src, size_t n) {
+      if (dst && n && cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault) != cudaSuccess)
+        throw CudaError("store_download: copy failed");
+    };
+    cuda_check_set(s->s->device);
+    down(b, s->s->b, store_nb(m));
+    down(c, s->s->c, store_nc(m));
+    down(d, s->s->d, store_nd(m));
+    if (offset) *offset = s->s->offset;
+  });
+}
+
+QAPB_API qapb_status qapb_store_destroy(qapb_store* s) {
+  return guard([&] { delete s; });
+}
+
+// AscentEngine(CoefficientStore, cfg), rlt2.cpp:207-230, device-to-device
+QAPB_API qapb_status qapb_engine_create_from_store(const qapb_store* s, const qapb_config* cfg,
+                                                   qapb_engine** out) {
+  return guard([&] {
+    need(s && out, "engine_create_from_store: null pointer");
+    qapb_config c0;
+    qapb_config_init(&c0);
+    qapb_config cc = cfg ? *cfg : c0;
+    need(cc.device == s->s->device, "engine_create_from_store: cfg.device must be the store's");
+    auto h = std::make_unique<qapb_engine>();
+    h->e = std::make_unique<Engine>(s->s->m, s->s->b, s->s->c, s->s->m >= 3 ? s->s->d : nullptr,
+                                    s->s->offset, cc);
+    *out = h.release();
+  });
+}

@@ -99,11 +99,10 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
   alloc();
   setup_shards(nullptr);
   init_state();
-  cuda_check(cudaMemcpyAsync(b_, b, nb_ * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D b");
-  cuda_check(cudaMemcpyAsync(c_, c, nc_ * sizeof(double), cudaMemcpyHostToDevice, st_), "H2D c");
+  cuda_check(cudaMemcpyAsync(b_, b, nb_ * sizeof(double), cudaMemcpyDefault, st_), "H2D b");
+  cuda_check(cudaMemcpyAsync(c_, c, nc_ * sizeof(double), cudaMemcpyDefault, st_), "H2D c");
   if (d)
-    cuda_check(cudaMemcpyAsync(d_, d, nd_ * sizeof(double), cudaMemcpyHostToDevice, st_),
-               "H2D d");
+    cuda_check(cudaMemcpyAsync(d_, d, nd_ * sizeof(double), cudaMemcpyDefault, st_), "H2D d");
   else
     cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
   split_gather();
@@ -904,7 +903,8 @@ void Engine::get_array(int which, double* dst, size_t count) const {
     case QAPB_ARR_DELTA: src = delta_; break;
     case QAPB_ARR_INCZ: src = incz_; break;
   }
-  if (n) cuda_check(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H array");
+  // dst may be host or device memory (device snapshots, store.cu)
+  if (n) cuda_check(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault), "D2H array");
 }
 
 // ---- measurement hooks ---------------------------------------------------

@@ -45,6 +45,7 @@ class Engine {
   void run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<int>* cert);
 
   int m() const { return m_; }
+  int device() const { return dev_; }
   int iteration() const { return hS_.iter; }
   double best_bound() const { return hS_.best; }
   double gap() const;                                // rlt2.cpp:532-535

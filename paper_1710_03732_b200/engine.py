@@ -58,6 +58,13 @@ lib.qapb_engine_snapshot.argtypes = [_vp, _vp, _vp, _vp, _P(C.c_double)]
 lib.qapb_engine_launch_count.argtypes = [_vp, _P(C.c_longlong)]
 lib.qapb_run_ascent.argtypes = [C.c_int, _vp, _vp, _vp, _P(Config), _P(Report), _vp, C.c_int,
                                 _vp]
+lib.qapb_store_upload.argtypes = [C.c_int, _vp, _vp, _vp, C.c_double, C.c_int, _P(_vp)]
+lib.qapb_store_from_engine.argtypes = [_vp, _P(_vp)]
+lib.qapb_store_collapse.argtypes = [_vp, C.c_int, C.c_int, _P(_vp)]
+lib.qapb_store_info.argtypes = [_vp, _P(C.c_int), _P(C.c_double)]
+lib.qapb_store_download.argtypes = [_vp, _vp, _vp, _vp, _P(C.c_double)]
+lib.qapb_store_destroy.argtypes = [_vp]
+lib.qapb_engine_create_from_store.argtypes = [_vp, _P(Config), _P(_vp)]
 lib.qapb_device_count.argtypes = [_P(C.c_int)]
 lib.qapb_engine_enqueue.argtypes = [_vp, C.c_int]
 lib.qapb_engine_synchronize.argtypes = [_vp]
@@ -257,6 +264,60 @@ def collapse_store(st: CoefficientStore, fac: int, loc: int) -> CoefficientStore
     return CoefficientStore(mc, ob, oc, od, off.value)
 
 
+class DeviceStore:
+    """A CoefficientStore held in HBM (include/qapb200.h): the B&B
+    node flow of bnb.cpp:317-387 -- parent snapshot, collapse_store per child,
+    AscentEngine(child) -- without host round trips."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def upload(cls, st: CoefficientStore, device: int = 0) -> "DeviceStore":
+        h = _vp()
+        d = None if st.d is None else np.ascontiguousarray(st.d, np.float64)
+        _check(lib.qapb_store_upload(st.m, dptr(np.ascontiguousarray(st.b, np.float64)),
+                                     dptr(np.ascontiguousarray(st.c, np.float64)), dptr(d),
+                                     float(st.offset), device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_engine(cls, eng: "AscentEngine") -> "DeviceStore":
+        """AscentEngine::snapshot() (rlt2.cpp:537-542) kept on the device."""
+        h = _vp()
+        _check(lib.qapb_store_from_engine(eng._h, C.byref(h)))
+        return cls(h)
+
+    def collapse(self, fac: int, loc: int) -> "DeviceStore":
+        """collapse_store(st, fac, loc), rlt2.cpp:109-182, on the device."""
+        h = _vp()
+        _check(lib.qapb_store_collapse(self._h, fac, loc, C.byref(h)))
+        return DeviceStore(h)
+
+    @property
+    def m(self) -> int:
+        m = C.c_int()
+        _check(lib.qapb_store_info(self._h, C.byref(m), None))
+        return m.value
+
+    def download(self) -> CoefficientStore:
+        m = self.m
+        nb, nc, nd = store_sizes(m)
+        b, c, d = np.empty(nb), np.empty(nc), np.empty(max(nd, 0))
+        off = C.c_double()
+        _check(lib.qapb_store_download(self._h, dptr(b), dptr(c), dptr(d) if nd > 0 else None,
+                                       C.byref(off)))
+        return CoefficientStore(m, b, c, d, off.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.qapb_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
 def redistribute_family(pi, virtual_slots: int = 3, tol: float = 1e-9):
     """rlt2.cpp:184-205 -> (ok, add[3])."""
     pi = np.ascontiguousarray(pi, dtype=np.float64)
@@ -369,6 +430,18 @@ class AscentEngine:
         c = self.cfg.to_c()
         _check(lib.qapb_engine_create_instance(inst.n, dptr(inst.flow), dptr(inst.dist),
                                                dptr(inst.linear), C.byref(c), C.byref(h)))
+        self._h = h
+        return self
+
+    @classmethod
+    def from_device_store(cls, store: "DeviceStore", cfg: Optional[AscentConfig] = None):
+        """AscentEngine(CoefficientStore, cfg) from a store already in HBM."""
+        self = cls.__new__(cls)
+        self.cfg = cfg or AscentConfig()
+        self.m = store.m
+        h = C.c_void_p()
+        c = self.cfg.to_c()
+        _check(lib.qapb_engine_create_from_store(store._h, C.byref(c), C.byref(h)))
         self._h = h
         return self
 
