@@ -279,6 +279,16 @@ QAPB_API qapb_status qapb_run_ascent(int n, const double* flow,
                                      qapb_record* records, int max_records,
                                      int* certificate);
 
+/* BoundReport::to_json, rlt2.cpp:604-630, byte-identical to the reference's
+ * nlohmann output.  recs: 6 doubles per record (iteration, bound, gap, z_ms,
+ * y_ms, x_ms).  QAPB_EINVAL when cap <= *len (the length is still set). */
+QAPB_API qapb_status qapb_report_json(const char* instance, const char* variant,
+                                      int sa_enabled, double best_bound, double upper_bound,
+                                      double gap, const char* termination, int iterations,
+                                      double wall_ms, const int* cert, int ncert,
+                                      double cert_value, const double* recs, int nrec,
+                                      char* out, size_t cap, size_t* len);
+
 /* ---- Device-resident stores: branch-and-bound node evaluation ----
  * A qapb_store is a CoefficientStore (rlt2.hpp:72-82) held in HBM.  The B&B
  * flow of bnb.cpp:317-387 (parent snapshot -> collapse_store per child ->

@@ -353,3 +353,40 @@ QREF int qref_run_ascent(int n, const double* flow, const double* dist,
                 rep, recs, max_records, cert);
   });
 }
+
+// BoundReport::to_json of the reference (nlohmann dump(2), rlt2.cpp:604-630),
+// same argument convention as qapb_report_json (include/qapb200.h)
+QREF int qref_report_json(const char* instance, const char* variant, int sa_enabled,
+                          double best_bound, double upper_bound, double gap,
+                          const char* termination, int iterations, double wall_ms,
+                          const int* cert, int ncert, double cert_value, const double* recs,
+                          int nrec, char* out, size_t cap, size_t* len) {
+  return guard([&] {
+    qap::BoundReport r;
+    r.instance = instance ? instance : "";
+    r.variant = variant ? variant : "";
+    r.sa_enabled = sa_enabled != 0;
+    r.best_bound = best_bound;
+    r.upper_bound = upper_bound;
+    r.gap = gap;
+    r.termination = termination ? termination : "";
+    r.iterations = iterations;
+    r.wall_ms = wall_ms;
+    if (cert) r.certificate.assign(cert, cert + ncert);
+    r.certificate_value = cert_value;
+    for (int k = 0; k < nrec; ++k) {
+      qap::IterationRecord x;
+      x.iteration = (int)recs[6 * k];
+      x.bound = recs[6 * k + 1];
+      x.gap = recs[6 * k + 2];
+      x.z_ms = recs[6 * k + 3];
+      x.y_ms = recs[6 * k + 4];
+      x.x_ms = recs[6 * k + 5];
+      r.records.push_back(x);
+    }
+    const std::string j = r.to_json();
+    if (len) *len = j.size();
+    if (!out || cap <= j.size()) throw std::invalid_argument("buffer too small");
+    std::memcpy(out, j.c_str(), j.size() + 1);
+  });
+}

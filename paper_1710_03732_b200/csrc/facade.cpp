@@ -5,6 +5,8 @@
 // headers and link libqapb200.so.  Status codes become the reference's
 // exception types again.
 #include <algorithm>
+#include <cstdint>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -548,36 +550,315 @@ QAP_API BoundReport run_ascent_warm(CoefficientStore warm, const AscentConfig& c
   return eng.run();
 }
 
+// ---- BoundReport::to_json, byte-identical to the reference's (rlt2.cpp:604-630,
+// nlohmann::json::dump(2)): object keys in sorted order (std::map), 2-space
+// indent, integers as integers, doubles as nlohmann's Grisu2 digits in its
+// layout (digits[.0] up to 10^15, 0.000ddd down to 1e-4, d.ddde+XX
+// otherwise), non-finite as null, strings escaped as nlohmann does.
+namespace {
+
+// Shortest-digit conversion of nlohmann/json (the reference's vendored
+// serializer, absent from /root/reference): Grisu2 (F. Loitsch, "Printing
+// Floating-Point Numbers Quickly and Accurately with Integers", PLDI 2010)
+// with alpha = -60, gamma = -32, cached powers 10^(-300 + 8i) and the
+// "round toward w" step, then nlohmann's layout rules.  Grisu2 is not always
+// the shortest or the closest representation, so std::to_chars would differ
+// from the reference in ~0.5% of values.
+struct DiyFp {
+  std::uint64_t f;
+  int e;
+};
+
+DiyFp diy_mul(DiyFp x, DiyFp y) {  // upper 64 bits of the 128-bit product, rounded
+  const std::uint64_t u_lo = x.f & 0xFFFFFFFFu, u_hi = x.f >> 32;
+  const std::uint64_t v_lo = y.f & 0xFFFFFFFFu, v_hi = y.f >> 32;
+  const std::uint64_t p0 = u_lo * v_lo, p1 = u_lo * v_hi, p2 = u_hi * v_lo, p3 = u_hi * v_hi;
+  std::uint64_t q = (p0 >> 32) + (p1 & 0xFFFFFFFFu) + (p2 & 0xFFFFFFFFu);
+  q += std::uint64_t{1} << 31;
+  return {p3 + (p2 >> 32) + (p1 >> 32) + (q >> 32), x.e + y.e + 64};
+}
+
+DiyFp diy_normalize(DiyFp x) {
+  while ((x.f >> 63) == 0) {
+    x.f <<= 1;
+    --x.e;
+  }
+  return x;
+}
+
+struct CachedPow {
+  std::uint64_t f;
+  int e, k;
+};
+
+const CachedPow kCachedPows[79] = {
+    {0xAB70FE17C79AC6CAull, -1060, -300},
+    {0xFF77B1FCBEBCDC4Full, -1034, -292},
+    {0xBE5691EF416BD60Cull, -1007, -284},
+    {0x8DD01FAD907FFC3Cull, -980, -276},
+    {0xD3515C2831559A83ull, -954, -268},
+    {0x9D71AC8FADA6C9B5ull, -927, -260},
+    {0xEA9C227723EE8BCBull, -901, -252},
+    {0xAECC49914078536Dull, -874, -244},
+    {0x823C12795DB6CE57ull, -847, -236},
+    {0xC21094364DFB5637ull, -821, -228},
+    {0x9096EA6F3848984Full, -794, -220},
+    {0xD77485CB25823AC7ull, -768, -212},
+    {0xA086CFCD97BF97F4ull, -741, -204},
+    {0xEF340A98172AACE5ull, -715, -196},
+    {0xB23867FB2A35B28Eull, -688, -188},
+    {0x84C8D4DFD2C63F3Bull, -661, -180},
+    {0xC5DD44271AD3CDBAull, -635, -172},
+    {0x936B9FCEBB25C996ull, -608, -164},
+    {0xDBAC6C247D62A584ull, -582, -156},
+    {0xA3AB66580D5FDAF6ull, -555, -148},
+    {0xF3E2F893DEC3F126ull, -529, -140},
+    {0xB5B5ADA8AAFF80B8ull, -502, -132},
+    {0x87625F056C7C4A8Bull, -475, -124},
+    {0xC9BCFF6034C13053ull, -449, -116},
+    {0x964E858C91BA2655ull, -422, -108},
+    {0xDFF9772470297EBDull, -396, -100},
+    {0xA6DFBD9FB8E5B88Full, -369, -92},
+    {0xF8A95FCF88747D94ull, -343, -84},
+    {0xB94470938FA89BCFull, -316, -76},
+    {0x8A08F0F8BF0F156Bull, -289, -68},
+    {0xCDB02555653131B6ull, -263, -60},
+    {0x993FE2C6D07B7FACull, -236, -52},
+    {0xE45C10C42A2B3B06ull, -210, -44},
+    {0xAA242499697392D3ull, -183, -36},
+    {0xFD87B5F28300CA0Eull, -157, -28},
+    {0xBCE5086492111AEBull, -130, -20},
+    {0x8CBCCC096F5088CCull, -103, -12},
+    {0xD1B71758E219652Cull, -77, -4},
+    {0x9C40000000000000ull, -50, 4},
+    {0xE8D4A51000000000ull, -24, 12},
+    {0xAD78EBC5AC620000ull, 3, 20},
+    {0x813F3978F8940984ull, 30, 28},
+    {0xC097CE7BC90715B3ull, 56, 36},
+    {0x8F7E32CE7BEA5C70ull, 83, 44},
+    {0xD5D238A4ABE98068ull, 109, 52},
+    {0x9F4F2726179A2245ull, 136, 60},
+    {0xED63A231D4C4FB27ull, 162, 68},
+    {0xB0DE65388CC8ADA8ull, 189, 76},
+    {0x83C7088E1AAB65DBull, 216, 84},
+    {0xC45D1DF942711D9Aull, 242, 92},
+    {0x924D692CA61BE758ull, 269, 100},
+    {0xDA01EE641A708DEAull, 295, 108},
+    {0xA26DA3999AEF774Aull, 322, 116},
+    {0xF209787BB47D6B85ull, 348, 124},
+    {0xB454E4A179DD1877ull, 375, 132},
+    {0x865B86925B9BC5C2ull, 402, 140},
+    {0xC83553C5C8965D3Dull, 428, 148},
+    {0x952AB45CFA97A0B3ull, 455, 156},
+    {0xDE469FBD99A05FE3ull, 481, 164},
+    {0xA59BC234DB398C25ull, 508, 172},
+    {0xF6C69A72A3989F5Cull, 534, 180},
+    {0xB7DCBF5354E9BECEull, 561, 188},
+    {0x88FCF317F22241E2ull, 588, 196},
+    {0xCC20CE9BD35C78A5ull, 614, 204},
+    {0x98165AF37B2153DFull, 641, 212},
+    {0xE2A0B5DC971F303Aull, 667, 220},
+    {0xA8D9D1535CE3B396ull, 694, 228},
+    {0xFB9B7CD9A4A7443Cull, 720, 236},
+    {0xBB764C4CA7A44410ull, 747, 244},
+    {0x8BAB8EEFB6409C1Aull, 774, 252},
+    {0xD01FEF10A657842Cull, 800, 260},
+    {0x9B10A4E5E9913129ull, 827, 268},
+    {0xE7109BFBA19C0C9Dull, 853, 276},
+    {0xAC2820D9623BF429ull, 880, 284},
+    {0x80444B5E7AA7CF85ull, 907, 292},
+    {0xBF21E44003ACDD2Dull, 933, 300},
+    {0x8E679C2F5E44FF8Full, 960, 308},
+    {0xD433179D9C8CB841ull, 986, 316},
+    {0x9E19DB92B4E31BA9ull, 1013, 324},
+};
+
+int find_largest_pow10(std::uint32_t n, std::uint32_t& pow10) {
+  static const std::uint32_t p[10] = {1,      10,      100,      1000,      10000,
+                                      100000, 1000000, 10000000, 100000000, 1000000000};
+  int k = 10;
+  while (k > 1 && n < p[k - 1]) --k;
+  pow10 = p[k - 1];
+  return k;
+}
+
+void grisu2_round(char* buf, int len, std::uint64_t dist, std::uint64_t delta, std::uint64_t rest,
+                  std::uint64_t ten_k) {
+  // move the last digit down while that brings the value closer to w
+  while (rest < dist && delta - rest >= ten_k &&
+         (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+    buf[len - 1]--;
+    rest += ten_k;
+  }
+}
+
+// digits of some V in [M-, M+] (all three share the exponent e, -60 <= e <= -32)
+void grisu2_digits(char* buf, int& len, int& dexp, DiyFp Mm, DiyFp w, DiyFp Mp) {
+  std::uint64_t delta = Mp.f - Mm.f;
+  std::uint64_t dist = Mp.f - w.f;
+  const int sh = -Mp.e;
+  const std::uint64_t one = std::uint64_t{1} << sh;
+  auto p1 = static_cast<std::uint32_t>(Mp.f >> sh);
+  std::uint64_t p2 = Mp.f & (one - 1);
+  std::uint32_t pow10 = 0;
+  int n = find_largest_pow10(p1, pow10);
+  while (n > 0) {
+    const std::uint32_t d = p1 / pow10, r = p1 % pow10;
+    buf[len++] = static_cast<char>('0' + d);
+    p1 = r;
+    --n;
+    const std::uint64_t rest = (std::uint64_t{p1} << sh) + p2;
+    if (rest <= delta) {
+      dexp += n;
+      grisu2_round(buf, len, dist, delta, rest, std::uint64_t{pow10} << sh);
+      return;
+    }
+    pow10 /= 10;
+  }
+  int m = 0;
+  for (;;) {
+    p2 *= 10;
+    const std::uint64_t d = p2 >> sh, r = p2 & (one - 1);
+    buf[len++] = static_cast<char>('0' + d);
+    p2 = r;
+    ++m;
+    delta *= 10;
+    dist *= 10;
+    if (p2 <= delta) break;
+  }
+  dexp -= m;
+  grisu2_round(buf, len, dist, delta, p2, one);
+}
+
+// v > 0 finite -> digits in buf, value = digits * 10^dexp
+void grisu2(char* buf, int& len, int& dexp, double v) {
+  std::uint64_t bits;
+  std::memcpy(&bits, &v, sizeof bits);
+  const std::uint64_t E = bits >> 52, F = bits & ((std::uint64_t{1} << 52) - 1);
+  const DiyFp x = E == 0 ? DiyFp{F, 1 - 1075} : DiyFp{F + (std::uint64_t{1} << 52), (int)E - 1075};
+  const bool lower_closer = F == 0 && E > 1;
+  const DiyFp mp = diy_normalize(DiyFp{2 * x.f + 1, x.e - 1});
+  DiyFp mm = lower_closer ? DiyFp{4 * x.f - 1, x.e - 2} : DiyFp{2 * x.f - 1, x.e - 1};
+  mm = DiyFp{mm.f << (mm.e - mp.e), mp.e};
+  const DiyFp w = diy_normalize(x);
+  // cached power c = 10^-k with -60 <= e_c + mp.e + 64 <= -32
+  const int f = -60 - mp.e - 1;
+  const int k = (f * 78913) / (1 << 18) + (f > 0 ? 1 : 0);
+  const CachedPow& c = kCachedPows[(300 + k + 7) / 8];
+  const DiyFp ck{c.f, c.e};
+  const DiyFp W = diy_mul(w, ck), Wm = diy_mul(mm, ck), Wp = diy_mul(mp, ck);
+  dexp = -c.k;
+  len = 0;
+  grisu2_digits(buf, len, dexp, DiyFp{Wm.f + 1, Wm.e}, W, DiyFp{Wp.f - 1, Wp.e});
+}
+
+std::string json_double(double v) {
+  if (!std::isfinite(v)) return "null";
+  std::string out;
+  if (std::signbit(v)) {
+    out += '-';
+    v = -v;
+  }
+  if (v == 0) return out + "0.0";
+  char dig[32];
+  int k = 0, dexp = 0;
+  grisu2(dig, k, dexp, v);
+  const std::string digits(dig, dig + k);
+  const int n = k + dexp;  // value = 0.d1d2... x 10^n
+  if (k <= n && n <= 15) {
+    out += digits + std::string(n - k, '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    out += digits.substr(0, n) + "." + digits.substr(n);
+  } else if (-4 < n && n <= 0) {
+    out += "0." + std::string(-n, '0') + digits;
+  } else {
+    out += digits.substr(0, 1);
+    if (k > 1) out += "." + digits.substr(1);
+    const int x = n - 1;
+    char eb[16];
+    std::snprintf(eb, sizeof eb, "e%c%02d", x < 0 ? '-' : '+', x < 0 ? -x : x);
+    out += eb;
+  }
+  return out;
+}
+
+std::string json_string(const std::string& s) {
+  std::string o = "\"";
+  for (unsigned char ch : s) {
+    switch (ch) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\b': o += "\\b"; break;
+      case '\f': o += "\\f"; break;
+      case '\n': o += "\\n"; break;
+      case '\r': o += "\\r"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (ch < 0x20) {
+          char u[8];
+          std::snprintf(u, sizeof u, "\\u%04x", ch);
+          o += u;
+        } else {
+          o += (char)ch;
+        }
+    }
+  }
+  return o + "\"";
+}
+
+// one "key": value member per line at the given indent, keys sorted
+std::string json_object(const std::vector<std::pair<std::string, std::string>>& kv, int ind) {
+  if (kv.empty()) return "{}";
+  auto sorted = kv;
+  std::sort(sorted.begin(), sorted.end(),
+            [](const auto& a, const auto& b) { return a.first < b.first; });
+  const std::string pad(ind + 2, ' ');
+  std::string o = "{\n";
+  for (size_t i = 0; i < sorted.size(); ++i)
+    o += pad + json_string(sorted[i].first) + ": " + sorted[i].second +
+         (i + 1 < sorted.size() ? ",\n" : "\n");
+  return o + std::string(ind, ' ') + "}";
+}
+
+std::string json_array(const std::vector<std::string>& items, int ind) {
+  if (items.empty()) return "[]";
+  const std::string pad(ind + 2, ' ');
+  std::string o = "[\n";
+  for (size_t i = 0; i < items.size(); ++i)
+    o += pad + items[i] + (i + 1 < items.size() ? ",\n" : "\n");
+  return o + std::string(ind, ' ') + "]";
+}
+
+}  // namespace
+
 QAP_API std::string BoundReport::to_json() const {
-  std::ostringstream o;
-  o.precision(17);
-  auto num = [&](double v) {
-    std::ostringstream t;
-    t.precision(17);
-    t << v;
-    return t.str();
-  };
-  o << "{\n  \"instance\": \"" << instance << "\",\n  \"variant\": \"" << variant
-    << "\",\n  \"sa_enabled\": " << (sa_enabled ? "true" : "false")
-    << ",\n  \"best_bound\": " << num(best_bound);
-  if (std::isfinite(upper_bound)) o << ",\n  \"upper_bound\": " << num(upper_bound);
-  if (std::isfinite(gap)) o << ",\n  \"gap\": " << num(gap);
-  o << ",\n  \"termination\": \"" << termination << "\",\n  \"iterations\": " << iterations
-    << ",\n  \"wall_ms\": " << num(wall_ms);
+  std::vector<std::pair<std::string, std::string>> kv;
+  kv.emplace_back("instance", json_string(instance));
+  kv.emplace_back("variant", json_string(variant));
+  kv.emplace_back("sa_enabled", sa_enabled ? "true" : "false");
+  kv.emplace_back("best_bound", json_double(best_bound));
+  if (std::isfinite(upper_bound)) kv.emplace_back("upper_bound", json_double(upper_bound));
+  if (std::isfinite(gap)) kv.emplace_back("gap", json_double(gap));
+  kv.emplace_back("termination", json_string(termination));
+  kv.emplace_back("iterations", std::to_string(iterations));
+  kv.emplace_back("wall_ms", json_double(wall_ms));
   if (!certificate.empty()) {
-    o << ",\n  \"certificate\": [";
-    for (size_t i = 0; i < certificate.size(); ++i) o << (i ? ", " : "") << certificate[i];
-    o << "],\n  \"certificate_value\": " << num(certificate_value);
+    std::vector<std::string> c;
+    for (int x : certificate) c.push_back(std::to_string(x));
+    kv.emplace_back("certificate", json_array(c, 2));
+    kv.emplace_back("certificate_value", json_double(certificate_value));
   }
-  o << ",\n  \"records\": [";
-  for (size_t k = 0; k < records.size(); ++k) {
-    const auto& r = records[k];
-    o << (k ? "," : "") << "\n    {\"m\": " << r.iteration << ", \"bound\": " << num(r.bound)
-      << ", \"gap\": " << num(std::isfinite(r.gap) ? r.gap : -1.0) << ", \"z_ms\": " << num(r.z_ms)
-      << ", \"y_ms\": " << num(r.y_ms) << ", \"x_ms\": " << num(r.x_ms) << "}";
-  }
-  o << (records.empty() ? "]" : "\n  ]") << "\n}";
-  return o.str();
+  std::vector<std::string> recs;
+  for (const auto& r : records)
+    recs.push_back(json_object({{"m", std::to_string(r.iteration)},
+                                {"bound", json_double(r.bound)},
+                                {"gap", json_double(std::isfinite(r.gap) ? r.gap : -1.0)},
+                                {"z_ms", json_double(r.z_ms)},
+                                {"y_ms", json_double(r.y_ms)},
+                                {"x_ms", json_double(r.x_ms)}},
+                               4));
+  kv.emplace_back("records", json_array(recs, 2));
+  return json_object(kv, 0);
 }
 
 QAP_API std::string BoundReport::to_csv() const {
@@ -590,3 +871,42 @@ QAP_API std::string BoundReport::to_csv() const {
 }
 
 }  // namespace qap
+
+// BoundReport::to_json through the C-ABI (tests compare it byte for byte with
+// the reference's nlohmann output).  recs: 6 doubles per record (iteration,
+// bound, gap, z_ms, y_ms, x_ms).
+extern "C" QAP_API int qapb_report_json(const char* instance, const char* variant, int sa_enabled,
+                                        double best_bound, double upper_bound, double gap,
+                                        const char* termination, int iterations, double wall_ms,
+                                        const int* cert, int ncert, double cert_value,
+                                        const double* recs, int nrec, char* out, size_t cap,
+                                        size_t* len) {
+  qap::BoundReport r;
+  r.instance = instance ? instance : "";
+  r.variant = variant ? variant : "";
+  r.sa_enabled = sa_enabled != 0;
+  r.best_bound = best_bound;
+  r.upper_bound = upper_bound;
+  r.gap = gap;
+  r.termination = termination ? termination : "";
+  r.iterations = iterations;
+  r.wall_ms = wall_ms;
+  r.certificate.assign(cert, cert + (cert ? ncert : 0));
+  r.certificate_value = cert_value;
+  for (int k = 0; k < nrec; ++k) {
+    qap::IterationRecord x;
+    x.iteration = (int)recs[6 * k];
+    x.bound = recs[6 * k + 1];
+    x.gap = recs[6 * k + 2];
+    x.z_ms = recs[6 * k + 3];
+    x.y_ms = recs[6 * k + 4];
+    x.x_ms = recs[6 * k + 5];
+    r.records.push_back(x);
+  }
+  const std::string j = r.to_json();
+  if (len) *len = j.size();
+  if (!out || cap <= j.size()) return QAPB_EINVAL;
+  std::memcpy(out, j.c_str(), j.size() + 1);
+  return QAPB_OK;
+}
+

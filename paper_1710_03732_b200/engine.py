@@ -65,6 +65,10 @@ lib.qapb_store_info.argtypes = [_vp, _P(C.c_int), _P(C.c_double)]
 lib.qapb_store_download.argtypes = [_vp, _vp, _vp, _vp, _P(C.c_double)]
 lib.qapb_store_destroy.argtypes = [_vp]
 lib.qapb_engine_create_from_store.argtypes = [_vp, _P(Config), _P(_vp)]
+lib.qapb_report_json.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_double,
+                                 C.c_double, C.c_char_p, C.c_int, C.c_double, _vp, C.c_int,
+                                 C.c_double, _vp, C.c_int, C.c_char_p, C.c_size_t,
+                                 _P(C.c_size_t)]
 lib.qapb_device_count.argtypes = [_P(C.c_int)]
 lib.qapb_engine_enqueue.argtypes = [_vp, C.c_int]
 lib.qapb_engine_synchronize.argtypes = [_vp]
@@ -386,6 +390,39 @@ class BoundReport:
     certificate_value: float = 0.0
     wall_ms: float = 0.0
     records: List[IterationRecord] = field(default_factory=list)
+
+    def to_json(self) -> str:
+        """rlt2.cpp:604-630, byte-identical to the reference (qapb_report_json)."""
+        recs = np.array([[r.iteration, r.bound, r.gap, r.z_ms, r.y_ms, r.x_ms]
+                         for r in self.records], np.float64).reshape(-1)
+        cert = (C.c_int * len(self.certificate))(*self.certificate) if self.certificate else None
+        ln = C.c_size_t()
+        lib.qapb_report_json(self.instance.encode(), self.variant.encode(), int(self.sa_enabled),
+                             self.best_bound, self.upper_bound, self.gap,
+                             self.termination.encode(), self.iterations, self.wall_ms, cert,
+                             len(self.certificate), self.certificate_value,
+                             dptr(recs) if len(self.records) else None, len(self.records), None,
+                             0, C.byref(ln))
+        buf = C.create_string_buffer(ln.value + 1)
+        _check(lib.qapb_report_json(self.instance.encode(), self.variant.encode(),
+                                    int(self.sa_enabled), self.best_bound, self.upper_bound,
+                                    self.gap, self.termination.encode(), self.iterations,
+                                    self.wall_ms, cert, len(self.certificate),
+                                    self.certificate_value,
+                                    dptr(recs) if len(self.records) else None,
+                                    len(self.records), buf, len(buf), C.byref(ln)))
+        return buf.value.decode()
+
+    def to_csv(self) -> str:
+        """rlt2.cpp:632-640 (default ostream formatting, precision 6)."""
+        def g(x):
+            s = "%g" % x
+            return "inf" if s == "inf" else ("-inf" if s == "-inf" else s)
+        out = ["iteration,bound,gap,z_ms,y_ms,x_ms"]
+        for r in self.records:
+            gap = r.gap if math.isfinite(r.gap) else -1.0
+            out.append(f"{r.iteration},{g(r.bound)},{g(gap)},{g(r.z_ms)},{g(r.y_ms)},{g(r.x_ms)}")
+        return "\n".join(out) + "\n"
 
 
 def _report(rep: Report, recs, cert, cfg: AscentConfig) -> BoundReport:
