@@ -66,6 +66,8 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   const bool real = lane < m;
   const double* __restrict__ colp = cost + (real ? lane : m - 1);
+  // During the solve L.p holds the matched row's byte offset p*m*8 (-1 when
+  // free): the next step's cost address is then one add away.
   L.p[0] = -1;
   L.w[0] = 0.0;
   L.v[0] = 0.0;
@@ -78,11 +80,11 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   for (int i = 0; i < m && !bad; ++i) {  // lap.cpp:33
     double minv = INF;
     if (lane == m) {  // p[m] = i; u[i] is still 0
-      L.p[0] = i;
+      L.p[0] = i * m * 8;
       L.w[0] = 0.0;
     }
     bool used = !real;  // padding lanes (and the virtual column m) never relax
-    int j0 = m, i0 = i;
+    int j0 = m, i0 = i * m * 8;
     double ui0 = 0.0;
     while (true) {  // lap.cpp:40-67 (at most m+1 steps: finite costs, checked above)
       // a used column's minv is never read again in this row (lap.cpp:47,58-64):
@@ -91,8 +93,9 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
         used = true;
         minv = INF;
       }
-      const double cur = dsub(dsub(colp[i0 * m], ui0), L.v[0]);  // lap.cpp:48
-      if (!used && cur < minv) {                                  // lap.cpp:49-52
+      const double cv = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(colp) + i0);
+      const double cur = dsub(dsub(cv, ui0), L.v[0]);  // lap.cpp:48
+      if (!used && cur < minv) {                              // lap.cpp:49-52
         minv = cur;
         way = j0;
       }
@@ -102,11 +105,13 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
       const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
       const int j1 = __ffs(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin)) - 1;
       const double delta = __shfl_sync(QAPB_FULL, minv, j1);
-      minv = dsub(minv, delta);                    // lap.cpp:63 (inf stays inf when used)
-      if (used) {  // lap.cpp:60-61
-        L.w[0] = dadd(L.w[0], delta);
-        L.v[0] = dsub(L.v[0], delta);
-      }
+      minv = dsub(minv, delta);  // lap.cpp:63 (inf stays inf when used)
+      // lap.cpp:60-61.  Adding +0.0 on unused columns is exact: u and v start
+      // at +0.0 and only ever receive sums/differences that cannot produce
+      // -0.0 from a non-negative-zero operand, so x + 0.0 == x bitwise here.
+      const double du = used ? delta : 0.0;
+      L.w[0] = dadd(L.w[0], du);
+      L.v[0] = dsub(L.v[0], du);
       j0 = j1;
       const int pj = __shfl_sync(QAPB_FULL, L.p[0], j1);
       const double wj = __shfl_sync(QAPB_FULL, L.w[0], j1);
@@ -130,7 +135,9 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
     L.w[0] = L.v[0] = __longlong_as_double(0x7ff8000000000000ll);
     return L.w[0];
   }
-  const double term = real ? cost[(size_t)L.p[0] * m + lane] : 0.0;
+  const int prow = L.p[0] < 0 ? -1 : L.p[0] / (8 * m);  // back to row indices
+  L.p[0] = prow;
+  const double term = real ? cost[(size_t)prow * m + lane] : 0.0;
   double value = 0.0;  // lap.cpp:75-80
   for (int l = 0; l < m; ++l) value = dadd(value, __shfl_sync(QAPB_FULL, term, l));
   return value;
