@@ -182,8 +182,7 @@ void Engine::alloc() {
   dalloc(&fpair_ij_, fpairs_);
   plan_pipeline();
   split_mode_ = env_int("QAPB_X3SPLIT", 2);
-  split_ = world_ == 1 && !is_two_phase() && !cfg_.sa_enabled && stage_ev_.size() == 1 &&
-           split_mode_ != 0;
+  split_ = world_ == 1 && !is_two_phase() && !cfg_.sa_enabled && split_mode_ != 0;
   if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
     const size_t nx = (size_t)ntriples_ * nchunks_ * lpairs_ * chunk_;
     dalloc(&x3buf_, nx);
@@ -534,9 +533,9 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
   p.theta_ref = theta_ref ? theta_ref + t0 : nullptr;
   p.err_tile = &S_->err_tile;
   p.tile_base = t0;
-  if (split_ && t0 == 0 && count == tiles_) {  // X3 split (FoldParams::x3buf)
+  if (split_) {  // X3 split (FoldParams::x3buf)
     p.x3buf = x3buf_;
-    p.costs_w = costs;
+    p.costs_w = costs + (size_t)t0 * esz;
     p.x3_chunk = chunk_;
     p.x3_nchunks = nchunks_;
     p.fpair_ij = fpair_ij_;
@@ -553,6 +552,7 @@ FoldParams Engine::fold_params(int stage) const {
   f.m = m_;
   f.triples = triples_ + 3 * (size_t)(stage < 0 ? 0 : stage_t0_[stage]);
   f.ntriples = stage < 0 ? ntriples_ : stage_tiles_[stage];
+  f.tri0 = stage < 0 ? 0 : stage_t0_[stage];
   f.chunk = chunk_;
   f.nchunks = nchunks_;
   f.kz = cfg_.kappa_z_upper;

@@ -148,7 +148,7 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
   f.fbc = ix.fpair(f.b, f.c);
   f.esz = (size_t)ix.esz;
   f.lpairs = ix.lpairs;
-  f.unit = unit;
+  f.unit = unit + P.tri0 * P.nchunks;  // global unit (pipelined stages fold triple ranges)
   f.C = P.chunk;
   f.x3buf = P.x3buf;
   f.d3 = P.d3;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
     const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
     const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
     const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
-    const size_t ub = ((size_t)T * nch + ch) * lpairs * C;  // fold-order base of the unit
+    const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;  // fold-order base of the unit
     // ---- stage: every load of the unit in flight before one wait ----
 #pragma unroll
     for (int k = 0; k < kFoldSlots; ++k) {
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
       if constexpr (MODE == 1)
         x3_lanes<CPL>(*P.sh, P.fpair_ij, n, tg, lane, X, xb, tb);
       else
-        x3_split_lanes<CPL>(P, n, tg, lane, X, xb, tb);
+        x3_split_lanes<CPL>(P, n, P.tile_base + tg, lane, X, xb, tb);
       if (P.patch) {  // remote-folded / split cells: the fold stored their new cost
 #pragma unroll 4
         for (int a = 0; a < xb; ++a) {

@@ -113,6 +113,7 @@ struct FoldParams {
   int m;
   const int* triples;  // (a,b,c) a<b<c, 3 ints each, lexicographic
   int ntriples, chunk, nchunks;  // triples of this launch start at `triples`
+  int tri0;                      // global index of the launch's first triple
   double kz, phi;
   int fast;
   double* d;           // D' (store)

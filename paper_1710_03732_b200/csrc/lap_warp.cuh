@@ -77,35 +77,36 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   bool ok = true;
   for (int e = lane; e < m * m; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
   const bool bad = !__all_sync(QAPB_FULL, ok);
+  // A used column (and padding lanes, and the virtual column m) carries
+  // minv = NaN: `cur < NaN` is false, so it never relaxes, and its order key
+  // (0xfff8...) sorts above every finite and +inf key, so it is never the
+  // argmin while an unused column remains (lap.cpp:47,58-64).  `used` is
+  // therefore just isnan(minv).
+  const double QNAN = __longlong_as_double(0x7ff8000000000000ll);
   for (int i = 0; i < m && !bad; ++i) {  // lap.cpp:33
-    double minv = INF;
+    double minv = real ? INF : QNAN;
     if (lane == m) {  // p[m] = i; u[i] is still 0
       L.p[0] = i * m * 8;
       L.w[0] = 0.0;
     }
-    bool used = !real;  // padding lanes (and the virtual column m) never relax
     int j0 = m, i0 = i * m * 8;
     double ui0 = 0.0;
     while (true) {  // lap.cpp:40-67 (at most m+1 steps: finite costs, checked above)
-      // a used column's minv is never read again in this row (lap.cpp:47,58-64):
-      // park it at +inf so the order key needs no activity mask
-      if (lane == j0) {
-        used = true;
-        minv = INF;
-      }
+      if (lane == j0) minv = QNAN;  // column j0 joins the tree
       const double cv = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(colp) + i0);
       const double cur = dsub(dsub(cv, ui0), L.v[0]);  // lap.cpp:48
-      if (!used && cur < minv) {                              // lap.cpp:49-52
+      if (cur < minv) {                                 // lap.cpp:49-52 (false when used)
         minv = cur;
         way = j0;
       }
-      unsigned hi, lo;  // order key of minv (+inf for used / padding lanes)
+      unsigned hi, lo;  // order key of minv (NaN keys last: used / padding lanes)
       ordkey2(minv, hi, lo);
       const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
       const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
       const int j1 = __ffs(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin)) - 1;
       const double delta = __shfl_sync(QAPB_FULL, minv, j1);
-      minv = dsub(minv, delta);  // lap.cpp:63 (inf stays inf when used)
+      const bool used = isnan(minv);
+      minv = dsub(minv, delta);  // lap.cpp:63 (NaN stays NaN when used)
       // lap.cpp:60-61.  Adding +0.0 on unused columns is exact: u and v start
       // at +0.0 and only ever receive sums/differences that cannot produce
       // -0.0 from a non-negative-zero operand, so x + 0.0 == x bitwise here.
