@@ -608,6 +608,11 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
 // Per-lane view of a sharded Z tile (b,c,pb,pc) for the fused X3 exchange:
 // rows a < b are X3 members of families (a,b,c) whose fold owner is
 // owner(pa) of the column's location pa (ShardInfo, kernels.h).
+// C(k, 3) for 0 <= k <= 1624 in 32-bit arithmetic (triple indices)
+__device__ __forceinline__ int c3u(int k) {
+  return (int)((unsigned)(k * (k - 1)) * (unsigned)(k - 2) / 6u);
+}
+
 struct X3Lane {
   const double* gsrc = nullptr;  // cost of row a: gsrc[T(a,b,c) * gstride] (null: local column)
   double* sdst = nullptr;        // pi of row a: sdst[a * nA] (fold owner's buffer, peer)
@@ -617,7 +622,7 @@ struct X3Lane {
 
 template <int CPL>
 __device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_ij, int n, int tg,
-                                         int lane, X3Lane (&X)[CPL], int& b, long long& tb) {
+                                         int lane, X3Lane (&X)[CPL], int& b, int& tb) {
   const int nm1 = n - 1, m = n - 2, lpairs = n * nm1;
   const int f = tg / lpairs, lp = tg - f * lpairs;
   const int ij = fpair_ij[f];
@@ -628,7 +633,7 @@ __device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_i
   const int me = sh.rank, p_lo = sh.pbound[me], nB = sh.pbound[me + 1] - p_lo;
   const int pci = pc - (pc > pb);
   // T(a,b,c) = tri(a+1) - C(n-b,2) + (c-b-1), tri(x) = C(n,3) - C(n-x,3)
-  tb = (long long)n * (n - 1) * (n - 2) / 6 - (long long)(n - b) * (n - b - 1) / 2 + (c - b - 1);
+  tb = c3u(n) - (n - b) * (n - b - 1) / 2 + (c - b - 1);
   const size_t rows_base = (size_t)nB * nm1 * sh.rows_before[f] + (size_t)(lp - p_lo * nm1) * b;
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
@@ -651,7 +656,7 @@ __device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_i
 // pa of tile (b,c,pb,pc) maps to slot ((T*nch + pa/C)*lpairs + lp)*C + pa%C.
 template <int CPL>
 __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, int tg, int lane,
-                                               X3Lane (&X)[CPL], int& b, long long& tb) {
+                                               X3Lane (&X)[CPL], int& b, int& tb) {
   const int nm1 = n - 1, m = n - 2, lpairs = n * nm1;
   const int f = tg / lpairs, lp = tg - f * lpairs;
   const int ij = P.fpair_ij[f];
@@ -659,7 +664,7 @@ __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, i
   const int c = ij >> 16;
   const int pb = lp / nm1, qq = lp - pb * nm1, pc = qq + (qq >= pb);
   const int lo = min(pb, pc), hi = max(pb, pc);
-  tb = (long long)n * (n - 1) * (n - 2) / 6 - (long long)(n - b) * (n - b - 1) / 2 + (c - b - 1);
+  tb = c3u(n) - (n - b) * (n - b - 1) / 2 + (c - b - 1);
   const int C = P.x3_chunk;
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
@@ -729,7 +734,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
     const int tnn = grab();
     X3Lane X[CPL];
     int xb = 0;
-    long long tb = 0;
+    int tb = 0;
     if constexpr (MODE != 0) {
       const int n = m + 2;
       if constexpr (MODE == 1)
@@ -739,7 +744,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
       if (P.patch) {  // remote-folded / split cells: the fold stored their new cost
 #pragma unroll 4
         for (int a = 0; a < xb; ++a) {
-          const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
+          const int T = tb - c3u(n - a - 1);  // T(a,b,c) = tb - C(n-a-1, 3)
 #pragma unroll
           for (int s = 0; s < CPL; ++s) {
             if (!X[s].gsrc) continue;
@@ -770,24 +775,36 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
                               P.u ? P.u + (size_t)tg * m : nullptr,
                               P.v ? P.v + (size_t)tg * m : nullptr);
     if constexpr (MODE != 0) {
-      warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
-      // pi of the X3 cells folded elsewhere -> their fold slots (peer stores
-      // when sharded, the split buffer on one GPU)
+      // slack (rlt2.cpp:320-322) of the whole tile; rows a < b also go to the
+      // X3 cells' fold slots (peer stores when sharded, the split buffer on
+      // one GPU), computed once
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {
+        const int j = s * 32 + lane;
+        if (j < m) urow[L.p[s]] = L.w[s];
+      }
+      __syncwarp();
+      double* __restrict__ out = P.pi + (size_t)tg * esz;
       const int n = m + 2;
-      for (int a = 0; a < xb; ++a) {
+      for (int a = 0; a < m; ++a) {
         const double ua = urow[a];
-        const long long T = tb - (long long)(n - a - 1) * (n - a - 2) * (n - a - 3) / 6;
+        const bool x3row = a < xb;
+        const int T = tb - c3u(n - a - 1);  // T(a,b,c), rows a < b
 #pragma unroll
         for (int s = 0; s < CPL; ++s) {
-          if (!X[s].gsrc) continue;
           const int j = s * 32 + lane;
+          if (j >= m) continue;
           const double sl = dsub(dsub(cb[a * m + j], ua), L.v[s]);
-          if constexpr (MODE == 1)
-            X[s].sdst[(size_t)a * X[s].nA] = sl;
-          else
-            X[s].sdst[(size_t)T * X[s].gstride] = sl;
+          out[a * m + j] = sl;
+          if (x3row && X[s].gsrc) {
+            if constexpr (MODE == 1)
+              X[s].sdst[(size_t)a * X[s].nA] = sl;
+            else
+              X[s].sdst[(size_t)T * X[s].gstride] = sl;
+          }
         }
       }
+      __syncwarp();
     } else if (P.pi) {
       warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
     }

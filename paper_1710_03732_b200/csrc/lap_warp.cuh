@@ -83,13 +83,17 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   // argmin while an unused column remains (lap.cpp:47,58-64).  `used` is
   // therefore just isnan(minv).
   const double QNAN = __longlong_as_double(0x7ff8000000000000ll);
-  for (int i = 0; i < m && !bad; ++i) {  // lap.cpp:33
-    double minv = real ? INF : QNAN;
-    if (lane == m) {  // p[m] = i; u[i] is still 0
-      L.p[0] = i * m * 8;
+  const bool virt = lane == m;
+  const double minv0 = real ? INF : QNAN;
+  const int m8 = m * 8;
+  int row8 = 0;  // i*m*8
+  for (int i = 0; i < m && !bad; ++i, row8 += m8) {  // lap.cpp:33
+    double minv = minv0;
+    if (virt) {  // p[m] = i; u[i] is still 0
+      L.p[0] = row8;
       L.w[0] = 0.0;
     }
-    int j0 = m, i0 = i * m * 8;
+    int j0 = m, i0 = row8;
     double ui0 = 0.0;
     while (true) {  // lap.cpp:40-67 (at most m+1 steps: finite costs, checked above)
       if (lane == j0) minv = QNAN;  // column j0 joins the tree
