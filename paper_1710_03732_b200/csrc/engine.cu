@@ -182,9 +182,16 @@ void Engine::alloc() {
   dalloc(&fpair_ij_, fpairs_);
   plan_pipeline();
   split_mode_ = env_int("QAPB_X3SPLIT", 2);
-  split_ = world_ == 1 && !is_two_phase() && !cfg_.sa_enabled && split_mode_ != 0;
+  // sharded engines split only their local X3 members, in hybrid mode
+  split_ = !is_two_phase() && !cfg_.sa_enabled &&
+           (world_ == 1 ? split_mode_ != 0 : split_mode_ == 2);
   if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
-    const size_t nx = (size_t)ntriples_ * nchunks_ * lpairs_ * chunk_;
+    int nch = nchunks_;
+    if (world_ > 1) {
+      const std::vector<int> pb = shard_plan(m, world_);
+      nch = (pb[rank_ + 1] - pb[rank_] + chunk_ - 1) / chunk_;
+    }
+    const size_t nx = (size_t)ntriples_ * nch * lpairs_ * chunk_;
     dalloc(&x3buf_, nx);
     dalloc(&d3_, nx);
   }
@@ -440,6 +447,11 @@ void Engine::enqueue_sharded_z(int it) {
     p.sh = shard_dev_;
     p.fpair_ij = fpair_ij_;
     p.patch = it > 0 ? 1 : 0;
+    if (split_) {  // local X3 members: slack into the fold-order split buffer
+      p.x3buf = x3buf_;
+      p.x3_chunk = chunk_;
+      p.x3_nchunks = chunks_me_;
+    }
     kbegin(QAPB_K_ZLAP, st_);
     cuda_check(launch_lap_batch(p, st_), "z-stage");
     kend(st_);
@@ -503,7 +515,8 @@ void Engine::plan_pipeline() {
 
 void Engine::split_gather() {
   if (!split_) return;
-  cuda_check(launch_x3_sync(m_, chunk_, nchunks_, triples_, ntriples_, d_, d3_, 1, st_),
+  cuda_check(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
+                            p_lo_, p_hi_, d_, d3_, 1, st_),
              "x3 gather");
   d_stale_ = false;
 }
@@ -511,7 +524,8 @@ void Engine::split_gather() {
 // the tile-layout D' of the X3 members is stale after a split fold
 void Engine::split_scatter() const {
   if (!split_ || !d_stale_) return;
-  cuda_check(launch_x3_sync(m_, chunk_, nchunks_, triples_, ntriples_, d_, d3_, 0, st_),
+  cuda_check(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
+                            p_lo_, p_hi_, d_, d3_, 0, st_),
              "x3 scatter");
   cuda_check(cudaStreamSynchronize(st_), "x3 scatter");
   d_stale_ = false;

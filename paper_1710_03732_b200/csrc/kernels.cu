@@ -231,22 +231,18 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
     const int pc = pci + (pci >= pb);
     const int pa = f.pa0 + pa_l;
     if (pa != pb && pa != pc) {
-      if (f.x3buf) {  // X3 split: tile offset g; the fold-order slot follows from pb, pc, pa_l
-        const int lo = min(pb, pc), hi = max(pb, pc);
-        const int col = pa - (pa > lo) - (pa > hi);
-        fn(2, pa_l, pb, pc,
-           (size_t)(f.fbc * f.lpairs + pb * nm1 + pci) * f.esz + (size_t)f.a * nm2 + col,
-           base3 + e, -2);
-      } else {
-        // X3 lives with owner(pb); when that is another rank (xr >= 0) this
-        // rank still owns the cell's D' (its copy at g) and receives pi
-        const int lo = min(pb, pc), hi = max(pb, pc);
-        const int col = pa - (pa > lo) - (pa > hi);
-        const size_t g = (size_t)(f.fbc * f.lpairs + ix.lpair(pb, pc)) * f.esz +
-                         (size_t)f.a * nm2 + col;
-        const int xb = f.sh ? shard_owner(*f.sh, pb) : 0;
-        fn(2, pa_l, pb, pc, g, base3 + e, (!f.sh || xb == f.sh->rank) ? -1 : xb);
-      }
+      const int lo = min(pb, pc), hi = max(pb, pc);
+      const int col = pa - (pa > lo) - (pa > hi);
+      const size_t g = (size_t)(f.fbc * f.lpairs + pb * nm1 + pci) * f.esz +
+                       (size_t)f.a * nm2 + col;
+      // X3 lives with owner(pb): another rank (xr >= 0, this rank owns the
+      // cell's D' and receives pi), or here -- in the split buffers (-2) or
+      // in the tile layout (-1)
+      const int xb = f.sh ? shard_owner(*f.sh, pb) : -1;
+      if (f.sh && xb != f.sh->rank)
+        fn(2, pa_l, pb, pc, g, base3 + e, xb);
+      else
+        fn(2, pa_l, pb, pc, g, base3 + e, f.x3buf ? -2 : -1);
     }
     pa_l += dpl;
     int inc = dpr;
@@ -615,14 +611,15 @@ __device__ __forceinline__ int c3u(int k) {
 
 struct X3Lane {
   const double* gsrc = nullptr;  // cost of row a: gsrc[T(a,b,c) * gstride] (null: local column)
-  double* sdst = nullptr;        // pi of row a: sdst[a * nA] (fold owner's buffer, peer)
+  double* sdst = nullptr;        // pi of row a: sdst[a * nA] (peer row), sdst[T * gstride] (split)
   size_t gstride = 0;
   int nA = 0;
 };
 
 template <int CPL>
-__device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_ij, int n, int tg,
-                                         int lane, X3Lane (&X)[CPL], int& b, int& tb) {
+__device__ __forceinline__ void x3_lanes(const BatchLapParams& P, const ShardInfo& sh,
+                                         const int* fpair_ij, int n, int tg, int lane,
+                                         X3Lane (&X)[CPL], int& b, int& tb) {
   const int nm1 = n - 1, m = n - 2, lpairs = n * nm1;
   const int f = tg / lpairs, lp = tg - f * lpairs;
   const int ij = fpair_ij[f];
@@ -639,10 +636,19 @@ __device__ __forceinline__ void x3_lanes(const ShardInfo& sh, const int* fpair_i
   for (int s = 0; s < CPL; ++s) {
     const int j = s * 32 + lane;
     X[s].gsrc = nullptr;
+    X[s].sdst = nullptr;
     if (j >= m) continue;
     const int pa = skip2(j, lo, hi);
     const int A = shard_owner(sh, pa);
-    if (A == me) continue;
+    if (A == me) {  // folded here: with the X3 split its slack goes to the fold slot
+      if (P.x3buf) {
+        const int C = P.x3_chunk, po = pa - p_lo, ch = po / C;
+        X[s].sdst = P.x3buf + ((size_t)ch * lpairs + lp) * C + (po - ch * C);
+        X[s].gstride = (size_t)P.x3_nchunks * lpairs * C;
+        X[s].nA = 0;
+      }
+      continue;
+    }
     const int a_lo = sh.pbound[A], po = pa - a_lo, ch = po / sh.chunk;
     X[s].nA = sh.pbound[A + 1] - a_lo;
     X[s].gstride = (size_t)shard_chunks(sh, A) * nB * nm1 * sh.chunk;
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
     if constexpr (MODE != 0) {
       const int n = m + 2;
       if constexpr (MODE == 1)
-        x3_lanes<CPL>(*P.sh, P.fpair_ij, n, tg, lane, X, xb, tb);
+        x3_lanes<CPL>(P, *P.sh, P.fpair_ij, n, tg, lane, X, xb, tb);
       else
         x3_split_lanes<CPL>(P, n, P.tile_base + tg, lane, X, xb, tb);
       if (P.patch) {  // remote-folded / split cells: the fold stored their new cost
@@ -796,9 +802,9 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
           if (j >= m) continue;
           const double sl = dsub(dsub(cb[a * m + j], ua), L.v[s]);
           out[a * m + j] = sl;
-          if (x3row && X[s].gsrc) {
-            if constexpr (MODE == 1)
-              X[s].sdst[(size_t)a * X[s].nA] = sl;
+          if (x3row && X[s].sdst) {
+            if constexpr (MODE == 1)  // peer row segment, or the local split slot (nA == 0)
+              X[s].sdst[X[s].nA ? (size_t)a * X[s].nA : (size_t)T * X[s].gstride] = sl;
             else
               X[s].sdst[(size_t)T * X[s].gstride] = sl;
           }
@@ -971,9 +977,11 @@ __global__ void xfinish_kernel(XStageParams P) {
 
 // Single-GPU X3 split: copy the X3 members' D' between the tile layout (d)
 // and fold order (d3): to_d3 at engine creation, back on a store download.
+// Locations pa (fold owner) and pb (X3 owner) both in [p_lo, p_hi): the
+// rank's local split cells (the whole range on one GPU).
 __global__ void x3_sync_kernel(int n, int C, int nch, const int* __restrict__ triples,
-                               double* __restrict__ d, double* __restrict__ d3, size_t total,
-                               int to_d3) {
+                               int p_lo, int p_hi, double* __restrict__ d,
+                               double* __restrict__ d3, size_t total, int to_d3) {
   const int nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
   const size_t esz = (size_t)nm2 * nm2;
   const DIdx ix(n);
@@ -981,9 +989,9 @@ __global__ void x3_sync_kernel(int n, int C, int nch, const int* __restrict__ tr
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t u = i / ((size_t)lpairs * C);
     const int rem = (int)(i - u * lpairs * C), pair = rem / C, pa_l = rem - pair * C;
-    const int T = (int)(u / nch), ch = (int)(u - (size_t)T * nch), pa = ch * C + pa_l;
+    const int T = (int)(u / nch), ch = (int)(u - (size_t)T * nch), pa = p_lo + ch * C + pa_l;
     const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
-    if (pa >= n || pa == pb || pa == pc) continue;
+    if (pa >= p_hi || pa == pb || pa == pc || pb < p_lo || pb >= p_hi) continue;
     const int a = triples[3 * T], b = triples[3 * T + 1], c = triples[3 * T + 2];
     const int lo = min(pb, pc), hi = max(pb, pc), col = pa - (pa > lo) - (pa > hi);
     const size_t g = ((size_t)ix.fpair(b, c) * lpairs + pair) * esz + (size_t)a * nm2 + col;
@@ -1193,9 +1201,10 @@ cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
-                           double* d, double* d3, int to_d3, cudaStream_t st) {
+                           int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st) {
   const size_t total = (size_t)ntriples * nchunks * n * (n - 1) * chunk;
-  x3_sync_kernel<<<4 * num_sms(), 256, 0, st>>>(n, chunk, nchunks, triples, d, d3, total, to_d3);
+  x3_sync_kernel<<<4 * num_sms(), 256, 0, st>>>(n, chunk, nchunks, triples, p_lo, p_hi, d, d3,
+                                                total, to_d3);
   return cudaGetLastError();
 }
 

@@ -195,7 +195,7 @@ cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
 // theta of every rank's tile runs <-> one contiguous buffer (rank segments)
 // single-GPU X3 split: D' of the X3 members, tile layout <-> fold order
 cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
-                           double* d, double* d3, int to_d3, cudaStream_t st);
+                           int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st);
 cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
                               cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
