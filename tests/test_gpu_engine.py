@@ -8,6 +8,7 @@ import pytest
 
 from conftest import digest, golden_instance, hexs
 from oracle.pyoracle import Oracle, available, best_oracle
+from paper_1710_03732_b200 import abi
 from paper_1710_03732_b200.abi import default_config
 
 pytestmark = pytest.mark.gpu
@@ -171,3 +172,32 @@ def test_launch_accounting(q, golden):
     n0 = eng.launch_count()
     eng.run()
     assert eng.launch_count() - n0 >= 10 * 4
+
+
+def test_n30_n42_reference_pins(q):
+    """Large sizes.  n=30: bitwise against the compiled reference (oracle/_ref) for 4
+    iterations of generate_instance(30,1,99) F1 and S1 when it is present.  n=42 (the
+    sko42 size: 2.37 G z cells, the CPL=2 LAP path for m=40): generate_instance(42,1,99) S1
+    iterations 1-2 against the reference values printed in SURVEY.md §8c (16 significant
+    digits, so compared to 1e-15 relative; a reference run there takes ~1 min/iteration)."""
+    inst30 = q.generate_instance(30, 1, 99)
+    for variant in ("F1", "S1"):
+        eng = q.AscentEngine.from_instance(inst30, q.AscentConfig(variant=variant, iter_limit=4))
+        got = [eng.iterate() for _ in range(4)]
+        eng.close()
+        if available("ref"):
+            cfg = default_config()
+            cfg.variant = abi.VARIANTS[variant]
+            cfg.iter_limit = 4
+            ref = Oracle("ref").engine_from_instance(inst30.flow, inst30.dist, None, cfg)
+            want = [ref.iterate() for _ in range(4)]
+            assert got == want, (variant, got, want)
+        else:
+            want4 = {"F1": 1538557.650137826, "S1": 1538728.316958316}[variant]
+            assert got[0] == 1473912.0 and math.isclose(got[3], want4, rel_tol=1e-15)
+    eng = q.AscentEngine.from_instance(q.generate_instance(42, 1, 99),
+                                       q.AscentConfig(variant="S1", iter_limit=2))
+    got = [eng.iterate() for _ in range(2)]
+    eng.close()
+    assert got[0] == 3146129.0
+    assert math.isclose(got[1], 3184361.336432928, rel_tol=1e-15), got
