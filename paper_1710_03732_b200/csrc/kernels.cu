@@ -262,10 +262,15 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
 // dense [chunk][n][n+1] cube each (odd pitch: conflict-free column walks),
 // the CTA's D' / cost values in visit order, and the push terms.
 struct FoldSmem {
-  int np, cube, nslots;
+  // cube[pa_l][pb][pc] with row pitch np = n+1 and pa_l stride ps = n*np
+  // rounded to 8 (mod 16) doubles: consecutive pb rows fall on distinct bank
+  // pairs and the two pa_l halves of an X3 access (pa fastest) on disjoint
+  // bank halves, so neither the cp.async fills nor the reads conflict
+  int np, ps, cube, nslots;
   __host__ __device__ FoldSmem(int n, int chunk)
-      : np(n + 1), cube(chunk * n * (n + 1)),
+      : np(n + 1), ps(n * (n + 1) + ((8 - (n * (n + 1)) % 16) + 16) % 16), cube(chunk * ps),
         nslots(2 * chunk * (n - 1) * (n - 2) + chunk * n * (n - 1)) {}
+  __host__ __device__ int fi(int pa_l, int pb, int pc) const { return pa_l * ps + pb * np + pc; }
   __host__ __device__ size_t pi_off() const { return 0; }
   __host__ __device__ size_t val_off() const { return (size_t)3 * cube; }
   __host__ __device__ size_t push_off() const { return (size_t)3 * cube + nslots; }
@@ -283,7 +288,7 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
   double* S = sm + L.pi_off();
   double* V = sm + L.val_off();
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
-    double* sp = S + (size_t)mem * L.cube + (pa_l * f.n + pb) * L.np + pc;
+    double* sp = S + (size_t)mem * L.cube + L.fi(pa_l, pb, pc);
     if (xr == -2) {  // X3 split: pi and D' in fold order
       const size_t ui = x3_slot(f, pa_l, pb, pc);
       cp_async8(sp, f.x3buf + ui);
@@ -339,7 +344,7 @@ __device__ __forceinline__ void fold_update(const FoldParams& P, const FamilyCtx
   double* __restrict__ incz = P.incz;
   const int fast = P.fast;
   for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
-    const int fi = (pa_l * n + pb) * L.np + pc;
+    const int fi = L.fi(pa_l, pb, pc);
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     const double s1 = dadd(dmul(kz, p1), U1[pa_l * n + pb]);  // rlt2.cpp:289-290
     const double s2 = dadd(dmul(kz, p2), U2[pa_l * n + pc]);
@@ -443,8 +448,7 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       const int pa = pa0 + pa_l, q = qi + (qi >= pa);
       const int other = skip2(r, min(pa, q), max(pa, q));
       rel12[k] = (uint32_t)lpair(pa, q) * esz + r;
-      fi12[k] = (uint32_t)((pa_l * n + q) * np + other) |
-                ((uint32_t)((pa_l * n + other) * np + q) << 16);
+      fi12[k] = (uint32_t)L.fi(pa_l, q, other) | ((uint32_t)L.fi(pa_l, other, q) << 16);
       ju12[k] = (uint32_t)(pa_l * nm1 + qi) | ((uint32_t)(pa_l * nm1 + other - (other > pa)) << 16);
       lu12[k] = (uint32_t)lpair(q, other) | ((uint32_t)lpair(other, q) << 16);
     }
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       if (pa != pb && pa != pc) {
         const int lo = min(pb, pc), hi = max(pb, pc);
         const int col = pa - (pa > lo) - (pa > hi);
-        x3a[k] = (uint32_t)((pa_l * n + pb) * np + pc) | ((uint32_t)col << 12) |
+        x3a[k] = (uint32_t)L.fi(pa_l, pb, pc) | ((uint32_t)col << 12) |
                  ((uint32_t)pair << 18);
         x3b[k] = (uint32_t)(pa_l * nm1 + pb - (pb > pa)) |
                  ((uint32_t)(pa_l * nm1 + pc - (pc > pa)) << 8) | ((uint32_t)pa_l << 16);
@@ -582,7 +586,7 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
   double* __restrict__ costs = P.costs;
   const double tol = 1e-9;
   for_family_cells(f, C, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int) {
-    const int fi = (pa_l * n + pb) * L.np + pc;
+    const int fi = L.fi(pa_l, pb, pc);
     const double p1 = S[fi], p2 = S[L.cube + fi], p3 = S[2 * L.cube + fi];
     double total = 0.0;
     int nb = 3;
@@ -1078,7 +1082,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
   if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_LEAN", 1) &&
       nz < 4294967295.0 && p.chunk * (n - 1) * (n - 2) <= kFoldSlots * 256 &&
-      p.chunk * n * (n - 1) <= kFoldSlots * 256 && p.chunk * n * (n + 1) < 4096 && n < 64 &&
+      p.chunk * n * (n - 1) <= kFoldSlots * 256 && FoldSmem(n, p.chunk).cube < 4096 && n < 64 &&
       p.chunk * (n - 1) < 256 && n * (n - 1) < 16384) {
     cudaFuncSetAttribute(zfold_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)std::max<size_t>(smem, 48 * 1024));
