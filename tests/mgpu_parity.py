@@ -58,6 +58,25 @@ def main():
                                              early_stop_delta=0.002, device=local))
     results["run_early_stop"] = ([r.bound for r in rep.records] == [r.bound for r in ref.records]
                                  and rep.termination == ref.termination)
+    # odd and small sizes (non-TMA LAP path for odd m, uneven location ranges, ranks
+    # owning 1-2 locations) with linear terms: sharded == single-GPU engine, bitwise
+    for n in (5, 7, 9, 11, 13):
+        inst = q.generate_instance(n, 1000 + n, 50)
+        inst.linear[:] = np.arange(n * n).reshape(n, n) % 7
+        for variant in ("F1", "S1"):
+            if world > n:
+                continue
+            idobj = [q.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idobj, src=0)
+            cfg = q.AscentConfig(variant=variant, iter_limit=12, device=local)
+            eng = q.AscentEngine.from_instance_sharded(inst, cfg, rank, world, idobj[0])
+            got = [eng.iterate() for _ in range(12)]
+            eng.close()
+            one = q.AscentEngine.from_instance(inst, q.AscentConfig(variant=variant,
+                                                                   iter_limit=12, device=local))
+            want = [one.iterate() for _ in range(12)]
+            one.close()
+            results[f"n{n}_{variant}"] = got == want or f"{got} != {want}"
     allres = [None] * world
     dist.all_gather_object(allres, results)
     ok = all(v is True for r in allres for v in r.values())
