@@ -75,7 +75,17 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   // Non-finite (or overflow-prone) costs would let the search run forever
   // (the reference is undefined there too): check the tile once and bail out.
   bool ok = true;
-  for (int e = lane; e < m * m; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
+  const int mm = m * m;
+  if ((reinterpret_cast<uintptr_t>(cost) & 15) == 0) {  // Z tiles: 16-byte reads
+    const double2* __restrict__ c2 = reinterpret_cast<const double2*>(cost);
+    for (int e = lane; e < (mm >> 1); e += 32) {
+      const double2 x = c2[e];
+      ok = ok && (fabs(x.x) <= 1e300) && (fabs(x.y) <= 1e300);
+    }
+    if ((mm & 1) && lane == 0) ok = ok && (fabs(cost[mm - 1]) <= 1e300);
+  } else {
+    for (int e = lane; e < mm; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
+  }
   const bool bad = !__all_sync(QAPB_FULL, ok);
   // A used column (and padding lanes, and the virtual column m) carries
   // minv = NaN: `cur < NaN` is false, so it never relaxes, and its order key
