@@ -186,14 +186,16 @@ void Engine::alloc() {
   split_ = !is_two_phase() && !cfg_.sa_enabled &&
            (world_ == 1 ? split_mode_ != 0 : split_mode_ == 2);
   if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
-    int nch = nchunks_;
+    int range = m;
     if (world_ > 1) {
       const std::vector<int> pb = shard_plan(m, world_);
-      nch = (pb[rank_ + 1] - pb[rank_] + chunk_ - 1) / chunk_;
+      range = pb[rank_ + 1] - pb[rank_];
     }
-    const size_t nx = (size_t)ntriples_ * nch * lpairs_ * chunk_;
-    dalloc(&x3buf_, nx);
-    dalloc(&d3_, nx);
+    const int nch = (range + chunk_ - 1) / chunk_;
+    x3_group_ = std::max(1, env_int("QAPB_X3_GROUP", 4) / chunk_) * chunk_;
+    x3_ngroups_ = (range + x3_group_ - 1) / x3_group_;
+    dalloc(&x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
+    dalloc(&d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
   }
   dalloc(&counter_, stage_ev_.size() + 2);
   dalloc(&S_, 1);
@@ -449,8 +451,8 @@ void Engine::enqueue_sharded_z(int it) {
     p.patch = it > 0 ? 1 : 0;
     if (split_) {  // local X3 members: slack into the fold-order split buffer
       p.x3buf = x3buf_;
-      p.x3_chunk = chunk_;
-      p.x3_nchunks = chunks_me_;
+      p.x3_group = x3_group_;
+      p.x3_ngroups = x3_ngroups_;
     }
     kbegin(QAPB_K_ZLAP, st_);
     cuda_check(launch_lap_batch(p, st_), "z-stage");
@@ -550,8 +552,8 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
   if (split_) {  // X3 split (FoldParams::x3buf)
     p.x3buf = x3buf_;
     p.costs_w = costs + (size_t)t0 * esz;
-    p.x3_chunk = chunk_;
-    p.x3_nchunks = nchunks_;
+    p.x3_group = x3_group_;
+    p.x3_ngroups = x3_ngroups_;
     p.fpair_ij = fpair_ij_;
     p.patch = (cur_iter_ > 0 && split_mode_ == 1) ? 1 : 0;
   }
@@ -583,6 +585,8 @@ FoldParams Engine::fold_params(int stage) const {
     f.x3buf = x3buf_;
     f.d3 = d3_;
     f.x3mode = split_mode_;
+    f.x3_group = x3_group_;
+    f.x3_ngroups = x3_ngroups_;
   }
   return f;
 }

@@ -117,14 +117,22 @@ struct FamilyCtx {
   int lpairs;
   const ShardInfo* sh;  // multi-GPU: X3 members owned by other ranks (null on one GPU)
   int unit, C;
-  double* x3buf;  // single-GPU X3 split (FoldParams::x3buf), else null
+  double* x3buf;  // X3 split (FoldParams::x3buf), else null
   double* d3;
   int x3mode;
+  int tglob, po0, G, ng;  // global triple, pa0 - p_lo, x3buf group and groups
 };
 
-// fold-order slot of X3 cell (pa_l, pb, pc) of the CTA's unit (X3 split)
+// fold-order slot of X3 cell (pa_l, pb, pc) of the CTA's unit in d3 (X3 split)
 __device__ __forceinline__ size_t x3_slot(const FamilyCtx& f, int pa_l, int pb, int pc) {
   return ((size_t)f.unit * f.lpairs + pb * f.nm1 + pc - (pc > pb)) * f.C + pa_l;
+}
+// its slot in x3buf: groups of G >= C locations per pair, so a Z-LAP row store
+// touches n/G segments (kernels.h, BatchLapParams::x3buf)
+__device__ __forceinline__ size_t x3_pi_slot(const FamilyCtx& f, int pa_l, int pb, int pc) {
+  const int po = f.po0 + pa_l, g = po / f.G;
+  return (((size_t)f.tglob * f.ng + g) * f.lpairs + pb * f.nm1 + pc - (pc > pb)) * f.G +
+         (po - g * f.G);
 }
 
 // unit = triple * nchunks + chunk (one CTA's work item)
@@ -153,6 +161,10 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
   f.x3buf = P.x3buf;
   f.d3 = P.d3;
   f.x3mode = P.x3mode;
+  f.tglob = P.tri0 + T;
+  f.po0 = f.pa0 - p_lo;
+  f.G = P.x3_group;
+  f.ng = P.x3_ngroups;
   return f;
 }
 
@@ -290,9 +302,8 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
   for_family_cells(f, chunk, [&](int mem, int pa_l, int pb, int pc, size_t g, int slot, int xr) {
     double* sp = S + (size_t)mem * L.cube + L.fi(pa_l, pb, pc);
     if (xr == -2) {  // X3 split: pi and D' in fold order
-      const size_t ui = x3_slot(f, pa_l, pb, pc);
-      cp_async8(sp, f.x3buf + ui);
-      cp_async8(V + slot, f.d3 + ui);
+      cp_async8(sp, f.x3buf + x3_pi_slot(f, pa_l, pb, pc));
+      cp_async8(V + slot, f.d3 + x3_slot(f, pa_l, pb, pc));
       return;
     }
     if (xr >= 0) {  // remote X3: its owner's Z-LAP stored pi; its D' lives here
@@ -363,10 +374,9 @@ __device__ __forceinline__ void fold_update(const FoldParams& P, const FamilyCtx
     const double dn = dadd(V[slot], dsub(gain, dmul(kz, own)));  // rlt2.cpp:292
     const double inc = fast ? dadd(dmul(omk, own), gain) : dn;  // rlt2.cpp:293
     if (xr == -2) {  // X3 split: D' stays in fold order
-      const size_t ui = x3_slot(f, pa_l, pb, pc);
-      f.d3[ui] = dn;
+      f.d3[x3_slot(f, pa_l, pb, pc)] = dn;
       if (f.x3mode == 1) {  // the LAP patches its tile from x3buf
-        f.x3buf[ui] = inc;
+        f.x3buf[x3_pi_slot(f, pa_l, pb, pc)] = inc;
       } else {  // hybrid: the LAP's next cost goes to the tile (scattered store)
         if (fast)
           incz[g] = inc;
@@ -491,7 +501,9 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
     const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
     const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
     const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
-    const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;  // fold-order base of the unit
+    const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;  // d3 base of the unit
+    const int G = P.x3_group, g0 = (ch * C) / G;
+    const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * G + (ch * C - g0 * G);
     // ---- stage: every load of the unit in flight before one wait ----
 #pragma unroll
     for (int k = 0; k < kFoldSlots; ++k) {
@@ -507,9 +519,9 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
     for (int k = 0; k < kFoldSlots; ++k) {
       if (x3b[k] == 0xffffffffu) continue;
       const int e = tid + k * bd;
-      const size_t ui = ub + (x3a[k] >> 18) * C + (x3b[k] >> 16);
-      cp_async8(S + 2 * cube + (x3a[k] & 0xfffu), x3buf + ui);
-      cp_async8(V + base3 + e, d3 + ui);
+      const uint32_t pr = x3a[k] >> 18, pl = x3b[k] >> 16;
+      cp_async8(S + 2 * cube + (x3a[k] & 0xfffu), x3buf + upi + pr * G + pl);
+      cp_async8(V + base3 + e, d3 + ub + pr * C + pl);
     }
     for (int e = tid; e < Pe * nm1; e += bd) {
       cp_async8(U1 + e, push + (size_t)fab * lpairs + pa0 * nm1 + e);
@@ -646,9 +658,9 @@ __device__ __forceinline__ void x3_lanes(const BatchLapParams& P, const ShardInf
     const int A = shard_owner(sh, pa);
     if (A == me) {  // folded here: with the X3 split its slack goes to the fold slot
       if (P.x3buf) {
-        const int C = P.x3_chunk, po = pa - p_lo, ch = po / C;
-        X[s].sdst = P.x3buf + ((size_t)ch * lpairs + lp) * C + (po - ch * C);
-        X[s].gstride = (size_t)P.x3_nchunks * lpairs * C;
+        const int G = P.x3_group, po = pa - p_lo, g = po / G;
+        X[s].sdst = P.x3buf + ((size_t)g * lpairs + lp) * G + (po - g * G);
+        X[s].gstride = (size_t)P.x3_ngroups * lpairs * G;
         X[s].nA = 0;
       }
       continue;
@@ -663,7 +675,7 @@ __device__ __forceinline__ void x3_lanes(const BatchLapParams& P, const ShardInf
 }
 
 // Single-GPU X3 split (kernels.h, BatchLapParams::x3buf): the lane's column
-// pa of tile (b,c,pb,pc) maps to slot ((T*nch + pa/C)*lpairs + lp)*C + pa%C.
+// pa of tile (b,c,pb,pc) maps to slot ((T*ng + pa/G)*lpairs + lp)*G + pa%G.
 template <int CPL>
 __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, int tg, int lane,
                                                X3Lane (&X)[CPL], int& b, int& tb) {
@@ -675,16 +687,16 @@ __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, i
   const int pb = lp / nm1, qq = lp - pb * nm1, pc = qq + (qq >= pb);
   const int lo = min(pb, pc), hi = max(pb, pc);
   tb = c3u(n) - (n - b) * (n - b - 1) / 2 + (c - b - 1);
-  const int C = P.x3_chunk;
+  const int G = P.x3_group;
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
     const int j = s * 32 + lane;
     X[s].gsrc = nullptr;
     if (j >= m) continue;
-    const int pa = skip2(j, lo, hi), ch = pa / C;
-    X[s].sdst = P.x3buf + ((size_t)ch * lpairs + lp) * C + (pa - ch * C);
+    const int pa = skip2(j, lo, hi), g = pa / G;
+    X[s].sdst = P.x3buf + ((size_t)g * lpairs + lp) * G + (pa - g * G);
     X[s].gsrc = X[s].sdst;
-    X[s].gstride = (size_t)P.x3_nchunks * lpairs * C;
+    X[s].gstride = (size_t)P.x3_ngroups * lpairs * G;
   }
 }
 

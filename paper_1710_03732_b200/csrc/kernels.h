@@ -49,14 +49,16 @@ struct BatchLapParams {
   const ShardInfo* sh;
   const int* fpair_ij;
   int patch;
-  // single-GPU X3 split (1-phase variants): the X3 member of every family
-  // lives in fold order in x3buf (slot ((T*nch + chunk)*lpairs + lp)*C + pa_l,
-  // holding the fold's new cost, then the LAP's slack) so neither kernel
-  // touches it with 16-byte scattered accesses in the fold; the LAP patches
-  // rows a < b from it (and writes them to costs_w) and stores their slack
+  // X3 split (1-phase variants): the X3 member T(b,c,pb,pc)[a,pa] of every
+  // family folded here keeps its D' in fold order (FoldParams::d3) and passes
+  // pi (mode 2: written by the LAP, read by the fold; mode 1 also the fold's
+  // new cost the other way) through x3buf, slot
+  //   ((T*ng + po/G)*lpairs + lpair(pb,pc))*G + po%G,  po = pa - first location,
+  // groups of G locations (a multiple of the fold chunk): the fold reads whole
+  // chunks, a Z-LAP row store touches only n/G segments
   double* x3buf;
   double* costs_w;
-  int x3_chunk, x3_nchunks;
+  int x3_group, x3_ngroups;
 };
 
 constexpr int kMaxRanks = 8;
@@ -131,6 +133,7 @@ struct FoldParams {
   double* x3buf;
   double* d3;
   int x3mode;  // 1: split (LAP patches), 2: hybrid (fold stores the cost to the tile)
+  int x3_group, x3_ngroups;  // x3buf layout (BatchLapParams::x3buf)
 };
 
 struct XYFoldParams {
