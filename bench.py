@@ -180,9 +180,12 @@ def run_reference_arm(args):
         "metric": METRIC, "impl": "reference", "value": its, "unit": "iterations/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        # same metric and config as our arm at this N (the CPU path itself is one
+        # process on the host's cores)
+        "scaling": "strong" if (world > 1 and not args.replicas) else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "laps_per_s": its * laps,
-        "config": config_block(args, world=1),
+        "config": config_block(args, world, sharded=world > 1 and not args.replicas),
         "cpu_baseline": {"value": its, "unit": "iterations/s", "cores": threads,
                          "kind": kind,
                          "sample": f"{args.steps} steady-state iterations (after {args.warmup} "
