@@ -249,12 +249,13 @@ QAPB_API qapb_status qapb_engine_kernel_times(qapb_engine* e, double* ms,
  * Rank r owns the half-Z tiles whose first location lies in
  * [p_bounds[r], p_bounds[r+1]) -- equal shares of tiles, fold work and
  * exchange volume -- and folds every facility triple for its own locations.
- * In a family the X3 member T(b,c,pb,pc)[a,pa] belongs to owner(pb): each
- * iteration owner(pb) sends sigma = kz*pi + push of those cells to owner(pa)
- * and receives their gain back (two NCCL grouped send/recv rounds); theta is
- * re-assembled with broadcasts and the O(n^4) Y/X stages run replicated, so
- * every rank holds the same bound.  Results are bitwise those of the
- * single-GPU engine. */
+ * In a family the X3 member T(b,c,pb,pc)[a,pa] lies in a tile of owner(pb):
+ * owner(pb)'s Z-LAP stores its slack into owner(pa)'s buffer and owner(pa)'s
+ * fold (which keeps its D') stores its new cost into owner(pb)'s buffer,
+ * both directly over NVLink through CUDA IPC mappings (no copy kernels); one
+ * all-reduce barrier and the theta broadcasts order them, the O(n^4) Y/X
+ * stages run replicated, so every rank holds the same bound.  Results are
+ * bitwise those of the single-GPU engine. */
 /* Location ranges per rank (p_bounds has world+1 entries). */
 QAPB_API qapb_status qapb_shard_plan(int n, int world, int* p_bounds);
 /* Doubles rank `rank` stores into (send[p]) / receives from (recv[p]) every
