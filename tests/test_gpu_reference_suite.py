@@ -1,6 +1,7 @@
-"""GPU: the reference's OWN unit tests (proj/tests/test_lap.cpp and
-test_rlt2.cpp), compiled unmodified against the B200 facade headers
-(include/qap/*.hpp) + libqapb200.so by `make -C oracle reftests`, must pass.
+"""GPU: the reference's OWN unit tests (proj/tests/test_lap.cpp, test_rlt2.cpp,
+and test_bnb.cpp with the reference's branch-and-bound proj/src/bnb.cpp bounding
+its nodes through the facade), compiled unmodified against the B200 facade
+headers (include/qap/*.hpp) + libqapb200.so by `make -C oracle reftests`, must pass.
 The binaries are built where /root/reference exists and travel in-tree
 (build/reftests); fixtures are regenerated from tests/golden/golden.json."""
 import json
@@ -25,7 +26,7 @@ def _write_fixtures(dirpath):
             fh.write(f"{inst['n']}\n\n{rows(inst['flow'])}\n\n{rows(inst['dist'])}\n")
 
 
-@pytest.mark.parametrize("name", ["test_lap_b200", "test_rlt2_b200"])
+@pytest.mark.parametrize("name", ["test_lap_b200", "test_rlt2_b200", "test_bnb_b200"])
 def test_reference_unit_tests_pass_on_b200(name, tmp_path):
     exe = os.path.join(BIN, name)
     if not os.path.exists(exe):
