@@ -17,13 +17,12 @@ BIN = os.path.join(ROOT, "build", "reftests")
 
 
 def _write_fixtures(dirpath):
-    with open(os.path.join(GOLDEN, "golden.json")) as fh:
-        g = json.load(fh)
-    for name in ("nug12", "zero", "nug5", "two"):
-        inst = g[name]
-        rows = lambda m: "\n".join(" ".join(str(int(x)) for x in r) for r in m)
-        with open(os.path.join(dirpath, f"{name}.dat"), "w") as fh:
-            fh.write(f"{inst['n']}\n\n{rows(inst['flow'])}\n\n{rows(inst['dist'])}\n")
+    """proj/fixtures/* as captured by tests/golden/make_fixtures.py."""
+    with open(os.path.join(GOLDEN, "fixtures.json")) as fh:
+        files = json.load(fh)
+    for name, text in files.items():
+        with open(os.path.join(dirpath, name), "w") as fh:
+            fh.write(text)
 
 
 @pytest.mark.parametrize("name", ["test_lap_b200", "test_rlt2_b200", "test_bnb_b200"])
