@@ -4,11 +4,13 @@
 
 #include <chrono>
 #include <climits>
+#include <cstdint>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <limits>
 
@@ -58,6 +60,32 @@ void dalloc(T** p, size_t n) {
 template <class T>
 void dfree(T*& p) {
   if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// Engine state comes from the device's stream-ordered pool: creating and
+// destroying engines (one per branch-and-bound node, several banks at once,
+// bnb.cpp:549-556) must not serialise the device the way cudaMalloc/cudaFree
+// do, and freed blocks stay cached for the next engine.
+void keep_pool_cached(int dev) {
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert(dev).second) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    std::uint64_t keep = ~std::uint64_t{0};
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
+template <class T>
+void salloc(cudaStream_t st, T** p, size_t n) {
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T), st),
+             "cudaMallocAsync");
+}
+template <class T>
+void sfree(cudaStream_t st, T*& p) {
+  if (p) cudaFreeAsync(p, st);
   p = nullptr;
 }
 
@@ -149,6 +177,7 @@ void Engine::alloc() {
   cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream");
+  keep_pool_cached(dev_);
   const int m = m_;
   fpairs_ = m * (m - 1) / 2;
   lpairs_ = m * (m - 1);
@@ -160,26 +189,26 @@ void Engine::alloc() {
   ntriples_ = m * (m - 1) * (m - 2) / 6;
   chunk_ = fold_chunk(m);
   nchunks_ = (m + chunk_ - 1) / chunk_;
-  dalloc(&b_, nb_);
-  dalloc(&c_, nc_);
-  dalloc(&d_, nd_);
-  dalloc(&piz_, nd_);
-  if (is_fast()) dalloc(&incz_, nd_);
-  dalloc(&piy_, nc_);
-  dalloc(&pix_, nb_);
-  dalloc(&theta_, tiles_);
-  if (is_two_phase()) dalloc(&theta1_, tiles_);
-  dalloc(&delta_, nb_);
-  dalloc(&ybar_, tiles_);
-  dalloc(&dx_, nb_);
-  dalloc(&push_, tiles_);
-  dalloc(&sa_fac_, m);
-  dalloc(&sa_loc_, m);
-  dalloc(&xrow_, m);
-  dalloc(&xcol_, m);
-  dalloc(&cert_, m);
-  dalloc(&triples_, 3 * (size_t)ntriples_);
-  dalloc(&fpair_ij_, fpairs_);
+  salloc(st_, &b_, nb_);
+  salloc(st_, &c_, nc_);
+  salloc(st_, &d_, nd_);
+  salloc(st_, &piz_, nd_);
+  if (is_fast()) salloc(st_, &incz_, nd_);
+  salloc(st_, &piy_, nc_);
+  salloc(st_, &pix_, nb_);
+  salloc(st_, &theta_, tiles_);
+  if (is_two_phase()) salloc(st_, &theta1_, tiles_);
+  salloc(st_, &delta_, nb_);
+  salloc(st_, &ybar_, tiles_);
+  salloc(st_, &dx_, nb_);
+  salloc(st_, &push_, tiles_);
+  salloc(st_, &sa_fac_, m);
+  salloc(st_, &sa_loc_, m);
+  salloc(st_, &xrow_, m);
+  salloc(st_, &xcol_, m);
+  salloc(st_, &cert_, m);
+  salloc(st_, &triples_, 3 * (size_t)ntriples_);
+  salloc(st_, &fpair_ij_, fpairs_);
   plan_pipeline();
   split_mode_ = env_int("QAPB_X3SPLIT", 2);
   // sharded engines split only their local X3 members, in hybrid mode
@@ -194,11 +223,11 @@ void Engine::alloc() {
     const int nch = (range + chunk_ - 1) / chunk_;
     x3_group_ = std::max(1, env_int("QAPB_X3_GROUP", 4) / chunk_) * chunk_;
     x3_ngroups_ = (range + x3_group_ - 1) / x3_group_;
-    dalloc(&x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
-    dalloc(&d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
+    salloc(st_, &x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
+    salloc(st_, &d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
   }
-  dalloc(&counter_, stage_ev_.size() + 2);
-  dalloc(&S_, 1);
+  salloc(st_, &counter_, stage_ev_.size() + 2);
+  salloc(st_, &S_, 1);
   cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hSpin_), sizeof(DevScalars)),
              "cudaMallocHost");
   std::vector<int> tr;
@@ -213,6 +242,7 @@ void Engine::alloc() {
   std::vector<int> fp(fpairs_);
   for (int i = 0; i < m; ++i)
     for (int j = i + 1; j < m; ++j) fp[i * m - i * (i + 1) / 2 + (j - i - 1)] = i | (j << 16);
+  cuda_check(cudaStreamSynchronize(st_), "stream-ordered allocations");
   cuda_check(cudaMemcpy(triples_, tr.data(), tr.size() * sizeof(int), cudaMemcpyHostToDevice),
              "H2D triples");
   cuda_check(cudaMemcpy(fpair_ij_, fp.data(), fp.size() * sizeof(int), cudaMemcpyHostToDevice),
@@ -252,10 +282,12 @@ Engine::~Engine() {
     cudaEventDestroy(pe.b);
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
-  dfree(b_); dfree(c_); dfree(d_); dfree(piz_); dfree(incz_); dfree(piy_); dfree(pix_);
-  dfree(theta_); dfree(theta1_); dfree(delta_); dfree(ybar_); dfree(dx_); dfree(push_);
-  dfree(sa_fac_); dfree(sa_loc_); dfree(xrow_); dfree(xcol_); dfree(cert_); dfree(triples_);
-  dfree(fpair_ij_); dfree(counter_); dfree(x3buf_); dfree(d3_); dfree(S_); dfree(hist_bound_); dfree(hist_best_);
+  for (double** p : {&b_, &c_, &d_, &piz_, &incz_, &piy_, &pix_, &theta_, &theta1_, &delta_, &ybar_,
+                     &dx_, &push_, &sa_fac_, &sa_loc_, &x3buf_, &d3_})
+    sfree(st_, *p);
+  for (int** p : {&xrow_, &xcol_, &cert_, &triples_, &fpair_ij_, &counter_}) sfree(st_, *p);
+  sfree(st_, S_);
+  dfree(hist_bound_); dfree(hist_best_);
   if (hSpin_) cudaFreeHost(hSpin_);
   for (void* p : peer_maps_) cudaIpcCloseMemHandle(p);
   if (comm_ && barrier_) {  // no peer may still map my receive buffers

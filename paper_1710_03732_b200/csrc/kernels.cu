@@ -12,6 +12,9 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/qapb200.h"
 #include "common.cuh"
@@ -1069,6 +1072,27 @@ cudaError_t launch_xyfold(const XYFoldParams& p, int tiles, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Raise a kernel's dynamic shared-memory cap to the device maximum once.  The
+// attribute is process-wide per function, and engines of different sizes may
+// launch (or capture) concurrently from several host threads (B&B banks,
+// bnb.cpp:549-556): a per-launch "set to what I need" would race with a
+// smaller setting from another thread.  The cap does not change occupancy.
+template <class K>
+void allow_max_smem(K kern) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert({reinterpret_cast<const void*>(kern), dev}).second) return;
+  int mx = 0;
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kern);  // dynamic + static must fit the opt-in limit
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (mx > 0 ? mx : 227 * 1024) - (int)fa.sharedSizeBytes);
+}
+
 int fold_chunk(int m) {
   // largest pa-chunk whose CTA plan fits ~96 KB (2 CTAs / SM, or two buffers
   // of the persistent fold), at least 1
@@ -1096,8 +1120,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
       nz < 4294967295.0 && p.chunk * (n - 1) * (n - 2) <= kFoldSlots * 256 &&
       p.chunk * n * (n - 1) <= kFoldSlots * 256 && FoldSmem(n, p.chunk).cube < 4096 && n < 64 &&
       p.chunk * (n - 1) < 256 && n * (n - 1) < 16384) {
-    cudaFuncSetAttribute(zfold_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(smem, 48 * 1024));
+    allow_max_smem(zfold_lean_kernel);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zfold_lean_kernel, 256, smem);
     const int slots = std::max(1, per_sm) * num_sms();
@@ -1107,8 +1130,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
     zfold_lean_kernel<<<R * p.nchunks, 256, smem, st>>>(p);
     return cudaGetLastError();
   }
-  cudaFuncSetAttribute(zfold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(smem, 48 * 1024));
+  allow_max_smem(zfold_kernel);
   zfold_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -1116,8 +1138,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
 cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st) {
   if (p.ntriples <= 0) return cudaSuccess;
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
-  cudaFuncSetAttribute(phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(smem, 48 * 1024));
+  allow_max_smem(phase2_kernel);
   phase2_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -1147,8 +1168,7 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const size_t smem = warp_smem * W;
   auto kern = p.sh ? lap_batch_kernel<CPL, 1>
                     : (p.x3buf ? lap_batch_kernel<CPL, 2> : lap_batch_kernel<CPL, 0>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(smem, 48 * 1024));
+  allow_max_smem(kern);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem);
   if (per_sm < 1) per_sm = 1;
@@ -1164,8 +1184,7 @@ cudaError_t launch_ystage_t(const YStageParams& p, cudaStream_t st) {
   const int my = p.m - 1;
   const int W = 4;
   const size_t smem = (size_t)W * ((size_t)my * my + my + 1) * sizeof(double);
-  cudaFuncSetAttribute(ystage_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(smem, 48 * 1024));
+  allow_max_smem(ystage_kernel<CPL>);
   const int blocks = (p.m * p.m + W - 1) / W;
   ystage_kernel<CPL><<<blocks, 32 * W, smem, st>>>(p, W);
   return cudaGetLastError();
@@ -1174,8 +1193,7 @@ cudaError_t launch_ystage_t(const YStageParams& p, cudaStream_t st) {
 template <int CPL>
 cudaError_t launch_xstage_t(const XStageParams& p, cudaStream_t st) {
   const size_t smem = ((size_t)p.m * p.m + p.m + 1) * sizeof(double);
-  cudaFuncSetAttribute(xstage_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(smem, 48 * 1024));
+  allow_max_smem(xstage_kernel<CPL>);
   xstage_kernel<CPL><<<1, 1024, smem, st>>>(p);
   return cudaGetLastError();
 }
