@@ -53,7 +53,7 @@ def _worker(rank, world, port, n, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 12), (2, 30)])
+@pytest.mark.parametrize("world,n", [(2, 12), (2, 30), (4, 13), (8, 30)])
 def test_exchange_counts_match_across_gloo_ranks(world, n):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
