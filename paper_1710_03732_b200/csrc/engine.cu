@@ -372,7 +372,6 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   std::memcpy(&id, nccl_id, sizeof id);
   comm_ = cached_comm(id, world_, rank_, dev_);
   shard_.chunk = chunk_;
-  shard_.fence = env_int("QAPB_FENCE", 0);
   // Receive buffers live here; peers write them directly over NVLink through
   // CUDA IPC mappings (pi from X3 owners, costs from fold owners).
   std::vector<long long> send, recv;

@@ -410,7 +410,6 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   cp_async_wait_all();
   __syncthreads();
   fold_update(P, f, sm, L, blockIdx.x);
-  if (P.shard && P.shard->fence) __threadfence_system();  // peer stores before the barrier
   if (blockIdx.x == 0 && threadIdx.x < f.n) {  // rlt2.cpp:297-298
     P.sa_fac[threadIdx.x] = 0.0;
     P.sa_loc[threadIdx.x] = 0.0;

@@ -83,11 +83,14 @@ constexpr int kMaxRanks = 8;
 //        slot = (T*nch(A) + chunk) * n(B)*(n-1)*chunk_cap
 //               + ((pb - pbound[B])*(n-1) + pci)*chunk_cap + pa_l,
 //        T = lexicographic triple index.
+// A kernel's peer stores are complete when it completes; the NCCL collective
+// that follows it on the engine stream (the barrier after the fold, the theta
+// broadcast after the Z-LAPs) orders them before the peer's next kernel, so
+// no system fences are needed inside the kernels.
 struct ShardInfo {
   int world, rank;
   int pbound[kMaxRanks + 1];
   int chunk;                           // fold chunk capacity (pa values per CTA)
-  int fence;                           // system fence after peer stores (QAPB_FENCE)
   const int* rows_before;              // [fpairs+1], prefix sums of b over pairs (b<c)
   const double* pi_recv[kMaxRanks];    // local: pi of my families' remote X3 cells
   double* cost_send[kMaxRanks];        // PEER: X3 owner's cost buffer for my families
