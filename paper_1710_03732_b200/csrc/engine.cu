@@ -226,6 +226,14 @@ void Engine::alloc() {
     salloc(st_, &x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
     salloc(st_, &d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
   }
+  sa_dev_ = cfg_.sa_enabled && world_ == 1 && m_ <= 128 && env_int("QAPB_HOST_SA", 0) == 0;
+  if (sa_dev_) {
+    salloc(st_, &sa_state_, 1);
+    SaState h;
+    sa_seed(&h, cfg_.seed);
+    cuda_check(cudaMemcpyAsync(sa_state_, &h, sizeof h, cudaMemcpyHostToDevice, st_), "H2D sa");
+    cuda_check(cudaStreamSynchronize(st_), "sa seed");
+  }
   salloc(st_, &counter_, stage_ev_.size() + 2);
   salloc(st_, &S_, 1);
   cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hSpin_), sizeof(DevScalars)),
@@ -287,6 +295,7 @@ Engine::~Engine() {
     sfree(st_, *p);
   for (int** p : {&xrow_, &xcol_, &cert_, &triples_, &fpair_ij_, &counter_}) sfree(st_, *p);
   sfree(st_, S_);
+  sfree(st_, sa_state_);
   dfree(hist_bound_); dfree(hist_best_);
   if (hSpin_) cudaFreeHost(hSpin_);
   for (void* p : peer_maps_) cudaIpcCloseMemHandle(p);
@@ -745,6 +754,18 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   cuda_check(launch_xfinish(xs, st_), "x-finish");
   kend(st_);
   launches_ += 2;
+  if (sa_dev_) {  // rlt2.cpp:521-523 on the device (kernels.cu sa_device_kernel)
+    SaParams sp{};
+    sp.m = m_;
+    sp.cool_period = cfg_.sa_cool_period;
+    sp.fast = is_fast() ? 1 : 0;
+    sp.t0_fraction = cfg_.sa_t0_fraction;
+    sp.kappa_cap = cfg_.sa_kappa_lb_cap;
+    sp.cool_factor = cfg_.sa_cool_factor;
+    sp.upper_bound = cfg_.upper_bound;
+    cuda_check(launch_sa_device(sp, b_, S_, sa_state_, sa_fac_, sa_loc_, st_), "sa step");
+    ++launches_;
+  }
   if (capture) {
     cuda_check(cudaStreamEndCapture(st_, &g), "end capture");
     cuda_check(cudaGraphInstantiate(&graph_, g, 0), "graph instantiate");
@@ -820,7 +841,7 @@ double Engine::iterate() {
   pull_scalars();
   if (profiling_) collect_events();
   check_phase2();
-  if (cfg_.sa_enabled && !hS_.has_cert) sa_perturb();
+  if (cfg_.sa_enabled && !sa_dev_ && !hS_.has_cert) sa_perturb();
   last_rec_ = qapb_record{hS_.iter, hS_.last_bound, gap(), 0, 0, 0};
   const int k = hS_.iter - 1;
   if ((int)stage_ms_.size() >= 3 * (k + 1)) {
@@ -868,12 +889,12 @@ void Engine::run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<i
     int batch = 4;
     while (true) {
       const int remaining = cfg_.iter_limit - hS_.iter;
-      const int B = cfg_.sa_enabled ? 1 : std::max(1, std::min(remaining, batch));
+      const int B = (cfg_.sa_enabled && !sa_dev_) ? 1 : std::max(1, std::min(remaining, batch));
       ensure_hist(hS_.iter + B);
       for (int k = 0; k < B; ++k) enqueue_iteration(hS_.iter + k);
       pull_scalars();
       check_phase2();
-      if (cfg_.sa_enabled && !hS_.has_cert) sa_perturb();
+      if (cfg_.sa_enabled && !sa_dev_ && !hS_.has_cert) sa_perturb();
       if (hS_.stop || hS_.iter >= cfg_.iter_limit) break;
       batch = std::min(batch * 2, 64);
     }

@@ -160,7 +160,9 @@ class Engine {
   int hist_cap_ = 0;
   DevScalars* hSpin_ = nullptr;  // pinned mirror for async copies
   DevScalars hS_{};
-  std::mt19937_64 rng_;
+  std::mt19937_64 rng_;  // host SA (QAPB_HOST_SA=1); the device SA keeps its own state
+  bool sa_dev_ = false;
+  SaState* sa_state_ = nullptr;
   double temp_ = 0;
   qapb_record last_rec_{};
   long long launches_ = 0;

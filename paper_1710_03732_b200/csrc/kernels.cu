@@ -965,6 +965,7 @@ __global__ void xfinish_kernel(XStageParams P) {
     P.hist_bound[it] = S->last_bound;
     P.hist_best[it] = S->best;
     S->iter = it + 1;
+    S->sa_pending = 1;  // the device SA step (if any) follows this iteration
     if (S->run_mode) {
       const double best = S->best;
       int term = -1;
@@ -1051,6 +1052,153 @@ __global__ void sa_apply_kernel(int m, double* b, const double* sa_fac, const do
     b[e] = dsub(b[e], dadd(sa_fac[i], sa_loc[p]));
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && fast) S->running = dsub(S->running, drained);
+}
+
+// ---------------------------------------------------------------------------
+// Device SA step, rlt2.cpp:477-513, one warp.  The draws are those of
+// std::uniform_real_distribution<double>(0,1) over std::mt19937_64 in
+// libstdc++ (generate_canonical: one 64-bit draw, (double)x / 2^64, clamped
+// below 1), so the state advances exactly as the reference's.  The accept
+// test U < exp(-kap/T) uses CUDA's exp (<= 1 ulp): it can differ from glibc's
+// only when U equals one of two adjacent doubles, p ~ 2^-52 per draw.
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+__device__ __forceinline__ unsigned long long mt_mix(unsigned long long a, unsigned long long b,
+                                                      unsigned long long c) {
+  const unsigned long long x = (a & 0xFFFFFFFF80000000ULL) | (b & 0x7FFFFFFFULL);
+  return c ^ (x >> 1) ^ ((x & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+}
+
+// the sequential twist in two parallel halves: [0,156) reads only old words,
+// [156,312) reads new words of the first half (and the new mt[0] at 311)
+__device__ void mt_twist_warp(unsigned long long* mt, int lane) {
+  unsigned long long nv[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int i = lane + 32 * k;
+    if (i < 156) nv[k] = mt_mix(mt[i], mt[i + 1], mt[i + 156]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int i = lane + 32 * k;
+    if (i < 156) mt[i] = nv[k];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int i = 156 + lane + 32 * k;
+    if (i < 312) nv[k] = mt_mix(mt[i], mt[(i + 1) % 312], mt[i - 156]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int i = 156 + lane + 32 * k;
+    if (i < 312) mt[i] = nv[k];
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) sa_device_kernel(SaParams p, double* __restrict__ b,
+                                                       DevScalars* S, SaState* st,
+                                                       double* __restrict__ sa_fac,
+                                                       double* __restrict__ sa_loc) {
+  __shared__ double u[4 * 128];
+  __shared__ double amt[2 * 128];
+  __shared__ unsigned char acc[2 * 128];
+  __shared__ unsigned long long mt[312];
+  __shared__ double tot_s, drained_s;
+  const int lane = threadIdx.x, m = p.m;
+  const int pending = S->sa_pending;
+  __syncwarp();
+  if (!pending) return;  // this iteration's X stage did not run (stopped earlier)
+  if (lane == 0) S->sa_pending = 0;
+  if (S->has_cert) return;  // rlt2.cpp:521-523
+  const double nu = S->best;
+  if (nu <= 0) return;  // rlt2.cpp:479 (no draws consumed)
+  double temp = st->temp;
+  if (temp <= 0) {  // rlt2.cpp:480-484
+    const double ub = isfinite(p.upper_bound) ? p.upper_bound : dadd(dmul(1.05, nu), 1.0);
+    temp = dmul(p.t0_fraction, ub);
+  }
+  const double cap = dmul(p.kappa_cap, nu);  // rlt2.cpp:485
+  for (int i = lane; i < 312; i += 32) mt[i] = st->mt[i];
+  __syncwarp();
+  const int nd = 4 * m;  // two draws per slot, 2m slots (rlt2.cpp:490-497)
+  int idx = st->idx;
+  for (int base = 0; base < nd;) {
+    if (idx >= 312) {
+      mt_twist_warp(mt, lane);
+      idx = 0;
+    }
+    const int take = min(nd - base, 312 - idx);
+    for (int k = lane; k < take; k += 32) {
+      double r = __ull2double_rn(mt_temper(mt[idx + k])) * 0x1p-64;
+      if (r >= 1.0) r = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
+      u[base + k] = r;
+    }
+    __syncwarp();
+    base += take;
+    idx += take;
+  }
+  for (int s = lane; s < 2 * m; s += 32) {
+    const double kap = dmul(u[2 * s], cap);
+    acc[s] = u[2 * s + 1] < exp(ddiv(-kap, temp));
+    amt[s] = kap;
+  }
+  __syncwarp();
+  if (lane == 0) {  // accepted mass in slot order (rlt2.cpp:494-497)
+    double total = 0.0;
+    for (int s = 0; s < 2 * m; ++s)
+      if (acc[s]) total = dadd(total, amt[s]);
+    tot_s = total;
+  }
+  __syncwarp();
+  const double total = tot_s;
+  const double f = total > cap ? ddiv(cap, total) : 1.0;  // rlt2.cpp:498-499
+  for (int s = lane; s < 2 * m; s += 32) {
+    double a = acc[s] ? amt[s] : 0.0;
+    if (total > cap) a = dmul(a, f);
+    amt[s] = a;
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) {  // rlt2.cpp:500-501
+    sa_fac[i] = ddiv(amt[i], (double)m);
+    sa_loc[i] = ddiv(amt[m + i], (double)m);
+  }
+  __syncwarp();
+  if (lane == 0) {  // rlt2.cpp:502-507, drained in i order
+    double drained = 0.0;
+    for (int i = 0; i < m; ++i) drained = dadd(drained, dadd(sa_fac[i], sa_loc[i]));
+    drained_s = drained;
+  }
+  for (int e = lane; e < m * m; e += 32) {
+    const int i = e / m, q = e - i * m;
+    b[e] = dsub(b[e], dadd(sa_fac[i], sa_loc[q]));
+  }
+  for (int i = lane; i < 312; i += 32) st->mt[i] = mt[i];
+  __syncwarp();
+  if (lane == 0) {
+    if (p.fast) S->running = dsub(S->running, drained_s);  // rlt2.cpp:508-511
+    if (p.cool_period > 0 && S->iter % p.cool_period == 0)  // (iter_+1) % period
+      temp = dmul(temp, p.cool_factor);
+    st->temp = temp;
+    st->idx = idx;
+  }
+}
+
+void sa_seed(SaState* h, unsigned long long seed) {
+  h->temp = 0.0;
+  h->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    h->mt[i] = 6364136223846793005ULL * (h->mt[i - 1] ^ (h->mt[i - 1] >> 62)) + (unsigned long long)i;
+  h->idx = 312;
 }
 
 // ===========================================================================
@@ -1238,6 +1386,13 @@ cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, in
   const size_t total = (size_t)ntriples * nchunks * n * (n - 1) * chunk;
   x3_sync_kernel<<<4 * num_sms(), 256, 0, st>>>(n, chunk, nchunks, triples, p_lo, p_hi, d, d3,
                                                 total, to_d3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,
+                             double* sa_fac, double* sa_loc, cudaStream_t stream) {
+  if (p.m > 128) return cudaErrorInvalidValue;
+  sa_device_kernel<<<1, 32, 0, stream>>>(p, b, S, st, sa_fac, sa_loc);
   return cudaGetLastError();
 }
 

@@ -21,8 +21,21 @@ struct DevScalars {
   int run_mode;       // 1 inside run(): evaluate termination on device
   int run_start;      // iter at run() entry (best_hist origin)
   int err_tile;       // phase-2 theta regression: smallest tile, INT_MAX = none
-  int pad;
+  int sa_pending;     // set by the X stage's finish kernel, consumed by the device SA step
 };
+
+// Device SA (rlt2.cpp:477-513): std::mt19937_64 state and the temperature
+struct SaState {
+  double temp;
+  int idx, pad;
+  unsigned long long mt[312];
+};
+struct SaParams {
+  int m, cool_period, fast;
+  double t0_fraction, kappa_cap, cool_factor, upper_bound;
+};
+// mt19937_64 seeding (std::mersenne_twister_engine::seed)
+void sa_seed(SaState* host_state, unsigned long long seed);
 
 struct ShardInfo;
 
@@ -202,6 +215,10 @@ cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
 // single-GPU X3 split: D' of the X3 members, tile layout <-> fold order
 cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
                            int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st);
+// one SA step on the device after an iteration (no-op unless that iteration's
+// X stage ran, when a certificate exists, or when best <= 0)
+cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,
+                             double* sa_fac, double* sa_loc, cudaStream_t st_);
 cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
                               cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
