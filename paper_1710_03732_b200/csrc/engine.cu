@@ -146,8 +146,8 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
   if (world_ < 1 || world_ > kMaxRanks || rank_ < 0 || rank_ >= world_)
     throw std::invalid_argument("AscentEngine: bad rank/world");
-  if (world_ > 1 && (is_two_phase() || cfg.sa_enabled))
-    throw std::invalid_argument("sharded engine: F1/S1 without SA only (round 1)");
+  if (world_ > 1 && (is_two_phase() || (cfg.sa_enabled && env_int("QAPB_HOST_SA", 0))))
+    throw std::invalid_argument("sharded engine: F1/S1 (SA on the device) only (round 1)");
   if (world_ > n) throw std::invalid_argument("sharded engine: more ranks than locations");
   alloc();
   setup_shards(nccl_id);
@@ -212,7 +212,7 @@ void Engine::alloc() {
   plan_pipeline();
   split_mode_ = env_int("QAPB_X3SPLIT", 2);
   // sharded engines split only their local X3 members, in hybrid mode
-  split_ = !is_two_phase() && !cfg_.sa_enabled &&
+  split_ = !is_two_phase() &&
            (world_ == 1 ? split_mode_ != 0 : split_mode_ == 2);
   if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
     int range = m;
@@ -226,7 +226,9 @@ void Engine::alloc() {
     salloc(st_, &x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
     salloc(st_, &d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
   }
-  sa_dev_ = cfg_.sa_enabled && world_ == 1 && m_ <= 128 && env_int("QAPB_HOST_SA", 0) == 0;
+  // every rank of a sharded engine holds the same b, best and RNG stream, so
+  // each runs the same SA step and the replicated state stays identical
+  sa_dev_ = cfg_.sa_enabled && m_ <= 128 && env_int("QAPB_HOST_SA", 0) == 0;
   if (sa_dev_) {
     salloc(st_, &sa_state_, 1);
     SaState h;

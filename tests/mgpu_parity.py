@@ -29,7 +29,8 @@ def main():
     with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
         g = json.load(fh)
     nug12 = QapInstance(12, np.array(g["nug12"]["flow"], float), np.array(g["nug12"]["dist"], float))
-    cases = {"nug12_F1": nug12, "nug12_S1": nug12, "rand20_F1": q.generate_instance(20, 1, 99),
+    cases = {"nug12_F1": nug12, "nug12_S1": nug12, "nug12_F1_SA": nug12, "nug12_S1_SA": nug12,
+             "rand20_F1": q.generate_instance(20, 1, 99),
              "rand20_S1": q.generate_instance(20, 1, 99), "grid20_F1": grid_instance(4, 5),
              "grid30_F1": grid_instance(5, 6)}
     results = {}
@@ -37,7 +38,8 @@ def main():
         tr = g["traces"][key]
         idobj = [q.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(idobj, src=0)
-        cfg = q.AscentConfig(variant=tr["variant"], iter_limit=tr["iters"], device=local)
+        cfg = q.AscentConfig(variant=tr["variant"], iter_limit=tr["iters"], device=local,
+                             sa_enabled=tr["sa"], upper_bound=tr["upper_bound"], seed=tr["seed"])
         eng = q.AscentEngine.from_instance_sharded(inst, cfg, rank, world, idobj[0])
         want = [float.fromhex(x) for x in tr["bounds"]]
         got = [eng.iterate() for _ in want]
