@@ -293,10 +293,15 @@ def run_ours(args):
                              "alg_bytes": kb[name], "achieved_gbs": gbs}
     dom = max(kernels, key=lambda k: kernels[k]["ms_per_launch"] * kernels[k]["launches"])
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    tdb = {}
+    tdb, idb = {}, {}
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            tdb = _json.load(fh).get(f"n{args.n}_{args.variant}", {})
+            nj = _json.load(fh)
+        tdb = nj.get(f"n{args.n}_{args.variant}", {})
+        idb = nj.get(f"n{args.n}_{args.variant}_issue_active_pct", {})
+    for name in kernels:  # ncu evidence (profiles/): DRAM bytes and issue-slot use per launch
+        kernels[name]["ncu_dram_bytes"] = tdb.get(name)
+        kernels[name]["ncu_issue_active_pct"] = idb.get(name)
 
     def kernel_roofline(name):
         return {"bound": "hbm", "kernel": name, "achieved": kernels[name]["achieved_gbs"],
