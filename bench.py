@@ -310,9 +310,11 @@ def run_ours(args):
                 "alg_bytes_per_launch": kb[name]}
     roofline = kernel_roofline(dom)
     if dom == "zlap":
-        roofline["note"] = ("the Z-LAP batch is issue-bound (warp-per-LAP Hungarian, ~75% issue "
-                            "slots busy in ncu), not HBM-bound; its HBM fraction is reported as "
-                            "the contract asks; the HBM-bound fold is in roofline_fold")
+        roofline["note"] = ("the Z-LAP batch is issue-bound (warp-per-LAP Hungarian, "
+                            f"{idb.get('zlap', 80):.0f}% of issue slots busy in ncu), not "
+                            "HBM-bound; its HBM fraction is reported as the contract asks; the "
+                            "HBM-bound fold is in roofline_fold")
+        roofline["issue_active_pct"] = idb.get("zlap")
     if "zfold" in kernels and dom != "zfold":
         roofline["roofline_fold"] = kernel_roofline("zfold")
     ib = iteration_bytes(args.n)
