@@ -283,6 +283,8 @@ def run_ours(args):
     its = (1 if sharded else world) * args.steps / (ms / 1000.0)
     peak, peak_src = peaks()
     kb = kernel_bytes(args.n, args.variant)
+    if sharded:  # each rank folds and solves 1/W of the z work (its location range)
+        kb = {k: (v / world if k in ("zfold", "zlap") else v) for k, v in kb.items()}
     kernels = {}
     for name, (kms, cnt) in ktimes.items():
         if cnt:
@@ -328,19 +330,22 @@ def run_ours(args):
     # host report out), 100 iterations = the reference's default iter_limit
     e2e_iters = 100
     if sharded:  # every rank runs its shard of the same run_ascent-equivalent call
-        # (same NCCL id as the timed engine: the library caches its communicator)
-        torch.distributed.barrier()
-        t0 = time.perf_counter()
-        e = q.AscentEngine.from_instance_sharded(
-            inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters, device=local), rank,
-            world, idobj[0])
-        rep = e.run()
-        e.close()
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+        # (same NCCL id as the timed engine: the library caches its communicator);
+        # best of 3 whole calls, each timed as the max over ranks
+        runs = []
+        for _ in range(3):
+            torch.distributed.barrier()
+            t0 = time.perf_counter()
+            e = q.AscentEngine.from_instance_sharded(
+                inst, q.AscentConfig(variant=args.variant, iter_limit=e2e_iters, device=local),
+                rank, world, idobj[0])
+            rep = e.run()
+            e.close()
+            torch.cuda.synchronize()
+            tt = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            runs.append(float(tt.item()))
+        e2e_s = min(runs)
     else:
         q.run_ascent(inst, q.AscentConfig(variant=args.variant, iter_limit=2))  # warm context
         runs = []
@@ -358,8 +363,7 @@ def run_ours(args):
                     "qapb_run_ascent") + f"(nug{args.n}-shaped, {args.variant}, iter_limit=100): "
                    "engine build on device, 100 iterations, report + records to host",
            "seconds": e2e_s, "final_bound": rep.best_bound}
-    if not sharded:
-        e2e["all_seconds"] = runs
+    e2e["all_seconds"] = runs
 
     if rank != 0:
         torch.distributed.destroy_process_group()
