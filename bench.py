@@ -299,8 +299,9 @@ def run_ours(args):
     if os.path.exists(tpath):
         with open(tpath) as fh:
             nj = _json.load(fh)
-        tdb = nj.get(f"n{args.n}_{args.variant}", {})
-        idb = nj.get(f"n{args.n}_{args.variant}_issue_active_pct", {})
+        if not sharded:  # the committed capture is of the single-GPU engine
+            tdb = nj.get(f"n{args.n}_{args.variant}", {})
+            idb = nj.get(f"n{args.n}_{args.variant}_issue_active_pct", {})
     for name in kernels:  # ncu evidence (profiles/): DRAM bytes and issue-slot use per launch
         kernels[name]["ncu_dram_bytes"] = tdb.get(name)
         kernels[name]["ncu_issue_active_pct"] = idb.get(name)
