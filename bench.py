@@ -404,7 +404,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=30)  # --size under torchrun
     ap.add_argument("--variant", default="F1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",

@@ -166,15 +166,24 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
   if constexpr (CPL == 1) {
     return warp_lap_solve_1(cost, m, lane, L);
   }
+  // Same scheme as warp_lap_solve_1 with CPL columns per lane: used and
+  // padding columns carry minv = NaN, rows travel as byte offsets, the dual
+  // update adds `used ? delta : +0.0` unconditionally.
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const double QNAN = __longlong_as_double(0x7ff8000000000000ll);
   double minv[CPL];
   int way[CPL];
+  const char* colp[CPL];
+  double minv0[CPL];
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
+    const int j = s * 32 + lane;
     L.p[s] = -1;
     L.w[s] = 0.0;
     L.v[s] = 0.0;
     way[s] = 0;
+    colp[s] = reinterpret_cast<const char*>(cost + (j < m ? j : m - 1));
+    minv0[s] = j < m ? INF : QNAN;
   }
   const int vs = m >> 5, vl = m & 31;  // owner of the virtual column m
   bool ok = true;  // finite costs bound every row to m+1 steps (see warp_lap_solve_1)
@@ -183,68 +192,57 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
 #pragma unroll
     for (int s = 0; s < CPL; ++s) {
       L.p[s] = (s * 32 + lane < m) ? s * 32 + lane : -1;
-      L.w[s] = L.v[s] = __longlong_as_double(0x7ff8000000000000ll);
+      L.w[s] = L.v[s] = QNAN;
     }
     return L.w[0];
   }
-  for (int i = 0; i < m; ++i) {  // lap.cpp:33
+  const int m8 = m * 8;
+  int row8 = 0;
+  for (int i = 0; i < m; ++i, row8 += m8) {  // lap.cpp:33
 #pragma unroll
     for (int s = 0; s < CPL; ++s) {
-      minv[s] = INF;
+      minv[s] = minv0[s];
       if (s == vs && lane == vl) {  // p[m] = i; u[i] is still 0
-        L.p[s] = i;
+        L.p[s] = row8;
         L.w[s] = 0.0;
       }
     }
-    unsigned used = 0;
-    int j0 = m, i0 = i;
+    int j0 = m, i0 = row8;
     double ui0 = 0.0;
     while (true) {  // Dijkstra step, lap.cpp:40-67
-      if ((j0 & 31) == lane) used |= 1u << (j0 >> 5);
-      const double* row = cost + (size_t)i0 * m;
-      unsigned long long bkey = ~0ull;
+      unsigned bhi = 0xffffffffu, blo = 0xffffffffu;
       int bcol = 0x7fffffff;
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {  // branch-free relaxation of this lane's columns
+      for (int s = 0; s < CPL; ++s) {
         const int j = s * 32 + lane;
-        const double cv = row[j < m ? j : m - 1];
-        const bool act = (j < m) && !((used >> s) & 1u);
+        if (j == j0) minv[s] = QNAN;  // column j0 joins the tree
+        const double cv = *reinterpret_cast<const double*>(colp[s] + i0);
         const double cur = dsub(dsub(cv, ui0), L.v[s]);  // lap.cpp:48
-        const bool upd = act && (cur < minv[s]);           // lap.cpp:49-52
-        minv[s] = upd ? cur : minv[s];
-        way[s] = upd ? j0 : way[s];
-        const unsigned long long k = act ? ordkey(minv[s]) : ~0ull;
-        if (CPL == 1) {
-          bkey = k;
-          bcol = act ? j : 0x7fffffff;
-        } else if (k < bkey) {
-          bkey = k;
+        if (cur < minv[s]) {                             // lap.cpp:49-52 (false when used)
+          minv[s] = cur;
+          way[s] = j0;
+        }
+        unsigned hi, lo;
+        ordkey2(minv[s], hi, lo);
+        if (hi < bhi || (hi == bhi && lo < blo)) {  // lowest column of this lane on ties
+          bhi = hi;
+          blo = lo;
           bcol = j;
         }
       }
       // argmin over unused columns, lowest column on ties (lap.cpp:53-56)
-      const unsigned hi = (unsigned)(bkey >> 32), lo = (unsigned)bkey;
-      const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
-      const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
-      const bool cand = (hi == hmin) && (lo == lmin) && (bcol != 0x7fffffff);
-      int j1;
-      if (CPL == 1) {
-        j1 = __ffs(__ballot_sync(QAPB_FULL, cand)) - 1;
-      } else {
-        j1 = (int)__reduce_min_sync(QAPB_FULL, cand ? (unsigned)bcol : 0xffffffffu);
-      }
+      const unsigned hmin = __reduce_min_sync(QAPB_FULL, bhi);
+      const unsigned lmin = __reduce_min_sync(QAPB_FULL, bhi == hmin ? blo : 0xffffffffu);
+      const bool cand = (bhi == hmin) && (blo == lmin);
+      const int j1 = (int)__reduce_min_sync(QAPB_FULL, cand ? (unsigned)bcol : 0xffffffffu);
       const int s1 = j1 >> 5, l1 = j1 & 31;
       const double delta = __shfl_sync(QAPB_FULL, pick<CPL>(minv, s1), l1);
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {  // dual update, lap.cpp:58-65
-        const int j = s * 32 + lane;
-        const bool us = ((used >> s) & 1u) != 0;
-        const bool inr = j <= m;
-        const double wn = dadd(L.w[s], delta), vn = dsub(L.v[s], delta);
-        const double mn = dsub(minv[s], delta);
-        L.w[s] = (inr && us) ? wn : L.w[s];
-        L.v[s] = (inr && us) ? vn : L.v[s];
-        minv[s] = (inr && !us) ? mn : minv[s];
+      for (int s = 0; s < CPL; ++s) {  // dual update, lap.cpp:58-65 (see warp_lap_solve_1)
+        const double du = isnan(minv[s]) ? delta : 0.0;
+        minv[s] = dsub(minv[s], delta);
+        L.w[s] = dadd(L.w[s], du);
+        L.v[s] = dsub(L.v[s], du);
       }
       j0 = j1;
       const int pj = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, s1), l1);
@@ -270,11 +268,12 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
       j0 = jw;
     }
   }
-  // value = sum_j cost[p[j]][j], accumulated in column order (lap.cpp:75-80)
+  // back to row indices; value = sum_j cost[p[j]][j] in column order (lap.cpp:75-80)
   double term[CPL];
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
     const int j = s * 32 + lane;
+    L.p[s] = L.p[s] < 0 ? -1 : L.p[s] / m8;
     term[s] = (j < m) ? cost[(size_t)L.p[s] * m + j] : 0.0;
   }
   double value = 0.0;
