@@ -124,7 +124,37 @@ struct FamilyCtx {
   double* d3;
   int x3mode;
   int tglob, po0, G, ng;  // global triple, pa0 - p_lo, x3buf group and groups
+  const struct ShardLocal* sl;  // shared-memory copy of the shard tables (null on one GPU)
+  int rb;                        // rows_before[fbc] (sharded)
 };
+
+// The shard tables a fold CTA reads per X3 cell, staged once into shared
+// memory (reading them through the ShardInfo pointer cost an L1 request per
+// cell and pass)
+struct ShardLocal {
+  int world, rank;
+  int pbound[kMaxRanks + 1];
+  int owner[130];  // n <= lap_max_m() + 2
+  const double* pi_recv[kMaxRanks];
+  double* d3[kMaxRanks];
+  double* cost_send[kMaxRanks];
+};
+
+__device__ __forceinline__ void shard_local_load(const ShardInfo* sh, int n, ShardLocal* sl) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sl->world = sh->world;
+    sl->rank = sh->rank;
+  }
+  if (tid <= sh->world) sl->pbound[tid] = sh->pbound[tid];
+  if (tid < sh->world) {
+    sl->pi_recv[tid] = sh->pi_recv[tid];
+    sl->d3[tid] = sh->d3[tid];
+    sl->cost_send[tid] = sh->cost_send[tid];
+  }
+  for (int p = tid; p < n; p += blockDim.x) sl->owner[p] = shard_owner(*sh, p);
+  __syncthreads();
+}
 
 // fold-order slot of X3 cell (pa_l, pb, pc) of the CTA's unit in d3 (X3 split)
 __device__ __forceinline__ size_t x3_slot(const FamilyCtx& f, int pa_l, int pb, int pc) {
@@ -139,7 +169,8 @@ __device__ __forceinline__ size_t x3_pi_slot(const FamilyCtx& f, int pa_l, int p
 }
 
 // unit = triple * nchunks + chunk (one CTA's work item)
-__device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
+__device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit,
+                                                 const ShardLocal* sl = nullptr) {
   FamilyCtx f;
   f.n = P.m;
   f.nm1 = f.n - 1;
@@ -168,6 +199,8 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
   f.po0 = f.pa0 - p_lo;
   f.G = P.x3_group;
   f.ng = P.x3_ngroups;
+  f.sl = sl;
+  f.rb = (f.sh && sl) ? f.sh->rows_before[f.fbc] : 0;
   return f;
 }
 
@@ -175,10 +208,20 @@ __device__ __forceinline__ FamilyCtx family_ctx(const FoldParams& P, int unit) {
 // shared with X3 owner xr (A's fold order, ShardInfo in kernels.h)
 __device__ __forceinline__ size_t shard_slot(const FamilyCtx& f, int xr, int pa_l, int pb,
                                              int pc) {
-  const ShardInfo& sh = *f.sh;
-  const int nB = sh.pbound[xr + 1] - sh.pbound[xr];
-  return ((size_t)f.unit * nB * f.nm1 + (size_t)(pb - sh.pbound[xr]) * f.nm1 + pc - (pc > pb)) *
-             f.C + pa_l;
+  const int* pbd = f.sl->pbound;
+  const int nB = pbd[xr + 1] - pbd[xr];
+  return ((size_t)f.unit * nB * f.nm1 + (size_t)(pb - pbd[xr]) * f.nm1 + pc - (pc > pb)) * f.C +
+         pa_l;
+}
+
+// x3_xindex from the shared-memory tables (X3 owner xb, this rank folds)
+__device__ __forceinline__ size_t x3_xindex_l(const FamilyCtx& f, int pb, int pc, int pa, int xb) {
+  const int* pbd = f.sl->pbound;
+  const int nm1 = f.nm1, xa = f.sl->rank;
+  const size_t rlB = (size_t)(pbd[xb + 1] - pbd[xb]) * nm1;
+  const int lp_local = pb * nm1 + pc - (pc > pb) - pbd[xb] * nm1;
+  const int nA = pbd[xa + 1] - pbd[xa];
+  return ((rlB * f.rb + (size_t)lp_local * f.b + f.a) * nA) + (pa - pbd[xa]);
 }
 
 // exchange-buffer index of X3 cell (row a, location pa) of tile (b,c,pb,pc),
@@ -253,8 +296,8 @@ __device__ __forceinline__ void for_family_cells(const FamilyCtx& f, int chunk, 
       // X3 lives with owner(pb): another rank (xr >= 0, this rank owns the
       // cell's D' and receives pi), or here -- in the split buffers (-2) or
       // in the tile layout (-1)
-      const int xb = f.sh ? shard_owner(*f.sh, pb) : -1;
-      if (f.sh && xb != f.sh->rank)
+      const int xb = f.sl ? f.sl->owner[pb] : -1;
+      if (f.sl && xb != f.sl->rank)
         fn(2, pa_l, pb, pc, g, base3 + e, xb);
       else
         fn(2, pa_l, pb, pc, g, base3 + e, f.x3buf ? -2 : -1);
@@ -310,9 +353,8 @@ __device__ __forceinline__ void stage_family(const FamilyCtx& f, int chunk,
       return;
     }
     if (xr >= 0) {  // remote X3: its owner's Z-LAP stored pi; its D' lives here
-      cp_async8(sp, f.sh->pi_recv[xr] + x3_xindex(*f.sh, f.n, f.fbc, f.b, pb, pc, f.a,
-                                                   f.pa0 + pa_l, xr, f.sh->rank));
-      cp_async8(V + slot, f.sh->d3[xr] + shard_slot(f, xr, pa_l, pb, pc));
+      cp_async8(sp, f.sl->pi_recv[xr] + x3_xindex_l(f, pb, pc, f.pa0 + pa_l, xr));
+      cp_async8(V + slot, f.sl->d3[xr] + shard_slot(f, xr, pa_l, pb, pc));
       return;
     }
     cp_async8(sp, piz + g);
@@ -392,8 +434,8 @@ __device__ __forceinline__ void fold_update(const FoldParams& P, const FamilyCtx
       // remote X3: D' stays here in fold order; its owner's next Z-LAP takes
       // the cost from its buffer (NVLink store, contiguous per CTA)
       const size_t gi = shard_slot(f, xr, pa_l, pb, pc);
-      f.sh->d3[xr][gi] = dn;
-      f.sh->cost_send[xr][gi] = inc;
+      f.sl->d3[xr][gi] = dn;
+      f.sl->cost_send[xr][gi] = inc;
       return;
     }
     d[g] = dn;
@@ -404,7 +446,9 @@ __device__ __forceinline__ void fold_update(const FoldParams& P, const FamilyCtx
 __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
-  const FamilyCtx f = family_ctx(P, blockIdx.x);
+  __shared__ ShardLocal sl;
+  if (P.shard) shard_local_load(P.shard, P.m, &sl);
+  const FamilyCtx f = family_ctx(P, blockIdx.x, P.shard ? &sl : nullptr);
   const FoldSmem L(f.n, P.chunk);
   fold_stage(P, f, sm, L);
   cp_async_wait_all();
