@@ -753,6 +753,15 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // sharded: the shard tables are read per tile and lane; keep a copy in
+  // shared memory instead of going through the ShardInfo pointer
+  __shared__ ShardInfo shs;
+  if constexpr (MODE == 1) {
+    const int words = (int)(sizeof(ShardInfo) / sizeof(int));
+    for (int w = threadIdx.x; w < words; w += blockDim.x)
+      reinterpret_cast<int*>(&shs)[w] = reinterpret_cast<const int*>(P.sh)[w];
+    __syncthreads();
+  }
   unsigned char* ws = smem_raw + (size_t)warp * warp_smem;
   double* buf0 = reinterpret_cast<double*>(ws);
   double* buf1 = buf0 + buf_elems;
@@ -806,7 +815,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
     if constexpr (MODE != 0) {
       const int n = m + 2;
       if constexpr (MODE == 1)
-        x3_lanes<CPL>(P, *P.sh, P.fpair_ij, n, tg, lane, X, xb, tb);
+        x3_lanes<CPL>(P, shs, P.fpair_ij, n, tg, lane, X, xb, tb);
       else
         x3_split_lanes<CPL>(P, n, P.tile_base + tg, lane, X, xb, tb);
       if (P.patch) {  // remote-folded / split cells: the fold stored their new cost
