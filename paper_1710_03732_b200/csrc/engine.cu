@@ -383,6 +383,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   std::memcpy(&id, nccl_id, sizeof id);
   comm_ = cached_comm(id, world_, rank_, dev_);
   shard_.chunk = chunk_;
+  cost_scatter_ = env_int("QAPB_COST_SCATTER", 0) != 0;
   // Receive buffers live here; peers write them directly over NVLink through
   // CUDA IPC mappings (pi from X3 owners, costs from fold owners).
   std::vector<long long> send, recv;
@@ -472,6 +473,12 @@ void Engine::enqueue_sharded_z(int it) {
     barrier();  // costs have landed in every X3 owner's buffer
     kend(st_);
     ++launches_;
+    if (cost_scatter_) {  // into the tile layout the Z-LAPs load (else they patch per row)
+      kbegin(QAPB_K_XCHG, st_);
+      cuda_check(launch_x3_cost_scatter(m_, shard_, triples_, costs, st_), "x3 cost scatter");
+      kend(st_);
+      ++launches_;
+    }
   }
   {  // Z-LAPs of my runs: one run of rl tiles per facility-pair block
     const int rl = (p_hi_ - p_lo_) * (m_ - 1);
@@ -490,7 +497,7 @@ void Engine::enqueue_sharded_z(int it) {
     p.run_off = p_lo_ * (m_ - 1);
     p.sh = shard_dev_;
     p.fpair_ij = fpair_ij_;
-    p.patch = it > 0 ? 1 : 0;
+    p.patch = (it > 0 && !cost_scatter_) ? 1 : 0;
     if (split_) {  // local X3 members: slack into the fold-order split buffer
       p.x3buf = x3buf_;
       p.x3_group = x3_group_;

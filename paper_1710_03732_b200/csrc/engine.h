@@ -125,6 +125,7 @@ class Engine {
   void split_scatter() const;
   bool split_ = false;
   int split_mode_ = 0;
+  bool cost_scatter_ = false;  // sharded: scatter remote X3 costs before the Z-LAPs
   int x3_group_ = 0, x3_ngroups_ = 0;
   mutable bool d_stale_ = false;
   double* x3buf_ = nullptr;

@@ -1074,6 +1074,41 @@ __global__ void x3_sync_kernel(int n, int C, int nch, const int* __restrict__ tr
   }
 }
 
+// Sharded: write the costs the fold owners stored for this rank's
+// remote-folded X3 cells (cost_recv, their fold order) into the tile-layout
+// cost array the Z-LAPs load, as one scatter pass instead of per-row patch
+// loads inside the issue-bound LAP kernel.  Thread per slot of peer A.
+__global__ void x3_cost_scatter_kernel(int n, ShardInfo sh, const int* __restrict__ triples,
+                                       double* __restrict__ costs) {
+  const int nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
+  const size_t esz = (size_t)nm2 * nm2;
+  const int me = sh.rank, p_lo = sh.pbound[me], nB = sh.pbound[me + 1] - p_lo;
+  const int C = sh.chunk;
+  const DIdx ix(n);
+  for (int A = 0; A < sh.world; ++A) {
+    if (A == me) continue;
+    const int a_lo = sh.pbound[A], nA = sh.pbound[A + 1] - a_lo, nch = shard_chunks(sh, A);
+    const size_t per_unit = (size_t)nB * nm1 * C;
+    const size_t total = (size_t)n * (n - 1) * (n - 2) / 6 * nch * per_unit;
+    const double* __restrict__ src = sh.cost_recv[A];
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+         i += (size_t)gridDim.x * blockDim.x) {
+      const size_t u = i / per_unit;
+      const int r = (int)(i - u * per_unit);
+      const int lpl = r / C, pa_l = r - lpl * C;
+      const int T = (int)(u / nch), ch = (int)(u - (size_t)T * nch);
+      const int po = ch * C + pa_l;
+      const int pb = p_lo + lpl / nm1, pci = lpl - (pb - p_lo) * nm1, pc = pci + (pci >= pb);
+      const int pa = a_lo + po;
+      if (po >= nA || pa == pc) continue;
+      const int a = triples[3 * T], b = triples[3 * T + 1], c = triples[3 * T + 2];
+      const int lo = min(pb, pc), hi = max(pb, pc), col = pa - (pa > lo) - (pa > hi);
+      costs[((size_t)ix.fpair(b, c) * lpairs + pb * nm1 + pci) * esz + (size_t)a * nm2 + col] =
+          src[i];
+    }
+  }
+}
+
 // theta of every rank's tile runs <-> one buffer of rank segments
 __global__ void theta_xfer_kernel(int m, double* theta, double* buf, ShardInfo sh, int pack) {
   const int nm1 = m - 1, lpairs = m * nm1, fpairs = m * nm1 / 2;
@@ -1446,6 +1481,12 @@ cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaStat
                              double* sa_fac, double* sa_loc, cudaStream_t stream) {
   if (p.m > 128) return cudaErrorInvalidValue;
   sa_device_kernel<<<1, 32, 0, stream>>>(p, b, S, st, sa_fac, sa_loc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_x3_cost_scatter(int n, const ShardInfo& sh, const int* triples, double* costs,
+                                   cudaStream_t st) {
+  x3_cost_scatter_kernel<<<4 * num_sms(), 256, 0, st>>>(n, sh, triples, costs);
   return cudaGetLastError();
 }
 

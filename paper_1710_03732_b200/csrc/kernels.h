@@ -219,6 +219,9 @@ cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, in
 // X stage ran, when a certificate exists, or when best <= 0)
 cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,
                              double* sa_fac, double* sa_loc, cudaStream_t st_);
+// sharded: remote-folded X3 costs (cost_recv) -> the tile-layout cost array
+cudaError_t launch_x3_cost_scatter(int n, const ShardInfo& sh, const int* triples, double* costs,
+                                   cudaStream_t st);
 cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
                               cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,
