@@ -472,14 +472,24 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
 // (TPC=0) lose the inter-CTA stage/update overlap: 3.25 vs 2.60 ms at n=30.
 constexpr int kFoldSlots = 7;  // cells per thread per member group (<= 7 * 256)
 
+template <bool SH>
 __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
+  // sharded: X3 members of tiles owned elsewhere go through the peer buffers
+  // (ShardInfo, kernels.h); the tables are read from shared memory
+  __shared__ ShardLocal sl;
+  int p_lo = 0, p_hi = P.m;
+  if constexpr (SH) {
+    shard_local_load(P.shard, P.m, &sl);
+    p_lo = sl.pbound[sl.rank];
+    p_hi = sl.pbound[sl.rank + 1];
+  }
   const int n = P.m, nm1 = n - 1, nm2 = n - 2, np = n + 1, C = P.chunk;
   const int lpairs = n * nm1;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
   const int nch = P.nchunks, ch = blockIdx.x % nch, r0 = blockIdx.x / nch, R = gridDim.x / nch;
-  const int pa0 = ch * C, Pe = min(C, n - pa0);
+  const int pa0 = p_lo + ch * C, Pe = min(C, p_hi - pa0);
   const FoldSmem L(n, C);
   const int cube = L.cube;
   double* S = sm + L.pi_off();
@@ -510,7 +520,8 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
     }
   }
   // X3 cell e = (pair*Pe + pa_l): fold-order slot pair*C + pa_l; packed as
-  // A = fi | col << 12 | pair << 18, B = j1 | j2 << 8 | pa_l << 16
+  // A = fi | col << 12 | pair << 18, B = j1 | j2 << 8 | pa_l << 16 | (xr+1) << 24
+  // (xr: the rank owning the cell's tile when it is not this one)
   uint32_t x3a[kFoldSlots], x3b[kFoldSlots];
   const int cnt3 = lpairs * Pe;
 #pragma unroll
@@ -528,6 +539,9 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
                  ((uint32_t)pair << 18);
         x3b[k] = (uint32_t)(pa_l * nm1 + pb - (pb > pa)) |
                  ((uint32_t)(pa_l * nm1 + pc - (pc > pa)) << 8) | ((uint32_t)pa_l << 16);
+        if constexpr (SH) {
+          if (sl.owner[pb] != sl.rank) x3b[k] |= (uint32_t)(sl.owner[pb] + 1) << 24;
+        }
       }
     }
   }
@@ -548,6 +562,11 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
     const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
     const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
     const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;  // d3 base of the unit
+    size_t unit = 0, rbT = 0;  // sharded: unit index and rows_before[fbc]
+    if constexpr (SH) {
+      unit = (size_t)(P.tri0 + T) * nch + ch;
+      rbT = (size_t)P.shard->rows_before[fbc];
+    }
     const int G = P.x3_group, g0 = (ch * C) / G;
     const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * G + (ch * C - g0 * G);
     // ---- stage: every load of the unit in flight before one wait ----
@@ -565,7 +584,19 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
     for (int k = 0; k < kFoldSlots; ++k) {
       if (x3b[k] == 0xffffffffu) continue;
       const int e = tid + k * bd;
-      const uint32_t pr = x3a[k] >> 18, pl = x3b[k] >> 16;
+      const uint32_t pr = x3a[k] >> 18, pl = (x3b[k] >> 16) & 0xffu;
+      if constexpr (SH) {
+        const int xr = (int)(x3b[k] >> 24) - 1;
+        if (xr >= 0) {  // tile of rank xr: its Z-LAP pushed pi; this rank keeps the D'
+          const int* pbd = sl.pbound;
+          const int lpl = (int)pr - pbd[xr] * nm1, nx = pbd[xr + 1] - pbd[xr];
+          const size_t xi = ((size_t)nx * nm1 * rbT + (size_t)lpl * b + a) * (p_hi - p_lo) +
+                            (size_t)(ch * C) + pl;
+          cp_async8(S + 2 * cube + (x3a[k] & 0xfffu), sl.pi_recv[xr] + xi);
+          cp_async8(V + base3 + e, sl.d3[xr] + (unit * nx * nm1 + lpl) * C + pl);
+          continue;
+        }
+      }
       cp_async8(S + 2 * cube + (x3a[k] & 0xfffu), x3buf + upi + pr * G + pl);
       cp_async8(V + base3 + e, d3 + ub + pr * C + pl);
     }
@@ -613,7 +644,19 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       const double s2 = dadd(dmul(kz, p2), U2[(x3b[k] >> 8) & 0xffu]);
       const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
       const double dn = dadd(V[base3 + e], dsub(gain, dmul(kz, p3)));
-      d3[ub + pair * C + (x3b[k] >> 16)] = dn;
+      const uint32_t pl = (x3b[k] >> 16) & 0xffu;
+      if constexpr (SH) {
+        const int xr = (int)(x3b[k] >> 24) - 1;
+        if (xr >= 0) {  // D' stays here, the new cost goes to the tile's owner (NVLink)
+          const int* pbd = sl.pbound;
+          const int lpl = (int)pair - pbd[xr] * nm1, nx = pbd[xr + 1] - pbd[xr];
+          const size_t gi = (unit * nx * nm1 + lpl) * C + pl;
+          sl.d3[xr][gi] = dn;
+          sl.cost_send[xr][gi] = fast ? dadd(dmul(omk, p3), gain) : dn;
+          continue;
+        }
+      }
+      d3[ub + pair * C + pl] = dn;
       const uint32_t o = tb3 + pair * esz + ((x3a[k] >> 12) & 63u);
       if (fast)
         incz[o] = dadd(dmul(omk, p3), gain);
@@ -1351,18 +1394,19 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
   const int n = p.m;
   const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
-  if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_LEAN", 1) &&
+  if (p.x3buf && p.x3mode == 2 && env_int("QAPB_FOLD_LEAN", 1) &&
       nz < 4294967295.0 && p.chunk * (n - 1) * (n - 2) <= kFoldSlots * 256 &&
       p.chunk * n * (n - 1) <= kFoldSlots * 256 && FoldSmem(n, p.chunk).cube < 4096 && n < 64 &&
       p.chunk * (n - 1) < 256 && n * (n - 1) < 16384) {
-    allow_max_smem(zfold_lean_kernel);
+    auto kern = p.shard ? zfold_lean_kernel<true> : zfold_lean_kernel<false>;
+    allow_max_smem(kern);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zfold_lean_kernel, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
     const int slots = std::max(1, per_sm) * num_sms();
     const int tpc = env_int("QAPB_FOLD_LEAN_TPC", 4);  // triples per CTA (0: persistent)
     const int R = tpc > 0 ? (p.ntriples + tpc - 1) / tpc
                           : std::max(1, std::min(p.ntriples, slots / p.nchunks));
-    zfold_lean_kernel<<<R * p.nchunks, 256, smem, st>>>(p);
+    kern<<<R * p.nchunks, 256, smem, st>>>(p);
     return cudaGetLastError();
   }
   allow_max_smem(zfold_kernel);
