@@ -964,9 +964,38 @@ size_t Engine::array_size(int which) const {
   throw std::invalid_argument("unknown engine array");
 }
 
+// Sharded engines hold pi(z), D' and incz partially (kernels.cu,
+// shard_state_mask_kernel): assemble the full array on every rank.  Collective:
+// every rank must call it for the same array.
+void Engine::assemble_sharded(int which, double* dst) const {
+  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  cuda_check(cudaStreamSynchronize(st_), "assemble");
+  double* src = which == QAPB_ARR_PI_Z ? piz_ : (which == QAPB_ARR_INCZ ? incz_ : d_);
+  if (which == QAPB_ARR_STORE_D) {
+    split_scatter();  // local split D' -> tiles
+    cuda_check(launch_shard_state_scatter(m_, shard_, triples_, d_, 0, st_), "d3 scatter");
+  } else if (which == QAPB_ARR_INCZ && hS_.iter >= 2) {  // a fold has stored costs
+    cuda_check(launch_shard_state_scatter(m_, shard_, triples_, incz_, 1, st_), "cost scatter");
+  }
+  unsigned long long* buf = nullptr;
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), nd_ * sizeof(double), st_),
+             "cudaMallocAsync");
+  cuda_check(launch_shard_state_mask(m_, shard_, src, buf, which == QAPB_ARR_STORE_D ? 1 : 0, st_),
+             "state mask");
+  nccl_check(nccl().AllReduce(buf, buf, nd_, ncclUint64, ncclSum, comm_, st_), "assemble");
+  cuda_check(cudaMemcpyAsync(dst, buf, nd_ * sizeof(double), cudaMemcpyDefault, st_), "D2H");
+  cuda_check(cudaFreeAsync(buf, st_), "cudaFreeAsync");
+  cuda_check(cudaStreamSynchronize(st_), "assemble");
+}
+
 void Engine::get_array(int which, double* dst, size_t count) const {
   const size_t n = array_size(which);
   if (count != n) throw std::invalid_argument("array size mismatch");
+  if (world_ > 1 && n &&
+      (which == QAPB_ARR_PI_Z || which == QAPB_ARR_STORE_D || which == QAPB_ARR_INCZ)) {
+    assemble_sharded(which, dst);
+    return;
+  }
   const double* src = nullptr;
   switch (which) {
     case QAPB_ARR_PI_Z: src = piz_; break;

@@ -120,6 +120,7 @@ class Engine {
   int* rows_before_ = nullptr;
   double* theta_buf_ = nullptr;
   void barrier();
+  void assemble_sharded(int which, double* dst) const;
   // single-GPU X3 split (kernels.h FoldParams::x3buf)
   void split_gather();
   void split_scatter() const;

@@ -1152,6 +1152,83 @@ __global__ void x3_cost_scatter_kernel(int n, ShardInfo sh, const int* __restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sharded z-state assembly (qapb_engine_get_array on a sharded engine is
+// collective).  Every rank first brings its own copy up to date where it is
+// authoritative, then keeps only those cells (others zeroed, as bit
+// patterns) so a uint64 sum all-reduce reproduces every value bitwise.
+//   pi(z), incz: the tile's owner (first location p);
+//   D': the fold owner owner(r) for the X3 cells (row k < i) of families
+//       folded on another rank, else the tile's owner.
+
+// D' of the X3 cells this rank folds for rank xr (d3[xr], fold order) ->
+// this rank's copy of d at their places in xr's tiles; or (costs) the
+// received costs cost_recv[A] -> this rank's own tiles.
+__global__ void shard_state_scatter_kernel(int n, ShardInfo sh, const int* __restrict__ triples,
+                                           double* __restrict__ dst, int costs) {
+  const int nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
+  const size_t esz = (size_t)nm2 * nm2;
+  const int me = sh.rank, C = sh.chunk;
+  const DIdx ix(n);
+  for (int R = 0; R < sh.world; ++R) {
+    if (R == me) continue;
+    // costs: fold owner A = R, X3 owner B = me; D': fold owner A = me, X3 owner B = R
+    const int A = costs ? R : me, B = costs ? me : R;
+    const int a_lo = sh.pbound[A], nA = sh.pbound[A + 1] - a_lo, nch = shard_chunks(sh, A);
+    const int b_lo = sh.pbound[B], nB = sh.pbound[B + 1] - b_lo;
+    const size_t per_unit = (size_t)nB * nm1 * C;
+    const size_t total = (size_t)n * (n - 1) * (n - 2) / 6 * nch * per_unit;
+    const double* __restrict__ src = costs ? sh.cost_recv[R] : sh.d3[R];
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+         i += (size_t)gridDim.x * blockDim.x) {
+      const size_t u = i / per_unit;
+      const int r = (int)(i - u * per_unit);
+      const int lpl = r / C, pa_l = r - lpl * C;
+      const int T = (int)(u / nch), ch = (int)(u - (size_t)T * nch);
+      const int po = ch * C + pa_l;
+      const int pb = b_lo + lpl / nm1, pci = lpl - (pb - b_lo) * nm1, pc = pci + (pci >= pb);
+      const int pa = a_lo + po;
+      if (po >= nA || pa == pc) continue;
+      const int a = triples[3 * T], b = triples[3 * T + 1], c = triples[3 * T + 2];
+      const int lo = min(pb, pc), hi = max(pb, pc), col = pa - (pa > lo) - (pa > hi);
+      dst[((size_t)ix.fpair(b, c) * lpairs + pb * nm1 + pci) * esz + (size_t)a * nm2 + col] =
+          src[i];
+    }
+  }
+}
+
+// keep the cells this rank is authoritative for (bit patterns), zero the rest
+__global__ void shard_state_mask_kernel(int n, ShardInfo sh, const double* __restrict__ src,
+                                        unsigned long long* __restrict__ out, int fold_owned) {
+  const int nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1, m = n;
+  const size_t esz = (size_t)nm2 * nm2;
+  const size_t total = (size_t)(m * (m - 1) / 2) * lpairs * esz;
+  const int me = sh.rank;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < total;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = g / esz;
+    const int cell = (int)(g - t * esz);
+    const int fp = (int)(t / lpairs), lp = (int)(t - (size_t)fp * lpairs);
+    const int p = lp / nm1, qq = lp - p * nm1, q = qq + (qq >= p);
+    int auth = shard_owner(sh, p);
+    if (fold_owned) {  // X3 member of family (k, i, j): folded by owner(r)
+      int i = 0, acc = 0;
+      while (fp >= acc + (m - 1 - i)) {
+        acc += m - 1 - i;
+        ++i;
+      }
+      const int kl = cell / nm2;
+      if (kl < i) {  // k = kl (k < i < j)
+        const int rl = cell - kl * nm2, lo = min(p, q), hi = max(p, q);
+        int r = rl + (rl >= lo);
+        r += (r >= hi);
+        auth = shard_owner(sh, r);
+      }
+    }
+    out[g] = (auth == me) ? __double_as_longlong(src[g]) : 0ULL;
+  }
+}
+
 // theta of every rank's tile runs <-> one buffer of rank segments
 __global__ void theta_xfer_kernel(int m, double* theta, double* buf, ShardInfo sh, int pack) {
   const int nm1 = m - 1, lpairs = m * nm1, fpairs = m * nm1 / 2;
@@ -1531,6 +1608,18 @@ cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaStat
 cudaError_t launch_x3_cost_scatter(int n, const ShardInfo& sh, const int* triples, double* costs,
                                    cudaStream_t st) {
   x3_cost_scatter_kernel<<<4 * num_sms(), 256, 0, st>>>(n, sh, triples, costs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_state_scatter(int n, const ShardInfo& sh, const int* triples,
+                                       double* dst, int costs, cudaStream_t st) {
+  shard_state_scatter_kernel<<<4 * num_sms(), 256, 0, st>>>(n, sh, triples, dst, costs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_state_mask(int n, const ShardInfo& sh, const double* src,
+                                    unsigned long long* out, int fold_owned, cudaStream_t st) {
+  shard_state_mask_kernel<<<8 * num_sms(), 256, 0, st>>>(n, sh, src, out, fold_owned);
   return cudaGetLastError();
 }
 

@@ -222,6 +222,11 @@ cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaStat
 // sharded: remote-folded X3 costs (cost_recv) -> the tile-layout cost array
 cudaError_t launch_x3_cost_scatter(int n, const ShardInfo& sh, const int* triples, double* costs,
                                    cudaStream_t st);
+// sharded z-state assembly (Engine::get_array on a sharded engine)
+cudaError_t launch_shard_state_scatter(int n, const ShardInfo& sh, const int* triples,
+                                       double* dst, int costs, cudaStream_t st);
+cudaError_t launch_shard_state_mask(int n, const ShardInfo& sh, const double* src,
+                                    unsigned long long* out, int fold_owned, cudaStream_t st);
 cudaError_t launch_theta_xfer(int m, double* theta, double* buf, const ShardInfo& sh, int pack,
                               cudaStream_t st);
 cudaError_t launch_sa_apply(int m, double* b, const double* sa_fac, const double* sa_loc,

@@ -21,6 +21,11 @@ import paper_1710_03732_b200 as q  # noqa: E402
 from paper_1710_03732_b200.instance import QapInstance, grid_instance  # noqa: E402
 
 
+def digest(a):  # as tests/conftest.py
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()[:32]
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -42,11 +47,22 @@ def main():
                              sa_enabled=tr["sa"], upper_bound=tr["upper_bound"], seed=tr["seed"])
         eng = q.AscentEngine.from_instance_sharded(inst, cfg, rank, world, idobj[0])
         want = [float.fromhex(x) for x in tr["bounds"]]
-        got = [eng.iterate() for _ in want]
+        got, state_ok = [], True
+        for it in range(1, len(want) + 1):
+            got.append(eng.iterate())
+            snap = tr["digests"].get(str(it))
+            if snap and key.startswith("nug12"):  # the assembled z state (collective)
+                for a in ("pi_z", "d"):
+                    if digest(eng.array(a)) != snap[a]:
+                        state_ok = f"iteration {it}: {a} digest"
+                if "incz" in snap and digest(eng.incz()) != snap["incz"]:
+                    state_ok = f"iteration {it}: incz digest"
         results[key] = got == want
         if not results[key]:
             bad = next(i for i, (a, b) in enumerate(zip(got, want)) if a != b)
             results[key] = f"iteration {bad + 1}: {got[bad]!r} != {want[bad]!r}"
+        elif state_ok is not True:
+            results[key] = state_ok
         eng.close()
     # run() with device-side termination on the sharded engine
     idobj = [q.nccl_unique_id() if rank == 0 else None]
