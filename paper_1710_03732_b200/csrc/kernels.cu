@@ -671,6 +671,402 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
   }
 }
 
+// Bulk-staged lean fold (single GPU, X3 split, n even, chunk 2); same
+// arithmetic as zfold_kernel (rlt2.cpp:269-298).  Shared memory keeps every
+// member in its own storage order instead of the family cube, so the X1/X2
+// rows of pi(z) and D' (n-2 contiguous doubles each) arrive as TMA bulk
+// copies on one mbarrier, the X3 D' block of the unit and the push row of
+// tile (b,c) as one bulk copy each, and the X3 pi pairs as 16-byte cp.async;
+// a thread keeps the partner indices of its cells in registers.  This drops
+// the per-cell 8-byte LDGSTS and their address arithmetic of zfold_lean_kernel.
+__global__ void __launch_bounds__(256, 2) zfold_bulk_kernel(FoldParams P) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int n = P.m, nm1 = n - 1, nm2 = n - 2;
+  constexpr int C = 2;
+  const int lpairs = n * nm1;
+  const uint32_t esz = (uint32_t)(nm2 * nm2);
+  const int nch = P.nchunks, ch = blockIdx.x % nch, r0 = blockIdx.x / nch, R = gridDim.x / nch;
+  const int pa0 = ch * C;
+  const int c12 = C * nm1 * nm2, c3 = lpairs * C;
+  double* P1 = sm;         // X1 pi, rows (pa_l, q) of n-2
+  double* P2 = P1 + c12;   // X2 pi
+  double* V1 = P2 + c12;   // X1 D'
+  double* V2 = V1 + c12;   // X2 D'
+  double* P3 = V2 + c12;   // X3 pi, [pair][pa_l]
+  double* V3 = P3 + c3;    // X3 D' (the unit's d3 block)
+  double* U1 = V3 + c3;    // push of tiles (a,b,pa,*)
+  double* U2 = U1 + C * nm1;
+  double* U3 = U2 + C * nm1;  // push of tiles (b,c,*,*)
+  const int tid = threadIdx.x, bd = blockDim.x;
+  auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
+  auto colskip = [](int x, int u, int v) { return x - (x > min(u, v)) - (x > max(u, v)); };
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // X1/X2 cell e = ((pa_l*nm1 + qi)*nm2 + r): tile (.,.,pa,q), column r -> other.
+  // ju = partner cell (the other member's row layout) | U1/U2 slot << 16;
+  // lu = X3 pi slot of the (q,other) | (other,q) family (U3 slot = slot >> 1)
+  uint32_t rel12[kFoldSlots], ju12[kFoldSlots], lu12[kFoldSlots];
+  const int cnt12 = c12;
+#pragma unroll
+  for (int k = 0; k < kFoldSlots; ++k) {
+    const int e = tid + k * bd;
+    rel12[k] = 0xffffffffu;
+    if (e < cnt12) {
+      const int pa_l = e / (nm1 * nm2), rem = e - pa_l * nm1 * nm2;
+      const int qi = rem / nm2, r = rem - qi * nm2;
+      const int pa = pa0 + pa_l, q = qi + (qi >= pa);
+      const int other = skip2(r, min(pa, q), max(pa, q));
+      const int jo = pa_l * nm1 + other - (other > pa);
+      rel12[k] = (uint32_t)lpair(pa, q) * esz + r;
+      ju12[k] = (uint32_t)(jo * nm2 + colskip(q, pa, other)) | ((uint32_t)jo << 16);
+      lu12[k] = (uint32_t)(lpair(q, other) * C + pa_l) |
+                ((uint32_t)(lpair(other, q) * C + pa_l) << 16);
+    }
+  }
+  // X3 cell e = pair*C + pa_l; A = r1 | r2 << 6 | col << 12 | pair << 18,
+  // B = j1 | j2 << 8 (U1/U2 slots; partner cells j1*(n-2)+r1, j2*(n-2)+r2)
+  uint32_t x3a[kFoldSlots], x3b[kFoldSlots];
+#pragma unroll
+  for (int k = 0; k < kFoldSlots; ++k) {
+    const int e = tid + k * bd;
+    x3b[k] = 0xffffffffu;
+    if (e < c3) {
+      const int pair = e / C, pa_l = e - pair * C;
+      const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
+      const int pa = pa0 + pa_l;
+      if (pa != pb && pa != pc) {
+        const int col = colskip(pa, pb, pc);
+        x3a[k] = (uint32_t)colskip(pc, pa, pb) | ((uint32_t)colskip(pb, pa, pc) << 6) |
+                 ((uint32_t)col << 12) | ((uint32_t)pair << 18);
+        x3b[k] = (uint32_t)(pa_l * nm1 + pb - (pb > pa)) |
+                 ((uint32_t)(pa_l * nm1 + pc - (pc > pa)) << 8);
+      }
+    }
+  }
+
+  const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
+  const double* __restrict__ piz = P.piz;
+  const double* __restrict__ push = P.push;
+  double* __restrict__ d = P.d;
+  double* __restrict__ incz = P.incz;
+  const double* __restrict__ x3buf = P.x3buf;
+  double* __restrict__ d3 = P.d3;
+  const int fast = P.fast;
+  const DIdx ix(n);
+  const int nrows = C * nm1;
+  const unsigned row_bytes = (unsigned)nm2 * 8u;
+  const unsigned tx_bytes = 4u * nrows * row_bytes + (unsigned)(c3 + lpairs) * 8u;
+  unsigned phase = 0;
+  for (int T = r0; T < P.ntriples; T += R) {
+    const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+    const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
+    const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
+    const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+    const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
+    const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;  // d3 base of the unit
+    const int G = P.x3_group, g0 = (ch * C) / G;
+    const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * G + (ch * C - g0 * G);
+    // ---- stage ----
+    if (tid == 0) mbar_expect_tx(&bar, tx_bytes);
+    for (int w = tid; w < 4 * nrows; w += bd) {  // P1, P2, V1, V2 rows
+      const int arr = w / nrows, row = w - arr * nrows;
+      const int pa_l = row / nm1, qi = row - pa_l * nm1, pa = pa0 + pa_l, q = qi + (qi >= pa);
+      const uint32_t off = ((arr & 1) ? tb2 : tb1) + (uint32_t)lpair(pa, q) * esz;
+      bulk_g2s(sm + (size_t)arr * c12 + row * nm2, ((arr & 2) ? d : piz) + off, row_bytes, &bar);
+    }
+    if (tid == bd - 1) bulk_g2s(V3, d3 + ub, (unsigned)c3 * 8u, &bar);
+    if (tid == bd - 2) bulk_g2s(U3, push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &bar);
+    for (int e = tid; e < lpairs; e += bd) cp_async16(P3 + e * C, x3buf + upi + (size_t)e * G);
+    for (int e = tid; e < nrows; e += bd) {
+      cp_async8(U1 + e, push + (size_t)fab * lpairs + pa0 * nm1 + e);
+      cp_async8(U2 + e, push + (size_t)fac * lpairs + pa0 * nm1 + e);
+    }
+    cp_async_wait_all();
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+    // ---- update: rlt2.cpp:280-293 per member cell ----
+#pragma unroll
+    for (int k = 0; k < kFoldSlots; ++k) {
+      if (rel12[k] == 0xffffffffu) continue;
+      const int e = tid + k * bd;
+      const uint32_t ep = ju12[k] & 0xffffu, jo = ju12[k] >> 16;
+      const uint32_t l1 = lu12[k] & 0xffffu, l2 = lu12[k] >> 16;
+      {  // X1: (pb, pc) = (q, other)
+        const double p1 = P1[e], p2 = P2[ep], p3 = P3[l1];
+        const double s2 = dadd(dmul(kz, p2), U2[jo]);
+        const double s3 = dadd(dmul(kz, p3), U3[l1 >> 1]);
+        const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
+        const uint32_t o = tb1 + rel12[k];
+        d[o] = dadd(V1[e], dsub(gain, dmul(kz, p1)));
+        if (fast) incz[o] = dadd(dmul(omk, p1), gain);
+      }
+      {  // X2: (pb, pc) = (other, q)
+        const double p2 = P2[e], p1 = P1[ep], p3 = P3[l2];
+        const double s1 = dadd(dmul(kz, p1), U1[jo]);
+        const double s3 = dadd(dmul(kz, p3), U3[l2 >> 1]);
+        const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
+        const uint32_t o = tb2 + rel12[k];
+        d[o] = dadd(V2[e], dsub(gain, dmul(kz, p2)));
+        if (fast) incz[o] = dadd(dmul(omk, p2), gain);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kFoldSlots; ++k) {
+      if (x3b[k] == 0xffffffffu) continue;
+      const int e = tid + k * bd;
+      const uint32_t j1 = x3b[k] & 0xffu, j2 = x3b[k] >> 8, pair = x3a[k] >> 18;
+      const double p3 = P3[e], p1 = P1[j1 * nm2 + (x3a[k] & 63u)];
+      const double p2 = P2[j2 * nm2 + ((x3a[k] >> 6) & 63u)];
+      const double s1 = dadd(dmul(kz, p1), U1[j1]);
+      const double s2 = dadd(dmul(kz, p2), U2[j2]);
+      const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
+      const double dn = dadd(V3[e], dsub(gain, dmul(kz, p3)));
+      d3[ub + e] = dn;
+      const uint32_t o = tb3 + pair * esz + ((x3a[k] >> 12) & 63u);
+      if (fast)
+        incz[o] = dadd(dmul(omk, p3), gain);
+      else
+        d[o] = dn;
+    }
+    __syncthreads();  // the next triple's staging overwrites shared memory
+  }
+  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
+    P.sa_fac[tid] = 0.0;
+    P.sa_loc[tid] = 0.0;
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Pipelined bulk fold: zfold_bulk_kernel's staging and update, one 512-thread
+// CTA per SM, two stage buffers: while the CTA updates unit i, the TMA copies
+// of unit i+1 are in flight.  Work item w = (block of K triples, chunk), dealt
+// round-robin, so the chunks of one triple (their X3 stores share tile rows)
+// run at the same time on neighbouring SMs; a thread re-derives its cell
+// pattern only when its chunk changes (once per K units).
+constexpr int kPipeSlots = 4;  // cells per thread per member group (<= 4 * 512)
+
+struct PipeCells {
+  uint32_t rel12[kPipeSlots], ju12[kPipeSlots], lu12[kPipeSlots];
+  uint32_t x3a[kPipeSlots], x3b[kPipeSlots];
+};
+
+__device__ __forceinline__ void pipe_cells(PipeCells& pc_, int n, int pa0, int tid, int bd) {
+  const int nm1 = n - 1, nm2 = n - 2, C = 2;
+  const uint32_t esz = (uint32_t)(nm2 * nm2);
+  auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
+  auto colskip = [](int x, int u, int v) { return x - (x > min(u, v)) - (x > max(u, v)); };
+  const int c12 = C * nm1 * nm2, c3 = n * nm1 * C;
+#pragma unroll
+  for (int k = 0; k < kPipeSlots; ++k) {
+    const int e = tid + k * bd;
+    pc_.rel12[k] = 0xffffffffu;
+    if (e < c12) {
+      const int pa_l = e / (nm1 * nm2), rem = e - pa_l * nm1 * nm2;
+      const int qi = rem / nm2, r = rem - qi * nm2;
+      const int pa = pa0 + pa_l, q = qi + (qi >= pa);
+      const int other = skip2(r, min(pa, q), max(pa, q));
+      const int jo = pa_l * nm1 + other - (other > pa);
+      pc_.rel12[k] = (uint32_t)lpair(pa, q) * esz + r;
+      pc_.ju12[k] = (uint32_t)(jo * nm2 + colskip(q, pa, other)) | ((uint32_t)jo << 16);
+      pc_.lu12[k] = (uint32_t)(lpair(q, other) * C + pa_l) |
+                    ((uint32_t)(lpair(other, q) * C + pa_l) << 16);
+    }
+    pc_.x3b[k] = 0xffffffffu;
+    if (e < c3) {
+      const int pair = e / C, pa_l = e - pair * C;
+      const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
+      const int pa = pa0 + pa_l;
+      if (pa != pb && pa != pc) {
+        pc_.x3a[k] = (uint32_t)colskip(pc, pa, pb) | ((uint32_t)colskip(pb, pa, pc) << 6) |
+                     ((uint32_t)colskip(pa, pb, pc) << 12) | ((uint32_t)pair << 18);
+        pc_.x3b[k] = (uint32_t)(pa_l * nm1 + pb - (pb > pa)) |
+                     ((uint32_t)(pa_l * nm1 + pc - (pc > pa)) << 8);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int n = P.m, nm1 = n - 1, nm2 = n - 2;
+  constexpr int C = 2;
+  const int lpairs = n * nm1;
+  const uint32_t esz = (uint32_t)(nm2 * nm2);
+  const int nch = P.nchunks;
+  const int c12 = C * nm1 * nm2, c3 = lpairs * C, nrows = C * nm1;
+  const int bufsz = 4 * c12 + 2 * c3 + 2 * nrows + lpairs;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int nblk = (P.ntriples + K - 1) / K, nwork = nblk * nch, G = gridDim.x;
+  int w = blockIdx.x;
+  if (w >= nwork) return;
+  auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const DIdx ix(n);
+  const unsigned row_bytes = (unsigned)nm2 * 8u;
+  const unsigned tx_bytes = 4u * nrows * row_bytes + (unsigned)(c3 + lpairs) * 8u;
+  const double* __restrict__ piz = P.piz;
+  const double* __restrict__ push = P.push;
+  double* __restrict__ d = P.d;
+  double* __restrict__ incz = P.incz;
+  const double* __restrict__ x3buf = P.x3buf;
+  double* __restrict__ d3 = P.d3;
+  const int Gx = P.x3_group;
+
+  auto stage = [&](int T, int ch, int buf) {
+    double* B = sm + (size_t)buf * bufsz;
+    const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+    const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
+    const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
+    const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+    const int pa0 = ch * C;
+    const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;
+    const int g0 = pa0 / Gx;
+    const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx + (pa0 - g0 * Gx);
+    if (tid == 0) mbar_expect_tx(&bar[buf], tx_bytes);
+    for (int v = tid; v < 4 * nrows; v += bd) {  // P1, P2, V1, V2 rows
+      const int arr = v / nrows, row = v - arr * nrows;
+      const int pa_l = row / nm1, qi = row - pa_l * nm1, pa = pa0 + pa_l, q = qi + (qi >= pa);
+      const uint32_t off = ((arr & 1) ? tb2 : tb1) + (uint32_t)lpair(pa, q) * esz;
+      bulk_g2s(B + (size_t)arr * c12 + row * nm2, ((arr & 2) ? d : piz) + off, row_bytes,
+               &bar[buf]);
+    }
+    double* P3 = B + 4 * c12;
+    double* U1 = P3 + 2 * c3;
+    if (tid == bd - 1) bulk_g2s(P3 + c3, d3 + ub, (unsigned)c3 * 8u, &bar[buf]);
+    if (tid == bd - 2)
+      bulk_g2s(U1 + 2 * nrows, push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &bar[buf]);
+    for (int e = tid; e < lpairs; e += bd) cp_async16(P3 + e * C, x3buf + upi + (size_t)e * Gx);
+    for (int e = tid; e < nrows; e += bd) {
+      cp_async8(U1 + e, push + (size_t)fab * lpairs + pa0 * nm1 + e);
+      cp_async8(U1 + nrows + e, push + (size_t)fac * lpairs + pa0 * nm1 + e);
+    }
+    cp_async_commit();
+  };
+
+  const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
+  const int fast = P.fast;
+  PipeCells cells;
+  int cur_ch = -1;
+  int T = (w / nch) * K;
+  unsigned ph = 0;  // bit b: parity of buffer b
+  int buf = 0;
+  stage(T, w % nch, 0);
+  while (true) {
+    // next unit of this CTA
+    int w2 = w, T2 = T + 1;
+    if (T2 >= min((w / nch + 1) * K, P.ntriples)) {
+      w2 = w + G;
+      T2 = (w2 / nch) * K;
+    }
+    const bool more = w2 < nwork;
+    if (more) stage(T2, w2 % nch, buf ^ 1);
+    const int ch = w % nch;
+    if (ch != cur_ch) {
+      pipe_cells(cells, n, ch * C, tid, bd);
+      cur_ch = ch;
+    }
+    if (more)
+      cp_async_wait_group<1>();
+    else
+      cp_async_wait_group<0>();
+    mbar_wait(&bar[buf], (ph >> buf) & 1u);
+    ph ^= 1u << buf;
+    __syncthreads();
+    // ---- update unit (T, ch): rlt2.cpp:280-293 per member cell ----
+    {
+      const double* P1 = sm + (size_t)buf * bufsz;
+      const double* P2 = P1 + c12;
+      const double* V1 = P2 + c12;
+      const double* V2 = V1 + c12;
+      const double* P3 = V2 + c12;
+      const double* V3 = P3 + c3;
+      const double* U1 = V3 + c3;
+      const double* U2 = U1 + nrows;
+      const double* U3 = U2 + nrows;
+      const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+      const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
+      const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
+      const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+      const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
+      const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;
+#pragma unroll
+      for (int k = 0; k < kPipeSlots; ++k) {
+        if (cells.rel12[k] == 0xffffffffu) continue;
+        const int e = tid + k * bd;
+        const uint32_t ep = cells.ju12[k] & 0xffffu, jo = cells.ju12[k] >> 16;
+        const uint32_t l1 = cells.lu12[k] & 0xffffu, l2 = cells.lu12[k] >> 16;
+        {  // X1: (pb, pc) = (q, other)
+          const double p1 = P1[e], p2 = P2[ep], p3 = P3[l1];
+          const double s2 = dadd(dmul(kz, p2), U2[jo]);
+          const double s3 = dadd(dmul(kz, p3), U3[l1 >> 1]);
+          const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
+          const uint32_t o = tb1 + cells.rel12[k];
+          d[o] = dadd(V1[e], dsub(gain, dmul(kz, p1)));
+          if (fast) incz[o] = dadd(dmul(omk, p1), gain);
+        }
+        {  // X2: (pb, pc) = (other, q)
+          const double p2 = P2[e], p1 = P1[ep], p3 = P3[l2];
+          const double s1 = dadd(dmul(kz, p1), U1[jo]);
+          const double s3 = dadd(dmul(kz, p3), U3[l2 >> 1]);
+          const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
+          const uint32_t o = tb2 + cells.rel12[k];
+          d[o] = dadd(V2[e], dsub(gain, dmul(kz, p2)));
+          if (fast) incz[o] = dadd(dmul(omk, p2), gain);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPipeSlots; ++k) {
+        if (cells.x3b[k] == 0xffffffffu) continue;
+        const int e = tid + k * bd;
+        const uint32_t j1 = cells.x3b[k] & 0xffu, j2 = cells.x3b[k] >> 8;
+        const uint32_t pair = cells.x3a[k] >> 18;
+        const double p3 = P3[e], p1 = P1[j1 * nm2 + (cells.x3a[k] & 63u)];
+        const double p2 = P2[j2 * nm2 + ((cells.x3a[k] >> 6) & 63u)];
+        const double s1 = dadd(dmul(kz, p1), U1[j1]);
+        const double s2 = dadd(dmul(kz, p2), U2[j2]);
+        const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
+        const double dn = dadd(V3[e], dsub(gain, dmul(kz, p3)));
+        d3[ub + e] = dn;
+        const uint32_t o = tb3 + pair * esz + ((cells.x3a[k] >> 12) & 63u);
+        if (fast)
+          incz[o] = dadd(dmul(omk, p3), gain);
+        else
+          d[o] = dn;
+      }
+    }
+    __syncthreads();  // buffer `buf` is restaged by the next iteration
+    if (!more) break;
+    w = w2;
+    T = T2;
+    buf ^= 1;
+  }
+  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
+    P.sa_fac[tid] = 0.0;
+    P.sa_loc[tid] = 0.0;
+  }
+}
+
 // Phase 2, rlt2.cpp:344-381 with redistribute_family (rlt2.cpp:184-205):
 // every member's cost gets add[s] + share from its family's pi triple.
 __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
@@ -1471,6 +1867,27 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
   const int n = p.m;
   const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
+  if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_BULK", 1) && n % 2 == 0 &&
+      p.chunk == 2 && p.x3_group % 2 == 0 && nz < 4294967295.0 &&
+      2 * (n - 1) * (n - 2) <= kFoldSlots * 256 && 2 * n * (n - 1) <= kFoldSlots * 256 &&
+      n * (n - 1) < 16384 && n < 64) {
+    const size_t bsmem =
+        (size_t)(8 * (n - 1) * (n - 2) + 4 * n * (n - 1) + 4 * (n - 1) + n * (n - 1)) *
+        sizeof(double);
+    if (env_int("QAPB_FOLD_PIPE", 1) && 2 * (n - 1) * (n - 2) <= kPipeSlots * 512 &&
+        2 * n * (n - 1) <= kPipeSlots * 512 && 2 * bsmem <= 220 * 1024) {
+      allow_max_smem(zfold_pipe_kernel);
+      const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
+      const int nwork = (p.ntriples + K - 1) / K * p.nchunks;
+      zfold_pipe_kernel<<<std::min(num_sms(), nwork), 512, 2 * bsmem, st>>>(p, K);
+      return cudaGetLastError();
+    }
+    allow_max_smem(zfold_bulk_kernel);
+    const int tpc = std::max(1, env_int("QAPB_FOLD_LEAN_TPC", 4));
+    const int R = (p.ntriples + tpc - 1) / tpc;
+    zfold_bulk_kernel<<<R * p.nchunks, 256, bsmem, st>>>(p);
+    return cudaGetLastError();
+  }
   if (p.x3buf && p.x3mode == 2 && env_int("QAPB_FOLD_LEAN", 1) &&
       nz < 4294967295.0 && p.chunk * (n - 1) * (n - 2) <= kFoldSlots * 256 &&
       p.chunk * n * (n - 1) <= kFoldSlots * 256 && FoldSmem(n, p.chunk).cube < 4096 && n < 64 &&
