@@ -255,6 +255,27 @@ void Engine::alloc() {
   cuda_check(cudaStreamSynchronize(st_), "stream-ordered allocations");
   cuda_check(cudaMemcpy(triples_, tr.data(), tr.size() * sizeof(int), cudaMemcpyHostToDevice),
              "H2D triples");
+  // fold processing order: triples in blocks of B values of a, b and c, so the
+  // units in flight together read several adjacent rows of each tile they touch
+  // (X1 rows c, X2 rows b, X3 rows a) instead of single 8(n-2)-byte rows
+  const int ob = env_int("QAPB_FOLD_ORDER_BLOCK", 0);
+  if (split_ && world_ == 1 && ob > 0) {
+    std::vector<int> lex((size_t)m * m * m, -1), ord;
+    ord.reserve(ntriples_);
+    for (int t = 0; t < ntriples_; ++t)
+      lex[((size_t)tr[3 * t] * m + tr[3 * t + 1]) * m + tr[3 * t + 2]] = t;
+    for (int a0 = 0; a0 < m; a0 += ob)
+      for (int b0 = a0; b0 < m; b0 += ob)
+        for (int c0 = b0; c0 < m; c0 += ob)
+          for (int a = a0; a < std::min(m, a0 + ob); ++a)
+            for (int b = std::max(b0, a + 1); b < std::min(m, b0 + ob); ++b)
+              for (int c = std::max(c0, b + 1); c < std::min(m, c0 + ob); ++c)
+                ord.push_back(lex[((size_t)a * m + b) * m + c]);
+    if ((int)ord.size() != ntriples_) throw std::logic_error("fold order: not a permutation");
+    salloc(st_, &order_, ord.size());
+    cuda_check(cudaMemcpy(order_, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice),
+               "H2D fold order");
+  }
   cuda_check(cudaMemcpy(fpair_ij_, fp.data(), fp.size() * sizeof(int), cudaMemcpyHostToDevice),
              "H2D fpairs");
   ensure_hist(std::max(cfg_.iter_limit, 64) + 1);
@@ -295,7 +316,8 @@ Engine::~Engine() {
   for (double** p : {&b_, &c_, &d_, &piz_, &incz_, &piy_, &pix_, &theta_, &theta1_, &delta_, &ybar_,
                      &dx_, &push_, &sa_fac_, &sa_loc_, &x3buf_, &d3_})
     sfree(st_, *p);
-  for (int** p : {&xrow_, &xcol_, &cert_, &triples_, &fpair_ij_, &counter_}) sfree(st_, *p);
+  for (int** p : {&xrow_, &xcol_, &cert_, &triples_, &order_, &fpair_ij_, &counter_})
+    sfree(st_, *p);
   sfree(st_, S_);
   sfree(st_, sa_state_);
   dfree(hist_bound_); dfree(hist_best_);
@@ -637,6 +659,7 @@ FoldParams Engine::fold_params(int stage) const {
     f.x3_group = x3_group_;
     f.x3_ngroups = x3_ngroups_;
   }
+  if (f.tri0 == 0 && f.ntriples == ntriples_) f.order = order_;
   return f;
 }
 

@@ -156,6 +156,7 @@ class Engine {
   double *delta_ = nullptr, *ybar_ = nullptr, *dx_ = nullptr, *push_ = nullptr;
   double *sa_fac_ = nullptr, *sa_loc_ = nullptr;
   int *xrow_ = nullptr, *xcol_ = nullptr, *cert_ = nullptr, *triples_ = nullptr;
+  int* order_ = nullptr;  // fold processing order (FoldParams::order); null = lexicographic
   int *fpair_ij_ = nullptr, *counter_ = nullptr;  // counter_: one per Z launch
   DevScalars* S_ = nullptr;
   double *hist_bound_ = nullptr, *hist_best_ = nullptr;

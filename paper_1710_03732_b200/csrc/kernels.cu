@@ -966,20 +966,24 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
 
   const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
   const int fast = P.fast;
+  const int* __restrict__ order = P.order;
+  auto tri = [&](int pos) { return order ? order[pos] : pos; };
   PipeCells cells;
   int cur_ch = -1;
-  int T = (w / nch) * K;
-  unsigned ph = 0;  // bit b: parity of buffer b
+  int pos = (w / nch) * K;  // position in the processing order
+  unsigned ph = 0;          // bit b: parity of buffer b
   int buf = 0;
+  int T = tri(pos);
   stage(T, w % nch, 0);
   while (true) {
     // next unit of this CTA
-    int w2 = w, T2 = T + 1;
-    if (T2 >= min((w / nch + 1) * K, P.ntriples)) {
+    int w2 = w, pos2 = pos + 1;
+    if (pos2 >= min((w / nch + 1) * K, P.ntriples)) {
       w2 = w + G;
-      T2 = (w2 / nch) * K;
+      pos2 = (w2 / nch) * K;
     }
     const bool more = w2 < nwork;
+    const int T2 = more ? tri(pos2) : 0;
     if (more) stage(T2, w2 % nch, buf ^ 1);
     const int ch = w % nch;
     if (ch != cur_ch) {
@@ -1058,6 +1062,7 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
     __syncthreads();  // buffer `buf` is restaged by the next iteration
     if (!more) break;
     w = w2;
+    pos = pos2;
     T = T2;
     buf ^= 1;
   }

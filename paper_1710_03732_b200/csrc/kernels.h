@@ -150,6 +150,10 @@ struct FoldParams {
   double* d3;
   int x3mode;  // 1: split (LAP patches), 2: hybrid (fold stores the cost to the tile)
   int x3_group, x3_ngroups;  // x3buf layout (BatchLapParams::x3buf)
+  // pipelined fold: the order in which triples are processed (a permutation
+  // of 0..ntriples-1 in blocks of a, b and c for DRAM row locality); null =
+  // lexicographic.  Only the processing order changes, never a buffer index.
+  const int* order;
 };
 
 struct XYFoldParams {
