@@ -58,6 +58,41 @@ def test_trace_bitwise(q, golden, key):
     eng.close()
 
 
+# Fold kernel variants (kernels.cu launch_zfold): chunk 2 at n even selects the
+# pipelined bulk-staged fold; the environment switches select the others.
+FOLD_VARIANTS = {
+    "pipe": {},
+    "pipe_k1": {"QAPB_FOLD_PIPE_K": "1"},
+    "pipe_blocked_order": {"QAPB_FOLD_ORDER_BLOCK": "3"},
+    "bulk": {"QAPB_FOLD_PIPE": "0"},
+    "lean": {"QAPB_FOLD_PIPE": "0", "QAPB_FOLD_BULK": "0"},
+    "family": {"QAPB_FOLD_PIPE": "0", "QAPB_FOLD_BULK": "0", "QAPB_FOLD_LEAN": "0"},
+}
+
+
+@pytest.mark.parametrize("fold", sorted(FOLD_VARIANTS))
+@pytest.mark.parametrize("key", ["nug12_F1", "nug12_S1", "rand20_F1", "nug12_F1_SA"])
+def test_fold_variants_bitwise(q, golden, key, fold, monkeypatch):
+    monkeypatch.setenv("QAPB_FOLD_CHUNK", "2")
+    for k, v in FOLD_VARIANTS[fold].items():
+        monkeypatch.setenv(k, v)
+    tr = golden["traces"][key]
+    inst = _inst(q, golden, key)
+    cfg = q.AscentConfig(variant=tr["variant"], iter_limit=tr["iters"], sa_enabled=tr["sa"],
+                         upper_bound=tr["upper_bound"], seed=tr["seed"])
+    eng = q.AscentEngine.from_instance(inst, cfg)
+    want = hexs(tr["bounds"])
+    for it in range(1, tr["iters"] + 1):
+        assert eng.iterate() == want[it - 1], (key, fold, it)
+        snap = tr["digests"].get(str(it))
+        if snap:
+            for a in ("pi_z", "d"):
+                assert digest(eng.array(a)) == snap[a], (key, fold, it, a)
+            if "incz" in snap:
+                assert digest(eng.incz()) == snap["incz"], (key, fold, it, "incz")
+    eng.close()
+
+
 @pytest.mark.parametrize("variant", ["F1", "S1", "F2", "S2"])
 def test_run_report_matches_oracle(q, golden, variant):
     orc = best_oracle()
