@@ -864,8 +864,9 @@ struct PipeCells {
   uint32_t x3a[kPipeSlots], x3b[kPipeSlots];
 };
 
+template <int C>
 __device__ __forceinline__ void pipe_cells(PipeCells& pc_, int n, int pa0, int tid, int bd) {
-  const int nm1 = n - 1, nm2 = n - 2, C = 2;
+  const int nm1 = n - 1, nm2 = n - 2;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
   auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
   auto colskip = [](int x, int u, int v) { return x - (x > min(u, v)) - (x > max(u, v)); };
@@ -900,12 +901,12 @@ __device__ __forceinline__ void pipe_cells(PipeCells& pc_, int n, int pa0, int t
   }
 }
 
+template <int C>  // pa values per unit: 2 (n=30), 1 (n=42)
 __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K) {
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t bar[2];
   const int n = P.m, nm1 = n - 1, nm2 = n - 2;
-  constexpr int C = 2;
   const int lpairs = n * nm1;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
   const int nch = P.nchunks;
@@ -956,7 +957,12 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
     if (tid == bd - 1) bulk_g2s(P3 + c3, d3 + ub, (unsigned)c3 * 8u, &bar[buf]);
     if (tid == bd - 2)
       bulk_g2s(U1 + 2 * nrows, push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &bar[buf]);
-    for (int e = tid; e < lpairs; e += bd) cp_async16(P3 + e * C, x3buf + upi + (size_t)e * Gx);
+    for (int e = tid; e < lpairs; e += bd) {
+      if constexpr (C == 2)
+        cp_async16(P3 + e * C, x3buf + upi + (size_t)e * Gx);
+      else
+        cp_async8(P3 + e, x3buf + upi + (size_t)e * Gx);
+    }
     for (int e = tid; e < nrows; e += bd) {
       cp_async8(U1 + e, push + (size_t)fab * lpairs + pa0 * nm1 + e);
       cp_async8(U1 + nrows + e, push + (size_t)fac * lpairs + pa0 * nm1 + e);
@@ -987,7 +993,7 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
     if (more) stage(T2, w2 % nch, buf ^ 1);
     const int ch = w % nch;
     if (ch != cur_ch) {
-      pipe_cells(cells, n, ch * C, tid, bd);
+      pipe_cells<C>(cells, n, ch * C, tid, bd);
       cur_ch = ch;
     }
     if (more)
@@ -1023,7 +1029,7 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
         {  // X1: (pb, pc) = (q, other)
           const double p1 = P1[e], p2 = P2[ep], p3 = P3[l1];
           const double s2 = dadd(dmul(kz, p2), U2[jo]);
-          const double s3 = dadd(dmul(kz, p3), U3[l1 >> 1]);
+          const double s3 = dadd(dmul(kz, p3), U3[l1 / C]);
           const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
           const uint32_t o = tb1 + cells.rel12[k];
           d[o] = dadd(V1[e], dsub(gain, dmul(kz, p1)));
@@ -1032,7 +1038,7 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
         {  // X2: (pb, pc) = (other, q)
           const double p2 = P2[e], p1 = P1[ep], p3 = P3[l2];
           const double s1 = dadd(dmul(kz, p1), U1[jo]);
-          const double s3 = dadd(dmul(kz, p3), U3[l2 >> 1]);
+          const double s3 = dadd(dmul(kz, p3), U3[l2 / C]);
           const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
           const uint32_t o = tb2 + cells.rel12[k];
           d[o] = dadd(V2[e], dsub(gain, dmul(kz, p2)));
@@ -1872,6 +1878,27 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
   const int n = p.m;
   const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
+  {  // pipelined bulk-staged fold (n even, chunk 1 or 2, single GPU)
+    const int C = p.chunk;
+    const size_t psmem = (size_t)(4 * C * (n - 1) * (n - 2) + 2 * C * n * (n - 1) +
+                                  2 * C * (n - 1) + n * (n - 1)) * sizeof(double);
+    if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_PIPE", 1) && n % 2 == 0 &&
+        (C == 1 || (C == 2 && p.x3_group % 2 == 0)) && nz < 4294967295.0 &&
+        C * (n - 1) * (n - 2) <= kPipeSlots * 512 && C * n * (n - 1) <= kPipeSlots * 512 &&
+        n < 64 && 2 * psmem <= 220 * 1024) {
+      const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
+      const int nwork = (p.ntriples + K - 1) / K * p.nchunks;
+      const int grid = std::min(num_sms(), nwork);
+      if (C == 2) {
+        allow_max_smem(zfold_pipe_kernel<2>);
+        zfold_pipe_kernel<2><<<grid, 512, 2 * psmem, st>>>(p, K);
+      } else {
+        allow_max_smem(zfold_pipe_kernel<1>);
+        zfold_pipe_kernel<1><<<grid, 512, 2 * psmem, st>>>(p, K);
+      }
+      return cudaGetLastError();
+    }
+  }
   if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_BULK", 1) && n % 2 == 0 &&
       p.chunk == 2 && p.x3_group % 2 == 0 && nz < 4294967295.0 &&
       2 * (n - 1) * (n - 2) <= kFoldSlots * 256 && 2 * n * (n - 1) <= kFoldSlots * 256 &&
@@ -1879,14 +1906,6 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
     const size_t bsmem =
         (size_t)(8 * (n - 1) * (n - 2) + 4 * n * (n - 1) + 4 * (n - 1) + n * (n - 1)) *
         sizeof(double);
-    if (env_int("QAPB_FOLD_PIPE", 1) && 2 * (n - 1) * (n - 2) <= kPipeSlots * 512 &&
-        2 * n * (n - 1) <= kPipeSlots * 512 && 2 * bsmem <= 220 * 1024) {
-      allow_max_smem(zfold_pipe_kernel);
-      const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
-      const int nwork = (p.ntriples + K - 1) / K * p.nchunks;
-      zfold_pipe_kernel<<<std::min(num_sms(), nwork), 512, 2 * bsmem, st>>>(p, K);
-      return cudaGetLastError();
-    }
     allow_max_smem(zfold_bulk_kernel);
     const int tpc = std::max(1, env_int("QAPB_FOLD_LEAN_TPC", 4));
     const int R = (p.ntriples + tpc - 1) / tpc;

@@ -62,6 +62,7 @@ def test_trace_bitwise(q, golden, key):
 # pipelined bulk-staged fold; the environment switches select the others.
 FOLD_VARIANTS = {
     "pipe": {},
+    "pipe_chunk1": {"QAPB_FOLD_CHUNK": "1"},
     "pipe_k1": {"QAPB_FOLD_PIPE_K": "1"},
     "pipe_blocked_order": {"QAPB_FOLD_ORDER_BLOCK": "3"},
     "bulk": {"QAPB_FOLD_PIPE": "0"},
@@ -73,7 +74,7 @@ FOLD_VARIANTS = {
 @pytest.mark.parametrize("fold", sorted(FOLD_VARIANTS))
 @pytest.mark.parametrize("key", ["nug12_F1", "nug12_S1", "rand20_F1", "nug12_F1_SA"])
 def test_fold_variants_bitwise(q, golden, key, fold, monkeypatch):
-    monkeypatch.setenv("QAPB_FOLD_CHUNK", "2")
+    monkeypatch.setenv("QAPB_FOLD_CHUNK", "2")  # n even, chunk 2: the pipelined fold
     for k, v in FOLD_VARIANTS[fold].items():
         monkeypatch.setenv(k, v)
     tr = golden["traces"][key]
