@@ -5,6 +5,8 @@
 // headers and link libqapb200.so.  Status codes become the reference's
 // exception types again.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cmath>
@@ -383,10 +385,36 @@ QAP_API bool redistribute_family(const double pi[3], double add[3], int virtual_
   return ok != 0;
 }
 
+// Bank-per-GPU placement (the reference's banks are threads,
+// bnb.cpp:549-556).  With QAPB_BANK_GPUS=N (N > 1, or "all"), every thread that
+// builds engines on the default device 0 is pinned to one of the first N visible
+// GPUs, round-robin in order of first use, so the reference's branch-and-bound
+// spreads its banks over the node without a source change.  Unset: device 0.
+namespace {
+int bank_device(int requested) {
+  if (requested != 0) return requested;
+  const char* e = std::getenv("QAPB_BANK_GPUS");
+  if (!e || !*e) return 0;
+  int visible = 0;
+  if (qapb_device_count(&visible) != QAPB_OK || visible < 1) return 0;
+  const int want = std::strcmp(e, "all") == 0 ? visible : std::atoi(e);
+  const int n = std::max(1, std::min(want, visible));
+  static std::atomic<int> next{0};
+  thread_local int dev = -1;
+  if (dev < 0) {
+    dev = next.fetch_add(1) % n;
+    if (std::getenv("QAPB_BANK_GPUS_VERBOSE"))
+      std::fprintf(stderr, "qapb: engine thread placed on device %d of %d\n", dev, n);
+  }
+  return dev;
+}
+}  // namespace
+
 QAP_API AscentEngine::AscentEngine(CoefficientStore store, const AscentConfig& cfg)
     : cfg_(cfg), m_(store.m) {
   if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");
-  const qapb_config c = to_c(cfg);
+  cfg_.device = bank_device(cfg.device);
+  const qapb_config c = to_c(cfg_);
   check(qapb_engine_create(store.m, store.b.data(), store.c.data(), store.d.data(), store.offset,
                            &c, &h_));
 }
