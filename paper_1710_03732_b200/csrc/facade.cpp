@@ -30,6 +30,9 @@ namespace {
 void check(qapb_status rc) {
   if (rc == QAPB_OK) return;
   const std::string msg = qapb_last_error();
+  // bnb.cpp's bank threads do not catch: QAPB_LOG_ERRORS=1 names the error
+  // before std::terminate hides it
+  if (std::getenv("QAPB_LOG_ERRORS")) std::fprintf(stderr, "qapb error %d: %s\n", (int)rc, msg.c_str());
   switch (rc) {
     case QAPB_EINVAL: throw std::invalid_argument(msg);
     case QAPB_ELOGIC: throw std::logic_error(msg);
