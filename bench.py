@@ -36,11 +36,38 @@ METRIC = "RLT2 dual-ascent iterations/sec and LAPs/sec at n=30; LB gap vs refere
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
 
+GRID_SHAPES = {12: (3, 4), 20: (4, 5), 30: (5, 6), 42: (6, 7)}
+
+
 def workload(n: int):
     from paper_1710_03732_b200.instance import grid_instance
-    shapes = {12: (3, 4), 20: (4, 5), 30: (5, 6), 42: (6, 7)}
-    r, c = shapes[n]
+    r, c = GRID_SHAPES[n]
     return grid_instance(r, c, flow_seed=1, max_flow=10, name=f"nug{n}-shaped")
+
+
+def workload_reference(orc, n: int):
+    """The same nug{n}-shaped instance built without importing the product
+    package: flows from the reference's own generate_instance(n, 1, 10)
+    (instance.cpp:131-150, via oracle/_ref), Manhattan grid distances as
+    tests/test_bnb.cpp:35-44 grid_instance."""
+    import numpy as np
+    r, c = GRID_SHAPES[n]
+    flow, _ = orc.generate_instance(n, 1, 10)
+    a = np.arange(n)
+    dist = (np.abs(a[:, None] // c - a[None, :] // c) +
+            np.abs(a[:, None] % c - a[None, :] % c)).astype(np.float64)
+    return flow, dist
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def sizes(n: int):
@@ -144,14 +171,14 @@ def cpu_reference_run(n, variant, warmup, steps, threads=None):
     reference build is absent) on this host: engine built untimed, `warmup`
     untimed iterations, then `steps` timed iterations.  Returns (it/s, kind,
     threads, seconds)."""
-    from oracle.pyoracle import Oracle, available
-    from paper_1710_03732_b200.abi import default_config
+    # the oracle loads the struct layouts standalone: nothing here maps libqapb200.so
+    from oracle.pyoracle import Oracle, available, default_config
     kind = "ref" if available("ref") else "port"
     threads = threads or os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     orc = Oracle(kind)
-    inst = workload(n)
-    eng = orc.engine_from_instance(inst.flow, inst.dist, cfg=default_config(
+    flow, dist = workload_reference(orc, n)
+    eng = orc.engine_from_instance(flow, dist, cfg=default_config(
         variant=variant, iter_limit=10 ** 6, workers=threads, record_history=0))
     for _ in range(warmup):
         eng.iterate()
@@ -187,7 +214,7 @@ def run_reference_arm(args):
         "laps_per_s": its * laps,
         "config": config_block(args, world, sharded=world > 1 and not args.replicas),
         "cpu_baseline": {"value": its, "unit": "iterations/s", "cores": threads,
-                         "kind": kind,
+                         "kind": kind, "cpu_model": cpu_model(),
                          "sample": f"{args.steps} steady-state iterations (after {args.warmup} "
                                    f"untimed) of the same n={args.n} {args.variant} workload, "
                                    f"OpenMP workers={threads}"},
@@ -372,10 +399,13 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cits, kind, threads, dt = cpu_reference_run(args.n, args.variant, 1, 2)
+            cw, cs = 3, 10
+            cits, kind, threads, dt = cpu_reference_run(args.n, args.variant, cw, cs)
             cpu = {"value": cits, "unit": "iterations/s", "cores": threads, "kind": kind,
-                   "sample": f"2 steady-state iterations (after 1 untimed) of the same "
-                             f"n={args.n} {args.variant} workload, {dt:.1f} s"}
+                   "cpu_model": cpu_model(),
+                   "sample": f"{cs} steady-state iterations (after {cw} untimed) of the same "
+                             f"n={args.n} {args.variant} workload, {dt:.1f} s, OpenMP "
+                             f"workers={threads}"}
         except Exception as e:  # reported, never silently substituted
             cpu = {"value": None, "unit": "iterations/s", "cores": os.cpu_count(),
                    "kind": "reference", "sample": f"failed: {e}"}

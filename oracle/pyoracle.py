@@ -21,10 +21,30 @@ import sys
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, os.path.dirname(HERE))
-from paper_1710_03732_b200.abi import (  # noqa: E402  (shared struct layouts)
-    Config, Record, Report, ARR, TERM_NAMES, default_config, dptr, iptr,
-    store_sizes)
+
+
+def _load_abi():
+    """The shared struct layouts (paper_1710_03732_b200/abi.py: plain ctypes,
+    loads no library) imported as a standalone module, so that using the
+    oracle never runs the product package's __init__ (which maps
+    libqapb200.so) -- the reference arm of bench.py must not load it."""
+    import importlib.util
+    name = "_qapb_abi_layouts"
+    if name in sys.modules:
+        return sys.modules[name]
+    path = os.path.join(os.path.dirname(HERE), "paper_1710_03732_b200", "abi.py")
+    spec = importlib.util.spec_from_file_location(name, path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+_abi = _load_abi()
+Config, Record, Report, ARR, TERM_NAMES = _abi.Config, _abi.Record, _abi.Report, _abi.ARR, \
+    _abi.TERM_NAMES
+default_config, dptr, iptr, store_sizes = _abi.default_config, _abi.dptr, _abi.iptr, \
+    _abi.store_sizes
 
 REF_LIB = os.path.join(HERE, "_ref", "libqapref.so")
 PORT_LIB = os.path.join(HERE, "liboracle_port.so")
@@ -170,10 +190,22 @@ class Oracle:
         return self.engine(flow.shape[0], b, c, d, 0.0, cfg)
 
 
+def _as_cfg(cfg) -> Config:
+    """A config struct of this module's Config type (callers may hold the
+    product package's identical-layout class)."""
+    if isinstance(cfg, Config):
+        return cfg
+    out = Config()
+    for name, _ in Config._fields_:
+        setattr(out, name, getattr(cfg, name))
+    return out
+
+
 class OracleEngine:
     def __init__(self, orc: Oracle, m, b, c, d, offset, cfg: Config):
         self.o = orc
         self.m = m
+        cfg = _as_cfg(cfg)
         self.cfg = cfg
         h = C.c_void_p()
         self._b, self._c = np.ascontiguousarray(b, np.float64), np.ascontiguousarray(c, np.float64)

@@ -105,6 +105,27 @@ size_t nc_of(int m) { return (size_t)m * m * (m - 1) * (m - 1); }
 size_t nd_of(int m) { return m >= 3 ? (size_t)HIdx(m).tiles() * (m - 2) * (m - 2) : 0; }
 }  // namespace
 
+namespace {
+// stream-ordered device buffer, freed on every exit path
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  DevBuf(size_t bytes, cudaStream_t s) : st(s) {
+    if (bytes) qapb::cuda_check(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+constexpr int kNoSlot = 0x7f7f7f7f;  // memset(0x7f) sentinel: no undefined slot
+}  // namespace
+
 extern "C" {
 
 QAPB_API const char* qapb_last_error(void) { return g_err.c_str(); }
@@ -162,31 +183,42 @@ QAPB_API qapb_status qapb_parse_variant(const char* s, int* variant) {  // rlt2.
 }
 
 // ---- LAP ---------------------------------------------------------------
+
+// lap.cpp:104-138 over device pointers.  Any m: m <= lap_max_m() runs the
+// warp-per-LAP solver, larger m one CTA per LAP.  Returns after the batch has
+// completed on `stream` (the undefined-slot check reads a device flag).
 QAPB_API qapb_status qapb_lap_solve_batch_device(const double* costs, int m, int count,
                                                  double* values, int* r2c, int* c2r, double* u,
                                                  double* v, void* stream) {
   return guard([&] {
     need(m > 0, "lap: m must be positive");  // lap.cpp:26
-    need(m <= qapb::lap_max_m(), "lap: m exceeds the device solver limit");
     need(count >= 0, "lap: count must be non-negative");
     if (count == 0) return;
-    int* counter = nullptr;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    qapb::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(int), st),
-                     "cudaMallocAsync");
+    DevBuf flags(2 * sizeof(int), st);
+    int* counter = flags.as<int>();
     qapb::cuda_check(cudaMemsetAsync(counter, 0, sizeof(int), st), "memset");
+    qapb::cuda_check(cudaMemsetAsync(counter + 1, 0x7f, sizeof(int), st), "memset");
     qapb::BatchLapParams p{};
     p.costs = costs;
     p.m = m;
     p.count = count;
     p.counter = counter;
+    p.undefined = counter + 1;
     p.values = values;
     p.r2c = r2c;
     p.c2r = c2r;
     p.u = u;
     p.v = v;
     qapb::cuda_check(qapb::launch_lap_batch(p, st), "lap batch");
-    qapb::cuda_check(cudaFreeAsync(counter, st), "cudaFreeAsync");
+    int und = kNoSlot;
+    qapb::cuda_check(cudaMemcpyAsync(&und, counter + 1, sizeof(int), cudaMemcpyDeviceToHost, st),
+                     "D2H");
+    qapb::cuda_check(cudaStreamSynchronize(st), "lap batch");
+    if (und != kNoSlot)
+      throw std::invalid_argument("lap: slot " + std::to_string(und) +
+                                  " has no finite-cost column to extend the assignment "
+                                  "(undefined in LapSolver::solve, lap.cpp:53)");
   });
 }
 
@@ -198,27 +230,23 @@ QAPB_API qapb_status qapb_lap_solve_batch(const double* costs, int m, int count,
     if (count == 0) return;
     cudaStream_t st = cudaStreamPerThread;
     const size_t nc = (size_t)count * m * m, nv = (size_t)count * m;
-    double *dc = nullptr, *dval = nullptr, *du = nullptr, *dv = nullptr;
-    int *dr = nullptr, *dcr = nullptr;
-    auto al = [&](void** p, size_t bytes) {
-      qapb::cuda_check(cudaMallocAsync(p, bytes, st), "cudaMallocAsync");
+    DevBuf dc(nc * 8, st), dval(values ? count * 8 : 0, st), du(u ? nv * 8 : 0, st),
+        dv(v ? nv * 8 : 0, st), dr(r2c ? nv * 4 : 0, st), dcr(c2r ? nv * 4 : 0, st);
+    qapb::cuda_check(cudaMemcpyAsync(dc.p, costs, nc * 8, cudaMemcpyHostToDevice, st), "H2D");
+    const qapb_status rc = qapb_lap_solve_batch_device(
+        dc.as<double>(), m, count, dval.as<double>(), dr.as<int>(), dcr.as<int>(),
+        du.as<double>(), dv.as<double>(), st);
+    if (rc == QAPB_EINVAL) throw std::invalid_argument(g_err);
+    if (rc == QAPB_ECUDA) throw CudaError(g_err);
+    if (rc) throw std::runtime_error(g_err);
+    auto d2h = [&](void* dst, const DevBuf& src, size_t bytes) {
+      if (dst) qapb::cuda_check(cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     };
-    al((void**)&dc, nc * 8);
-    if (values) al((void**)&dval, count * 8);
-    if (u) al((void**)&du, nv * 8);
-    if (v) al((void**)&dv, nv * 8);
-    if (r2c) al((void**)&dr, nv * 4);
-    if (c2r) al((void**)&dcr, nv * 4);
-    qapb::cuda_check(cudaMemcpyAsync(dc, costs, nc * 8, cudaMemcpyHostToDevice, st), "H2D");
-    const qapb_status rc = qapb_lap_solve_batch_device(dc, m, count, dval, dr, dcr, du, dv, st);
-    if (rc) throw std::invalid_argument(g_err);
-    if (values) cudaMemcpyAsync(values, dval, count * 8, cudaMemcpyDeviceToHost, st);
-    if (u) cudaMemcpyAsync(u, du, nv * 8, cudaMemcpyDeviceToHost, st);
-    if (v) cudaMemcpyAsync(v, dv, nv * 8, cudaMemcpyDeviceToHost, st);
-    if (r2c) cudaMemcpyAsync(r2c, dr, nv * 4, cudaMemcpyDeviceToHost, st);
-    if (c2r) cudaMemcpyAsync(c2r, dcr, nv * 4, cudaMemcpyDeviceToHost, st);
-    for (void* p : {(void*)dc, (void*)dval, (void*)du, (void*)dv, (void*)dr, (void*)dcr})
-      if (p) cudaFreeAsync(p, st);
+    d2h(values, dval, count * 8);
+    d2h(u, du, nv * 8);
+    d2h(v, dv, nv * 8);
+    d2h(r2c, dr, nv * 4);
+    d2h(c2r, dcr, nv * 4);
     qapb::cuda_check(cudaStreamSynchronize(st), "lap batch");
   });
 }

@@ -1146,7 +1146,7 @@ __device__ __forceinline__ void x3_lanes(const BatchLapParams& P, const ShardInf
   const size_t rows_base = (size_t)nB * nm1 * sh.rows_before[f] + (size_t)(lp - p_lo * nm1) * b;
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
-    const int j = s * 32 + lane;
+    const int j = lap_col<CPL>(s, lane);
     X[s].gsrc = nullptr;
     X[s].sdst = nullptr;
     if (j >= m) continue;
@@ -1186,8 +1186,9 @@ __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, i
   const int G = P.x3_group;
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
-    const int j = s * 32 + lane;
+    const int j = lap_col<CPL>(s, lane);
     X[s].gsrc = nullptr;
+    X[s].sdst = nullptr;
     if (j >= m) continue;
     const int pa = skip2(j, lo, hi), g = pa / G;
     X[s].sdst = P.x3buf + ((size_t)g * lpairs + lp) * G + (pa - g * G);
@@ -1196,13 +1197,19 @@ __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, i
   }
 }
 
-// MODE 0: plain batch; 1: sharded Z stage (ShardInfo); 2: single-GPU X3 split
+// MODE 0: plain batch; 1: sharded Z stage (ShardInfo); 2: single-GPU X3 split.
+// Per warp: one (or two) tile buffers filled by TMA bulk copies on an
+// mbarrier, then m/2 doubles x 2 of scratch (row duals / optimum terms and
+// column duals).  The slack pi = cost - u - v is computed in place in the
+// tile buffer and leaves with one TMA bulk store (flags bit 1), so the buffer
+// is only refilled after that store has read it.
 template <int CPL, int MODE>
 __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
-                                                        int buf_elems, int use_bulk, int nbuf) {
+                                                        int buf_elems, int flags, int nbuf) {
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool use_bulk = flags & 1, store_bulk = flags & 2;
   // sharded: the shard tables are read per tile and lane; keep a copy in
   // shared memory instead of going through the ShardInfo pointer
   __shared__ ShardInfo shs;
@@ -1212,12 +1219,14 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
       reinterpret_cast<int*>(&shs)[w] = reinterpret_cast<const int*>(P.sh)[w];
     __syncthreads();
   }
+  const int m = P.m;
+  const int mpad = (m + 1) & ~1;
   unsigned char* ws = smem_raw + (size_t)warp * warp_smem;
   double* buf0 = reinterpret_cast<double*>(ws);
   double* buf1 = buf0 + buf_elems;
-  double* urow = buf0 + nbuf * buf_elems;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(urow + ((P.m + 1) & ~1));
-  const int m = P.m;
+  double* urow = buf0 + nbuf * buf_elems;  // also the optimum's term scratch
+  double* vrow = urow + mpad;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vrow + mpad);
   const size_t esz = (size_t)m * m;
   const unsigned bytes = (unsigned)(esz * sizeof(double));
   auto grab = [&]() {
@@ -1229,6 +1238,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
     return P.run_len ? (t / P.run_len) * P.run_stride + P.run_off + t % P.run_len : t;
   };
   auto issue = [&](double* dst, int tile, uint64_t* b) {  // lane 0 only
+    if (store_bulk) bulk_wait_read0();  // the previous pi store has left dst
     fence_proxy_async();
     mbar_expect_tx(b, bytes);
     bulk_g2s(dst, P.costs + (size_t)gtile(tile) * esz, bytes, b);
@@ -1275,7 +1285,7 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
 #pragma unroll
           for (int s = 0; s < CPL; ++s) {
             if (!X[s].gsrc) continue;
-            const int j = s * 32 + lane;
+            const int j = lap_col<CPL>(s, lane);
             if constexpr (MODE == 1) {
               cb[a * m + j] = __ldg(X[s].gsrc + (size_t)T * X[s].gstride);
             } else {  // keep the tile-layout cost array current as well
@@ -1289,54 +1299,57 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
       }
     }
     LapLane<CPL> L;
-    const double value = warp_lap_solve<CPL>(cb, m, lane, L);
+    bool undefined = false;
+    const double value = warp_lap_solve<CPL>(cb, m, lane, L, urow, &undefined);
     if (lane == 0) {
       if (P.values) P.values[tg] = value;
       if (P.theta_ref && value < dsub(P.theta_ref[tg], 1e-7)) {  // rlt2.cpp:332-335
         atomicMin(P.err_tile, P.tile_base + tg);
         if (P.stop_w) atomicExch(P.stop_w, 1);
       }
+      if (undefined && P.undefined) atomicMin(P.undefined, P.tile_base + tg);
     }
     warp_lap_write_duals<CPL>(m, lane, L, P.r2c ? P.r2c + (size_t)tg * m : nullptr,
                               P.c2r ? P.c2r + (size_t)tg * m : nullptr,
                               P.u ? P.u + (size_t)tg * m : nullptr,
                               P.v ? P.v + (size_t)tg * m : nullptr);
-    if constexpr (MODE != 0) {
-      // slack (rlt2.cpp:320-322) of the whole tile; rows a < b also go to the
-      // X3 cells' fold slots (peer stores when sharded, the split buffer on
-      // one GPU), computed once
+    if (P.pi) {
+      // slack (rlt2.cpp:320-322) of the whole tile, in place
+      warp_lap_slack_inplace<CPL>(cb, m, lane, L, urow, vrow);
+      if constexpr (MODE != 0) {
+        // rows a < b are X3 members: their slack also goes to the cells' fold
+        // slots (peer stores when sharded, the split buffer on one GPU)
+        const int n = m + 2;
+        int T = tb - c3u(n - 1), k = n - 2;  // T(a,b,c) = tb - C(n-a-1, 3)
+        for (int a = 0; a < xb; ++a) {
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {
-        const int j = s * 32 + lane;
-        if (j < m) urow[L.p[s]] = L.w[s];
-      }
-      __syncwarp();
-      double* __restrict__ out = P.pi + (size_t)tg * esz;
-      const int n = m + 2;
-      for (int a = 0; a < m; ++a) {
-        const double ua = urow[a];
-        const bool x3row = a < xb;
-        const int T = tb - c3u(n - a - 1);  // T(a,b,c), rows a < b
-#pragma unroll
-        for (int s = 0; s < CPL; ++s) {
-          const int j = s * 32 + lane;
-          if (j >= m) continue;
-          const double sl = dsub(dsub(cb[a * m + j], ua), L.v[s]);
-          out[a * m + j] = sl;
-          if (x3row && X[s].sdst) {
+          for (int s = 0; s < CPL; ++s) {
+            const int j = lap_col<CPL>(s, lane);
+            if (j >= m || !X[s].sdst) continue;
+            const double sl = cb[a * m + j];
             if constexpr (MODE == 1)  // peer row segment, or the local split slot (nA == 0)
               X[s].sdst[X[s].nA ? (size_t)a * X[s].nA : (size_t)T * X[s].gstride] = sl;
             else
               X[s].sdst[(size_t)T * X[s].gstride] = sl;
           }
+          T += k * (k - 1) / 2;  // C(n-a-2, 2)
+          --k;
         }
       }
-      __syncwarp();
-    } else if (P.pi) {
-      warp_lap_write_slack<CPL>(cb, m, lane, L, urow, P.pi + (size_t)tg * esz);
+      double* __restrict__ out = P.pi + (size_t)tg * esz;
+      if (store_bulk) {
+        fence_proxy_async();  // this lane's generic writes -> the async proxy
+        __syncwarp();
+        if (lane == 0) {
+          bulk_s2g(out, cb, bytes);
+          bulk_commit();
+        }
+      } else {
+        for (int e = lane; e < (int)esz; e += 32) out[e] = cb[e];
+      }
     }
     __syncwarp();
-    if (use_bulk && lane == 0) {  // buffer `cur` is free again
+    if (use_bulk && lane == 0) {  // buffer `cur` is free again (after its store's read)
       if (nbuf == 2) {
         if (tnn < P.count) issue(cb, tnn, cur ? &bar[1] : &bar[0]);
       } else if (tn < P.count) {
@@ -1346,6 +1359,146 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
     if (nbuf == 2) cur ^= 1;
     t = tn;
     tn = tnn;
+  }
+  if (store_bulk && lane == 0) bulk_wait_all0();  // pi stores complete before exit
+}
+
+// ---------------------------------------------------------------------------
+// Large LAPs (m > lap_max_m(), public batch API only): one CTA per slot,
+// lap.cpp:24-84 step for step with the solver state in shared memory and the
+// cost rows read from global memory (one coalesced row per Dijkstra step).
+// Same argmin key and tie rule as the warp solvers; block-wide reduction.
+__global__ void __launch_bounds__(256) lap_block_kernel(BatchLapParams P) {
+  extern __shared__ __align__(16) unsigned char lbs[];
+  const int m = P.m, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = nt >> 5;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  double* minv = reinterpret_cast<double*>(lbs);
+  double* uu = minv + (m + 1);  // row duals (lap.cpp:31)
+  double* vv = uu + (m + 1);
+  int* p = reinterpret_cast<int*>(vv + (m + 1));
+  int* way = p + (m + 1);
+  int* used = way + (m + 1);
+  __shared__ unsigned rhi[32], rlo[32], rcol[32];
+  __shared__ int s_j1;
+  __shared__ double s_delta;
+  for (int slot = blockIdx.x; slot < P.count; slot += gridDim.x) {
+    const double* __restrict__ cost = P.costs + (size_t)slot * m * m;
+    for (int j = tid; j <= m; j += nt) {
+      p[j] = -1;
+      way[j] = -1;
+      uu[j] = 0.0;
+      vv[j] = 0.0;
+    }
+    __syncthreads();
+    bool undefined = false;
+    for (int i = 0; i < m && !undefined; ++i) {
+      for (int j = tid; j <= m; j += nt) {
+        minv[j] = INF;
+        used[j] = 0;
+      }
+      if (tid == 0) p[m] = i;
+      __syncthreads();
+      int j0 = m;
+      while (true) {
+        if (tid == 0) used[j0] = 1;  // lap.cpp:41
+        __syncthreads();
+        const int i0 = p[j0];
+        const double ui0 = uu[i0];
+        const double* __restrict__ row = cost + (size_t)i0 * m;
+        unsigned bhi = 0xffffffffu, blo = 0xffffffffu, bcol = 0xffffffffu;
+        for (int j = tid; j < m; j += nt) {  // lap.cpp:45-57
+          if (used[j]) continue;
+          const double cur = dsub(dsub(row[j], ui0), vv[j]);
+          if (cur < minv[j]) {
+            minv[j] = cur;
+            way[j] = j0;
+          }
+          if (minv[j] < INF) {
+            unsigned hi, lo;
+            ordkey2(minv[j], hi, lo);
+            if (hi < bhi || (hi == bhi && lo < blo)) {  // j ascending: first wins ties
+              bhi = hi;
+              blo = lo;
+              bcol = (unsigned)j;
+            }
+          }
+        }
+        {
+          const unsigned h = __reduce_min_sync(QAPB_FULL, bhi);
+          const unsigned l = __reduce_min_sync(QAPB_FULL, bhi == h ? blo : 0xffffffffu);
+          const unsigned c =
+              __reduce_min_sync(QAPB_FULL, (bhi == h && blo == l) ? bcol : 0xffffffffu);
+          if (lane == 0) {
+            rhi[warp] = h;
+            rlo[warp] = l;
+            rcol[warp] = c;
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {
+          const unsigned h0 = lane < nw ? rhi[lane] : 0xffffffffu;
+          const unsigned l0 = lane < nw ? rlo[lane] : 0xffffffffu;
+          const unsigned c0 = lane < nw ? rcol[lane] : 0xffffffffu;
+          const unsigned h = __reduce_min_sync(QAPB_FULL, h0);
+          const unsigned l = __reduce_min_sync(QAPB_FULL, h0 == h ? l0 : 0xffffffffu);
+          const unsigned c = __reduce_min_sync(QAPB_FULL, (h0 == h && l0 == l) ? c0 : 0xffffffffu);
+          if (lane == 0) {
+            s_j1 = c == 0xffffffffu ? -1 : (int)c;
+            s_delta = c == 0xffffffffu ? 0.0 : minv[c];
+          }
+        }
+        __syncthreads();
+        const int j1 = s_j1;
+        if (j1 < 0) {  // lap.cpp:53 found no column: undefined in the reference
+          undefined = true;
+          break;
+        }
+        const double delta = s_delta;
+        for (int j = tid; j <= m; j += nt) {  // lap.cpp:58-65
+          if (used[j]) {
+            uu[p[j]] = dadd(uu[p[j]], delta);
+            vv[j] = dsub(vv[j], delta);
+          } else {
+            minv[j] = dsub(minv[j], delta);
+          }
+        }
+        __syncthreads();
+        j0 = j1;
+        if (p[j0] == -1) break;  // lap.cpp:67
+      }
+      if (undefined) break;
+      if (tid == 0) {  // augment, lap.cpp:68-72
+        do {
+          const int j1 = way[j0];
+          p[j0] = p[j1];
+          j0 = j1;
+        } while (j0 != m);
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      if (undefined) {
+        for (int j = 0; j < m; ++j) p[j] = j;
+        if (P.undefined) atomicMin(P.undefined, P.tile_base + slot);
+      }
+      double value = 0.0;  // lap.cpp:75-80
+      for (int j = 0; j < m; ++j) value = dadd(value, cost[(size_t)p[j] * m + j]);
+      if (P.values) P.values[slot] = value;
+    }
+    __syncthreads();
+    for (int j = tid; j < m; j += nt) {
+      if (P.c2r) P.c2r[(size_t)slot * m + j] = p[j];
+      if (P.r2c) P.r2c[(size_t)slot * m + p[j]] = j;
+      if (P.u) P.u[(size_t)slot * m + j] = uu[j];
+      if (P.v) P.v[(size_t)slot * m + j] = vv[j];
+    }
+    if (P.pi)
+      for (int e = tid; e < m * m; e += nt) {
+        const int a = e / m, b = e - a * m;
+        P.pi[(size_t)slot * m * m + e] = dsub(dsub(cost[e], uu[a]), vv[b]);
+      }
+    __syncthreads();
   }
 }
 
@@ -1412,7 +1565,7 @@ __global__ void __launch_bounds__(1024) xstage_kernel(XStageParams P) {
     warp_lap_write_duals<CPL>(m, lane, L, P.xrow, P.xcol, nullptr, nullptr);
 #pragma unroll
     for (int s = 0; s < CPL; ++s) {
-      const int j = s * 32 + lane;
+      const int j = lap_col<CPL>(s, lane);
       if (j < m) sx[L.p[s]] = j;
     }
     if (lane == 0) {  // rlt2.cpp:441-447
@@ -1949,11 +2102,12 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const size_t tile_bytes = esz * sizeof(double);
   const bool aligned = (((uintptr_t)p.costs) & 15) == 0;
   const bool use_bulk = (tile_bytes % 16 == 0) && aligned;
+  const bool store_bulk = use_bulk && p.pi && (((uintptr_t)p.pi) & 15) == 0;
   const size_t buf_elems = align_up(esz, 16);  // 128-byte aligned buffers
   // tile buffers per warp: 1 (more resident warps) unless QAPB_LAP_NBUF=2
   int nbuf = use_bulk ? std::max(1, std::min(2, env_int("QAPB_LAP_NBUF", 1))) : 1;
-  auto wsm = [&](int nb) {
-    return align_up((nb * buf_elems + ((m + 1) & ~1)) * sizeof(double) + 16, 128);
+  auto wsm = [&](int nb) {  // tile buffers + row/column scratch + 2 mbarriers
+    return align_up((nb * buf_elems + 2 * (size_t)((m + 1) & ~1)) * sizeof(double) + 16, 128);
   };
   size_t warp_smem = wsm(nbuf);
   if (nbuf == 2 && warp_smem > 100 * 1024) {
@@ -1971,8 +2125,8 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   if (per_sm < 1) per_sm = 1;
   const int need = (p.count + W - 1) / W;
   const int blocks = std::max(1, std::min(need, per_sm * num_sms()));
-  kern<<<blocks, 32 * W, smem, st>>>(p, (unsigned)warp_smem, (int)buf_elems, use_bulk ? 1 : 0,
-                                     nbuf);
+  kern<<<blocks, 32 * W, smem, st>>>(p, (unsigned)warp_smem, (int)buf_elems,
+                                     (use_bulk ? 1 : 0) | (store_bulk ? 2 : 0), nbuf);
   return cudaGetLastError();
 }
 
@@ -2000,6 +2154,15 @@ inline int cpl_for(int m) { return m <= 31 ? 1 : (m <= 63 ? 2 : (m <= 95 ? 3 : 4
 
 cudaError_t launch_lap_batch(const BatchLapParams& p, cudaStream_t st) {
   if (p.count <= 0) return cudaSuccess;
+  if (p.m > lap_max_m()) {  // CTA per LAP (public API only; the engine's LAPs are <= 127)
+    if (p.sh || p.x3buf) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)(p.m + 1) * (3 * sizeof(double) + 3 * sizeof(int));
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    allow_max_smem(lap_block_kernel);
+    const int blocks = std::max(1, std::min(p.count, 4 * num_sms()));
+    lap_block_kernel<<<blocks, 256, smem, st>>>(p);
+    return cudaGetLastError();
+  }
   switch (cpl_for(p.m)) {
     case 1: return launch_lap_batch_t<1>(p, st);
     case 2: return launch_lap_batch_t<2>(p, st);

@@ -51,6 +51,8 @@ struct BatchLapParams {
   double *u, *v;        // optional
   const double* theta_ref;  // optional: phase-2 regression check (rlt2.cpp:332-335)
   int* err_tile;
+  int* undefined;           // optional: smallest slot whose LAP is undefined in the
+                            // reference (no column found by lap.cpp:53), INT_MAX = none
   int tile_base;            // global index of tile 0 of this launch (error reports)
   // optional run mapping (multi-GPU): launch tile t is global tile
   // (t / run_len) * run_stride + run_off + t % run_len

@@ -1,19 +1,35 @@
 // lap_warp.cuh — warp-per-LAP shortest-augmenting-path Hungarian (sm_100a).
 //
-// Bit-exact re-design of LapSolver::solve (lap.cpp:24-84) for one warp:
-// lane l owns columns j = s*32 + l (s < CPL), including the virtual start
-// column m (lap.cpp:21-23).  Per Dijkstra step (lap.cpp:40-67) every lane
-// relaxes its columns in parallel; the reference's ascending scan with a
-// strict `<` ("first minimum wins", lap.cpp:53) becomes a warp argmin over an
+// Bit-exact re-design of LapSolver::solve (lap.cpp:24-84) for one warp.  Each
+// lane owns CPL columns (lap_col below), including the virtual start column m
+// (lap.cpp:21-23).  Per Dijkstra step (lap.cpp:40-67) every lane relaxes its
+// columns in parallel; the reference's ascending scan with a strict `<`
+// ("first minimum wins", lap.cpp:53) becomes a warp argmin over an
 // order-preserving 64-bit key with the lowest column on ties, done with
-// `redux.sync` on the key halves (+ ballot / a third redux for the column).
-// Every per-element update (lap.cpp:48-65) is order independent, so the
-// result — assignment, duals, and the optimum summed in column order
-// (lap.cpp:75-80) — is bitwise identical to the serial reference.
+// `redux.sync` on the key halves.  Every per-element update (lap.cpp:48-65) is
+// order independent, so the result — assignment, duals, and the optimum summed
+// in column order (lap.cpp:75-80) — is bitwise identical to the serial
+// reference.
 //
 // Row duals are kept per *column* (w[j] == u[p[j]]): u[i0] for the row that
 // just entered the tree is then read from the same lane as p[j1], so a step
 // needs one round of shuffles instead of two dependent ones.
+//
+// Three solvers share that scheme:
+//  * warp_lap_solve_fast1 (m <= 31, the Z stage at n <= 33): lanes own
+//    columns in REVERSE order (column 31 - lane), so the lowest tied column is
+//    the highest ballot bit and a single FLO finds it; a used column carries
+//    minv = NaN (its key sorts last, `cur < NaN` is false); the dual update is
+//    three predicated DADDs; the augmenting path is shifted in one parallel
+//    shuffle round.
+//  * warp_lap_solve_fastN<CPL> (m <= 32*CPL-1): the same with CPL columns per
+//    lane (column s*32 + lane) and a third redux for the lowest tied column.
+//  * warp_lap_solve_safe<CPL>: explicit used flags and no NaN marking, for
+//    tiles whose costs are not all finite with |c| <= 1e300 (the fast solvers'
+//    NaN trick needs finite values).  It follows lap.cpp step for step, +inf
+//    and huge costs included; where the reference's scan finds no column
+//    (lap.cpp:53 never true: j1 = -1 and p[-1] is read — undefined behaviour)
+//    it stops and reports the slot as undefined instead.
 #pragma once
 
 #include "common.cuh"
@@ -43,10 +59,21 @@ __device__ __forceinline__ void ordkey2(double x, unsigned& khi, unsigned& klo) 
 
 template <int CPL>
 struct LapLane {
-  int p[CPL];     // row matched to column s*32+lane, -1 when free   (lap.cpp:30)
-  double w[CPL];  // dual of that row, u[p[j]]                       (lap.cpp:31 uu)
-  double v[CPL];  // column dual                                     (lap.cpp:31 vv)
+  int p[CPL];     // row matched to column lap_col(s, lane), -1 when free  (lap.cpp:30)
+  double w[CPL];  // dual of that row, u[p[j]]                              (lap.cpp:31 uu)
+  double v[CPL];  // column dual                                            (lap.cpp:31 vv)
 };
+
+// Column owned by slot s of `lane`.  One column per lane: reversed, so the
+// lowest column of a tie is the highest set bit of a ballot.
+template <int CPL>
+__device__ __forceinline__ int lap_col(int s, int lane) {
+  return CPL == 1 ? 31 - lane : s * 32 + lane;
+}
+template <int CPL>
+__device__ __forceinline__ int lap_lane_of(int j) {
+  return CPL == 1 ? 31 - j : (j & 31);
+}
 
 // a[s] for a warp-uniform runtime slot s, without spilling `a` to local memory
 template <int CPL, class T>
@@ -58,22 +85,49 @@ __device__ __forceinline__ T pick(const T (&a)[CPL], int s) {
   return r;
 }
 
-// One-column-per-lane form (m <= 31): the hot path of the Z stage at n <= 33.
-// Same arithmetic as the generic form; minv of a used column is dead until
-// the next row (lap.cpp:36-39 resets it), so it is shifted unconditionally.
-__device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ cost, int m,
-                                                   int lane, LapLane<1>& L) {
-  const double INF = __longlong_as_double(0x7ff0000000000000ll);
-  const bool real = lane < m;
-  const double* __restrict__ colp = cost + (real ? lane : m - 1);
-  // During the solve L.p holds the matched row's byte offset p*m*8 (-1 when
-  // free): the next step's cost address is then one add away.
-  L.p[0] = -1;
-  L.w[0] = 0.0;
-  L.v[0] = 0.0;
-  int way = 0;
-  // Non-finite (or overflow-prone) costs would let the search run forever
-  // (the reference is undefined there too): check the tile once and bail out.
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double x;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(addr));
+  return x;
+}
+
+// lap.cpp:58-65 for one column: used (minv = NaN) -> u[p[j]] += delta,
+// v[j] -= delta; unused -> minv[j] -= delta.  Branch-free: a used column's
+// minv stays NaN under the subtraction, and an unused column adds +0.0 to u
+// and v, which is exact because u and v never hold -0.0 (they start at +0.0
+// and x + (+0.0) = x, x - (+0.0) = x for every other x; a sum or difference
+// of non-negative-zero operands is -0.0 only from (-0.0) + (-0.0)).  ptxas
+// turns predicated DADDs into compute-and-select, so this form (2 selects,
+// 3 DADDs) is the cheaper one.
+__device__ __forceinline__ void lap_dual_update(double& minv, double& w, double& v,
+                                                double delta) {
+  const double du = isnan(minv) ? delta : 0.0;
+  minv = dsub(minv, delta);
+  w = dadd(w, du);
+  v = dsub(v, du);
+}
+
+// minv = NaN on the lane that owns column j1 (it joins the tree; lap.cpp:41)
+__device__ __forceinline__ void lap_mark_used(double& minv, int lane, int j1lane) {
+  asm("{\n\t.reg .pred q;\n\t.reg .b32 lo, hi;\n\t"
+      "setp.eq.s32 q, %1, %2;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "@q mov.b32 hi, 0x7ff80000;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "+d"(minv)
+      : "r"(lane), "r"(j1lane));
+}
+
+// highest set bit (FLO); the mask is never zero here
+__device__ __forceinline__ int bfind_u32(unsigned x) {
+  int r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+
+// True (warp-uniform) iff every cost is finite with |c| <= 1e300: the fast
+// solvers then never meet inf/NaN (|u|,|v| stay below 2m * 1e300).
+__device__ __forceinline__ bool lap_tile_finite(const double* __restrict__ cost, int m, int lane) {
   bool ok = true;
   const int mm = m * m;
   if ((reinterpret_cast<uintptr_t>(cost) & 15) == 0) {  // Z tiles: 16-byte reads
@@ -86,89 +140,110 @@ __device__ __forceinline__ double warp_lap_solve_1(const double* __restrict__ co
   } else {
     for (int e = lane; e < mm; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
   }
-  const bool bad = !__all_sync(QAPB_FULL, ok);
-  // A used column (and padding lanes, and the virtual column m) carries
-  // minv = NaN: `cur < NaN` is false, so it never relaxes, and its order key
-  // (0xfff8...) sorts above every finite and +inf key, so it is never the
-  // argmin while an unused column remains (lap.cpp:47,58-64).  `used` is
-  // therefore just isnan(minv).
+  return __all_sync(QAPB_FULL, ok);
+}
+
+// value = sum_j cost[p[j]][j] in column order from 0.0 (lap.cpp:75-80).
+// `term` is lane's cost[p[j]][j] for its column j (< m).  With a 16-byte
+// aligned scratch of m doubles the sum runs over shared memory (two terms per
+// load); otherwise over shuffles.
+template <int CPL>
+__device__ __forceinline__ double lap_value(const double (&term)[CPL], int m, int lane,
+                                            double* scratch) {
+  double value = 0.0;
+  if (scratch) {
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int j = lap_col<CPL>(s, lane);
+      if (j < m) scratch[j] = term[s];
+    }
+    __syncwarp();
+    int c = 0;
+#pragma unroll 4
+    for (; c + 1 < m; c += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(scratch + c);
+      value = dadd(dadd(value, t.x), t.y);
+    }
+    if (c < m) value = dadd(value, scratch[c]);
+    __syncwarp();
+    return value;
+  }
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int lim = m - s * 32 < 32 ? m - s * 32 : 32;
+    for (int l = 0; l < lim; ++l)
+      value = dadd(value, __shfl_sync(QAPB_FULL, term[s], lap_lane_of<CPL>(s * 32 + l)));
+  }
+  return value;
+}
+
+// One column per lane (m <= 31), costs in shared memory, all finite.
+__device__ __forceinline__ double warp_lap_solve_fast1(const double* __restrict__ cost, int m,
+                                                       int lane, LapLane<1>& L,
+                                                       double* scratch) {
   const double QNAN = __longlong_as_double(0x7ff8000000000000ll);
-  const bool virt = lane == m;
-  const double minv0 = real ? INF : QNAN;
+  const int col = 31 - lane;
+  const bool real = col < m;
+  const int vlane = 31 - m;  // owner of the virtual column m
+  // shared-memory address of this lane's column in row 0; rows are byte offsets
+  const unsigned colbase = smem_u32(cost) + (unsigned)((real ? col : 0) * 8);
+  // During the solve L.p holds the matched row's byte offset p*m*8 (-1 when free)
+  L.p[0] = -1;
+  L.w[0] = 0.0;
+  L.v[0] = 0.0;
+  int way = vlane;
   const int m8 = m * 8;
-  int row8 = 0;  // i*m*8
-  for (int i = 0; i < m && !bad; ++i, row8 += m8) {  // lap.cpp:33
-    double minv = minv0;
-    if (virt) {  // p[m] = i; u[i] is still 0
+  for (int row8 = 0; row8 < m * m8; row8 += m8) {  // lap.cpp:33
+    if (lane == vlane) {  // p[m] = i; u[i] is still 0
       L.p[0] = row8;
       L.w[0] = 0.0;
     }
-    int j0 = m, i0 = row8;
-    double ui0 = 0.0;
-    while (true) {  // lap.cpp:40-67 (at most m+1 steps: finite costs, checked above)
-      if (lane == j0) minv = QNAN;  // column j0 joins the tree
-      const double cv = *reinterpret_cast<const double*>(reinterpret_cast<const char*>(colp) + i0);
-      const double cur = dsub(dsub(cv, ui0), L.v[0]);  // lap.cpp:48
-      if (cur < minv) {                                 // lap.cpp:49-52 (false when used)
-        minv = cur;
-        way = j0;
-      }
+    // First step (j0 = m, u[i] = 0): every real column relaxes, cur - 0.0 is
+    // cur bitwise, and cur < +inf holds for finite costs (lap.cpp:48-52).
+    double minv = real ? dsub(lds_f64(colbase + row8), L.v[0]) : QNAN;
+    way = vlane;
+    int j1;
+    while (true) {
       unsigned hi, lo;  // order key of minv (NaN keys last: used / padding lanes)
       ordkey2(minv, hi, lo);
       const unsigned hmin = __reduce_min_sync(QAPB_FULL, hi);
       const unsigned lmin = __reduce_min_sync(QAPB_FULL, hi == hmin ? lo : 0xffffffffu);
-      const int j1 = __ffs(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin)) - 1;
+      j1 = bfind_u32(__ballot_sync(QAPB_FULL, hi == hmin && lo == lmin));  // lap.cpp:53-56
       const double delta = __shfl_sync(QAPB_FULL, minv, j1);
-      const bool used = isnan(minv);
-      minv = dsub(minv, delta);  // lap.cpp:63 (NaN stays NaN when used)
-      // lap.cpp:60-61.  Adding +0.0 on unused columns is exact: u and v start
-      // at +0.0 and only ever receive sums/differences that cannot produce
-      // -0.0 from a non-negative-zero operand, so x + 0.0 == x bitwise here.
-      const double du = used ? delta : 0.0;
-      L.w[0] = dadd(L.w[0], du);
-      L.v[0] = dsub(L.v[0], du);
-      j0 = j1;
+      lap_dual_update(minv, L.w[0], L.v[0], delta);  // lap.cpp:58-65
+      lap_mark_used(minv, lane, j1);                 // next step's used[j0]
       const int pj = __shfl_sync(QAPB_FULL, L.p[0], j1);
       const double wj = __shfl_sync(QAPB_FULL, L.w[0], j1);
-      if (pj == -1) break;
-      i0 = pj;
-      ui0 = wj;
-    }
-    while (j0 != m) {  // augment, lap.cpp:68-72
-      const int jw = __shfl_sync(QAPB_FULL, way, j0);
-      const int pw = __shfl_sync(QAPB_FULL, L.p[0], jw);
-      const double ww = __shfl_sync(QAPB_FULL, L.w[0], jw);
-      if (lane == j0) {
-        L.p[0] = pw;
-        L.w[0] = ww;
+      if (pj == -1) break;  // lap.cpp:67
+      // relax from the row of column j1 (lap.cpp:42-52)
+      const double cur = dsub(dsub(lds_f64(colbase + (unsigned)pj), wj), L.v[0]);
+      if (cur < minv) {  // false when used (NaN)
+        minv = cur;
+        way = j1;
       }
-      j0 = jw;
+    }
+    // augment (lap.cpp:68-72): p[j] = p[way[j]] along the path j1 -> ... -> m,
+    // all reads before any write, so one parallel shuffle round does it
+    bool onpath = false;
+    for (int j = j1; j != vlane; j = __shfl_sync(QAPB_FULL, way, j)) onpath |= (lane == j);
+    const int pw = __shfl_sync(QAPB_FULL, L.p[0], way);
+    const double ww = __shfl_sync(QAPB_FULL, L.w[0], way);
+    if (onpath) {
+      L.p[0] = pw;
+      L.w[0] = ww;
     }
   }
-  if (bad) {  // non-finite input: leave a valid permutation for the writers
-    L.p[0] = real ? lane : -1;
-    L.w[0] = L.v[0] = __longlong_as_double(0x7ff8000000000000ll);
-    return L.w[0];
-  }
-  const int prow = L.p[0] < 0 ? -1 : L.p[0] / (8 * m);  // back to row indices
-  L.p[0] = prow;
-  const double term = real ? cost[(size_t)prow * m + lane] : 0.0;
-  double value = 0.0;  // lap.cpp:75-80
-  for (int l = 0; l < m; ++l) value = dadd(value, __shfl_sync(QAPB_FULL, term, l));
-  return value;
+  double term[1];
+  term[0] = real ? lds_f64(colbase + (unsigned)L.p[0]) : 0.0;
+  L.p[0] = L.p[0] < 0 ? -1 : L.p[0] / m8;  // back to row indices
+  return lap_value<1>(term, m, lane, scratch);
 }
 
-// Solve the m x m LAP whose row-major costs sit in shared memory `cost`.
-// All 32 lanes must call it.  Returns the optimum (warp-uniform).
+// CPL columns per lane (column s*32 + lane), costs in shared memory, all finite.
 template <int CPL>
-__device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost, int m,
-                                                 int lane, LapLane<CPL>& L) {
-  if constexpr (CPL == 1) {
-    return warp_lap_solve_1(cost, m, lane, L);
-  }
-  // Same scheme as warp_lap_solve_1 with CPL columns per lane: used and
-  // padding columns carry minv = NaN, rows travel as byte offsets, the dual
-  // update adds `used ? delta : +0.0` unconditionally.
+__device__ __forceinline__ double warp_lap_solve_fastN(const double* __restrict__ cost, int m,
+                                                       int lane, LapLane<CPL>& L,
+                                                       double* scratch) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   const double QNAN = __longlong_as_double(0x7ff8000000000000ll);
   double minv[CPL];
@@ -186,16 +261,6 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
     minv0[s] = j < m ? INF : QNAN;
   }
   const int vs = m >> 5, vl = m & 31;  // owner of the virtual column m
-  bool ok = true;  // finite costs bound every row to m+1 steps (see warp_lap_solve_1)
-  for (int e = lane; e < m * m; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
-  if (!__all_sync(QAPB_FULL, ok)) {
-#pragma unroll
-    for (int s = 0; s < CPL; ++s) {
-      L.p[s] = (s * 32 + lane < m) ? s * 32 + lane : -1;
-      L.w[s] = L.v[s] = QNAN;
-    }
-    return L.w[0];
-  }
   const int m8 = m * 8;
   int row8 = 0;
   for (int i = 0; i < m; ++i, row8 += m8) {  // lap.cpp:33
@@ -238,12 +303,7 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
       const int s1 = j1 >> 5, l1 = j1 & 31;
       const double delta = __shfl_sync(QAPB_FULL, pick<CPL>(minv, s1), l1);
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {  // dual update, lap.cpp:58-65 (see warp_lap_solve_1)
-        const double du = isnan(minv[s]) ? delta : 0.0;
-        minv[s] = dsub(minv[s], delta);
-        L.w[s] = dadd(L.w[s], du);
-        L.v[s] = dsub(L.v[s], du);
-      }
+      for (int s = 0; s < CPL; ++s) lap_dual_update(minv[s], L.w[s], L.v[s], delta);
       j0 = j1;
       const int pj = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, s1), l1);
       const double wj = __shfl_sync(QAPB_FULL, pick<CPL>(L.w, s1), l1);
@@ -268,21 +328,148 @@ __device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost
       j0 = jw;
     }
   }
-  // back to row indices; value = sum_j cost[p[j]][j] in column order (lap.cpp:75-80)
   double term[CPL];
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
     const int j = s * 32 + lane;
-    L.p[s] = L.p[s] < 0 ? -1 : L.p[s] / m8;
+    L.p[s] = L.p[s] < 0 ? -1 : L.p[s] / m8;  // back to row indices
     term[s] = (j < m) ? cost[(size_t)L.p[s] * m + j] : 0.0;
   }
-  double value = 0.0;
+  return lap_value<CPL>(term, m, lane, scratch);
+}
+
+// lap.cpp:24-84 with explicit used flags (any costs, +inf and huge included).
+// Columns follow lap_col<CPL>.  Sets `undefined` (warp-uniform) where the
+// reference's scan would find no column.
+template <int CPL>
+__device__ __forceinline__ double warp_lap_solve_safe(const double* __restrict__ cost, int m,
+                                                   int lane, LapLane<CPL>& L, bool& undefined) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  double minv[CPL];
+  int way[CPL];
+  bool used[CPL];
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
-    const int lim = m - s * 32 < 32 ? m - s * 32 : 32;
-    for (int l = 0; l < lim; ++l) value = dadd(value, __shfl_sync(QAPB_FULL, term[s], l));
+    L.p[s] = -1;
+    L.w[s] = 0.0;
+    L.v[s] = 0.0;
+    way[s] = -1;
   }
-  return value;
+  undefined = false;
+  const int vown = lap_lane_of<CPL>(m), vslot = CPL == 1 ? 0 : (m >> 5);
+  for (int i = 0; i < m && !undefined; ++i) {  // lap.cpp:33
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      minv[s] = INF;
+      used[s] = false;
+      if (s == vslot && lane == vown) {  // p[m] = i
+        L.p[s] = i;
+        L.w[s] = 0.0;
+      }
+    }
+    int j0 = m;
+    while (true) {
+      const int o0 = lap_lane_of<CPL>(j0), s0 = CPL == 1 ? 0 : (j0 >> 5);
+#pragma unroll
+      for (int s = 0; s < CPL; ++s)
+        if (s == s0 && lane == o0) used[s] = true;  // lap.cpp:41
+      const int i0 = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, s0), o0);
+      const double ui0 = __shfl_sync(QAPB_FULL, pick<CPL>(L.w, s0), o0);
+      unsigned bhi = 0xffffffffu, blo = 0xffffffffu;
+      int bcol = 0x7fffffff;
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {
+        const int j = lap_col<CPL>(s, lane);
+        if (j >= m || used[s]) continue;
+        const double cur = dsub(dsub(cost[(size_t)i0 * m + j], ui0), L.v[s]);  // lap.cpp:48
+        if (cur < minv[s]) {
+          minv[s] = cur;
+          way[s] = j0;
+        }
+        if (minv[s] < INF) {  // a candidate of `minv[j] < delta` (delta starts at +inf)
+          unsigned hi, lo;
+          ordkey2(minv[s], hi, lo);
+          if (hi < bhi || (hi == bhi && lo < blo) || (hi == bhi && lo == blo && j < bcol)) {
+            bhi = hi;
+            blo = lo;
+            bcol = j;
+          }
+        }
+      }
+      const unsigned hmin = __reduce_min_sync(QAPB_FULL, bhi);
+      const unsigned lmin = __reduce_min_sync(QAPB_FULL, bhi == hmin ? blo : 0xffffffffu);
+      const bool cand = (bhi == hmin) && (blo == lmin) && bcol != 0x7fffffff;
+      const unsigned jm = __reduce_min_sync(QAPB_FULL, cand ? (unsigned)bcol : 0xffffffffu);
+      if (jm == 0xffffffffu) {  // j1 = -1 in lap.cpp:53: undefined there
+        undefined = true;
+        break;
+      }
+      const int j1 = (int)jm;
+      const int o1 = lap_lane_of<CPL>(j1), s1 = CPL == 1 ? 0 : (j1 >> 5);
+      const double delta = __shfl_sync(QAPB_FULL, pick<CPL>(minv, s1), o1);
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {  // lap.cpp:58-65 (columns 0..m)
+        const int j = lap_col<CPL>(s, lane);
+        if (j > m) continue;
+        if (used[s]) {
+          L.w[s] = dadd(L.w[s], delta);
+          L.v[s] = dsub(L.v[s], delta);
+        } else {
+          minv[s] = dsub(minv[s], delta);
+        }
+      }
+      j0 = j1;
+      const int pj = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, s1), o1);
+      if (pj == -1) break;  // lap.cpp:67
+    }
+    if (undefined) break;
+    while (j0 != m) {  // augment, lap.cpp:68-72
+      const int o0 = lap_lane_of<CPL>(j0), s0 = CPL == 1 ? 0 : (j0 >> 5);
+      const int jw = __shfl_sync(QAPB_FULL, pick<CPL>(way, s0), o0);
+      const int ow = lap_lane_of<CPL>(jw), sw = CPL == 1 ? 0 : (jw >> 5);
+      const int pw = __shfl_sync(QAPB_FULL, pick<CPL>(L.p, sw), ow);
+      const double ww = __shfl_sync(QAPB_FULL, pick<CPL>(L.w, sw), ow);
+      if (lane == o0) {
+#pragma unroll
+        for (int s = 0; s < CPL; ++s)
+          if (s == s0) {
+            L.p[s] = pw;
+            L.w[s] = ww;
+          }
+      }
+      j0 = jw;
+    }
+  }
+  double term[CPL];
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = lap_col<CPL>(s, lane);
+    if (undefined && j < m) L.p[s] = j;  // a valid permutation for the writers
+    term[s] = (j < m) ? cost[(size_t)L.p[s] * m + j] : 0.0;
+  }
+  return lap_value<CPL>(term, m, lane, nullptr);
+}
+
+// Solve the m x m LAP whose row-major costs sit in shared memory `cost`.
+// All 32 lanes must call it.  Returns the optimum (warp-uniform).  `scratch`
+// (optional): 16-byte aligned shared memory for m doubles.  `undefined`
+// (optional) is set when the reference's behaviour is undefined (see top).
+template <int CPL>
+__device__ __forceinline__ double warp_lap_solve(const double* __restrict__ cost, int m,
+                                                 int lane, LapLane<CPL>& L,
+                                                 double* scratch = nullptr,
+                                                 bool* undefined = nullptr) {
+  if (!lap_tile_finite(cost, m, lane)) {
+    bool und = false;
+    const double v = warp_lap_solve_safe<CPL>(cost, m, lane, L, und);
+    if (undefined) *undefined = und;
+    return v;
+  }
+  if (undefined) *undefined = false;
+  if constexpr (CPL == 1)
+    return warp_lap_solve_fast1(cost, m, lane, L, scratch);
+  else
+    return warp_lap_solve_fastN<CPL>(cost, m, lane, L, scratch);
 }
 
 // pi[a][b] = (cost[a][b] - u[a]) - v[b]   (rlt2.cpp:320-322, :420-422, :439-440)
@@ -293,7 +480,7 @@ __device__ __forceinline__ void warp_lap_write_slack(const double* __restrict__ 
                                                      double* urow, double* __restrict__ out) {
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
-    const int j = s * 32 + lane;
+    const int j = lap_col<CPL>(s, lane);
     if (j < m) urow[L.p[s]] = L.w[s];
   }
   __syncwarp();
@@ -301,8 +488,58 @@ __device__ __forceinline__ void warp_lap_write_slack(const double* __restrict__ 
     const double ua = urow[a];
 #pragma unroll
     for (int s = 0; s < CPL; ++s) {
-      const int b = s * 32 + lane;
+      const int b = lap_col<CPL>(s, lane);
       if (b < m) out[(size_t)a * m + b] = dsub(dsub(cost[(size_t)a * m + b], ua), L.v[s]);
+    }
+  }
+  __syncwarp();
+}
+
+// The slack in place: cost[a][b] <- (cost[a][b] - u[a]) - v[b] over the whole
+// tile in shared memory, element-parallel (two per lane and load when m is
+// even).  urow / vrow: m doubles of shared scratch each, vrow 16-byte aligned.
+template <int CPL>
+__device__ __forceinline__ void warp_lap_slack_inplace(double* __restrict__ cost, int m, int lane,
+                                                       const LapLane<CPL>& L, double* urow,
+                                                       double* vrow) {
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int j = lap_col<CPL>(s, lane);
+    if (j < m) {
+      urow[L.p[s]] = L.w[s];
+      vrow[j] = L.v[s];
+    }
+  }
+  __syncwarp();
+  const int esz = m * m;
+  if ((m & 1) == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0) {
+    int a = (2 * lane) / m, b = 2 * lane - a * m;  // element 2*lane + 64k
+    const int da = 64 / m, db = 64 - da * m;
+    for (int e = 2 * lane; e < esz; e += 64) {
+      double2 c = *reinterpret_cast<double2*>(cost + e);
+      const double ua = urow[a];
+      const double2 vb = *reinterpret_cast<const double2*>(vrow + b);
+      c.x = dsub(dsub(c.x, ua), vb.x);
+      c.y = dsub(dsub(c.y, ua), vb.y);
+      *reinterpret_cast<double2*>(cost + e) = c;
+      a += da;
+      b += db;
+      if (b >= m) {
+        b -= m;
+        ++a;
+      }
+    }
+  } else {
+    int a = lane / m, b = lane - a * m;  // element lane + 32k
+    const int da = 32 / m, db = 32 - da * m;
+    for (int e = lane; e < esz; e += 32) {
+      cost[e] = dsub(dsub(cost[e], urow[a]), vrow[b]);
+      a += da;
+      b += db;
+      if (b >= m) {
+        b -= m;
+        ++a;
+      }
     }
   }
   __syncwarp();
@@ -314,7 +551,7 @@ __device__ __forceinline__ void warp_lap_write_duals(int m, int lane, const LapL
                                                      int* r2c, int* c2r, double* u, double* v) {
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
-    const int j = s * 32 + lane;
+    const int j = lap_col<CPL>(s, lane);
     if (j < m) {
       if (c2r) c2r[j] = L.p[s];
       if (r2c) r2c[L.p[s]] = j;
