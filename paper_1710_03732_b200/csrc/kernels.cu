@@ -1078,6 +1078,299 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised z fold (single GPU, X3 split, n even; same arithmetic as
+// zfold_kernel, rlt2.cpp:269-298).  Units are zfold_pipe_kernel's (triple T,
+// chunk of C locations pa), dealt the same way.  What changes is the
+// pipeline:
+//  * only the data other threads read is staged: pi(z) of the X1 / X2 rows
+//    (TMA bulk row copies into rows of pitch R = n (16-byte aligned rows;
+//    the transposed partner reads are then 2-way instead of 4-way bank
+//    conflicts), the unit's X3 pi (fold order) and the push rows.  That is
+//    ~50 KB per unit at n=30, so S = 4 stages fit and three units' loads are
+//    in flight while one is folded;
+//  * every D' value is read and written by the thread that owns the cell, so
+//    D' never goes through shared memory: each thread loads the D' of its
+//    cells of the NEXT unit into registers while it folds the current one;
+//  * one producer warp issues the copies; the 15 consumer warps wait on
+//    per-stage full barriers and release the stage with one arrive per warp
+//    on its empty barrier — no CTA-wide barrier in the loop.
+constexpr int kWsMaxStages = 8;
+// 15 consumer warps + 1 producer warp: 16 warps, so each SM sub-partition holds
+// 4 and a thread may use 128 registers (17 warps would cap it at 96).
+constexpr int kWsCW = 15, kWsCT = 32 * kWsCW;
+
+struct WsCells {
+  uint32_t rel[kPipeSlots];   // X1/X2 cell: in-tile offset | jo << 22 (jo: partner row = push row)
+  uint32_t sm[kPipeSlots];    // own smem index | partner smem index << 16
+  uint32_t l12[kPipeSlots];   // X3 slots of the partners: l1 | l2 << 16
+  uint32_t x3a[kPipeSlots], x3b[kPipeSlots];
+};
+
+template <int C>
+__device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, int R) {
+  const int nm1 = n - 1, nm2 = n - 2;
+  const uint32_t esz = (uint32_t)(nm2 * nm2);
+  auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
+  auto colskip = [](int x, int u, int v) { return x - (x > min(u, v)) - (x > max(u, v)); };
+  const int c12 = C * nm1 * nm2, c3 = n * nm1 * C;
+#pragma unroll
+  for (int k = 0; k < kPipeSlots; ++k) {
+    const int e = tid + k * kWsCT;
+    w.rel[k] = 0xffffffffu;
+    if (e < c12) {
+      const int pa_l = e / (nm1 * nm2), rem = e - pa_l * nm1 * nm2;
+      const int qi = rem / nm2, r = rem - qi * nm2;
+      const int pa = pa0 + pa_l, q = qi + (qi >= pa);
+      const int other = skip2(r, min(pa, q), max(pa, q));
+      const int jo = pa_l * nm1 + other - (other > pa);
+      w.rel[k] = ((uint32_t)lpair(pa, q) * esz + r) | ((uint32_t)jo << 22);
+      w.sm[k] = (uint32_t)((pa_l * nm1 + qi) * R + r) |
+                ((uint32_t)(jo * R + colskip(q, pa, other)) << 16);
+      w.l12[k] = (uint32_t)(lpair(q, other) * C + pa_l) |
+                 ((uint32_t)(lpair(other, q) * C + pa_l) << 16);
+    }
+    w.x3b[k] = 0xffffffffu;
+    if (e < c3) {
+      const int pair = e / C, pa_l = e - pair * C;
+      const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
+      const int pa = pa0 + pa_l;
+      if (pa != pb && pa != pc) {
+        const int j1 = pa_l * nm1 + pb - (pb > pa), j2 = pa_l * nm1 + pc - (pc > pa);
+        // smem index of the X1 / X2 partner; its push row is that index / R
+        w.x3a[k] = (uint32_t)colskip(pa, pb, pc) | ((uint32_t)pair << 8);
+        w.x3b[k] = (uint32_t)(j1 * R + colskip(pc, pa, pb)) |
+                   ((uint32_t)(j2 * R + colskip(pb, pa, pc)) << 16);
+      }
+    }
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, int K, int S,
+                                                                 int rows_async) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
+  const int n = P.m, nm1 = n - 1, nm2 = n - 2;
+  const int lpairs = n * nm1;
+  const uint32_t esz = (uint32_t)(nm2 * nm2);
+  const int R = n;  // smem row pitch: nm2 + 2 doubles
+  const int nch = P.nchunks;
+  const int nrows = C * nm1, nrows_p = (nrows + 1) & ~1;
+  const int c3 = lpairs * C;
+  // stage: P1 rows | P2 rows | P3 (fold order) | U1 | U2 | U3 (all 16-byte aligned)
+  const int oP2 = nrows * R, oP3 = 2 * nrows * R, oU1 = oP3 + c3, oU2 = oU1 + nrows_p,
+            oU3 = oU2 + nrows_p;
+  const int stage_sz = (oU3 + lpairs + 15) & ~15;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nblk = (P.ntriples + K - 1) / K, nwork = nblk * nch, G = gridDim.x;
+  if ((int)blockIdx.x >= nwork) return;
+  const int Gx = P.x3_group;
+  const bool pieces = Gx != C;  // X3 pi not contiguous per unit: 16/8-byte cp.async pieces
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 32);  // one arrival per producer lane (after its cp.async pieces)
+      mbar_init(&empty[s], kWsCW);  // one per consumer warp
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const DIdx ix(n);
+  auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
+  const int* __restrict__ order = P.order;
+  auto tri = [&](int pos) { return order ? order[pos] : pos; };
+  // the CTA's unit sequence: blocks of K triples of one chunk, dealt round-robin
+  auto advance = [&](int& w, int& pos) {
+    ++pos;
+    if (pos >= min((w / nch + 1) * K, P.ntriples)) {
+      w += G;
+      pos = (w / nch) * K;
+    }
+  };
+
+  if (warp == kWsCW) {  // ---------------- producer warp ----------------
+    const unsigned row_bytes = (unsigned)nm2 * 8u;
+    const unsigned tx = (rows_async ? 0u : 2u * nrows * row_bytes) + (unsigned)lpairs * 8u +
+                        (pieces ? 0u : (unsigned)c3 * 8u);
+    int w = blockIdx.x, pos = (w / nch) * K;
+    for (int u = 0; w < nwork; ++u, advance(w, pos)) {
+      const int s = u % S;
+      if (u >= S) mbar_wait(&empty[s], ((u / S) - 1) & 1);
+      const int T = tri(pos), ch = w % nch, pa0 = ch * C;
+      const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+      const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
+      const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
+      const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+      double* B = sm + (size_t)s * stage_sz;
+      if (lane == 0) mbar_expect_tx_only(&full[s], tx);
+      __syncwarp();
+      if (rows_async) {  // X1 / X2 pi rows as 16-byte cp.async pieces
+        const int pr = nm2 / 2;
+        for (int v = lane; v < 2 * nrows * pr; v += 32) {
+          const int rr = v / pr, x = v - rr * pr;
+          const int arr = rr >= nrows, row = rr - arr * nrows;
+          const int pa_l = row / nm1, qi = row - pa_l * nm1, pa = pa0 + pa_l, q = qi + (qi >= pa);
+          const uint32_t off = (arr ? tb2 : tb1) + (uint32_t)lpair(pa, q) * esz + 2 * x;
+          cp_async16(B + (arr ? oP2 : 0) + row * R + 2 * x, P.piz + off);
+        }
+      } else {
+        for (int v = lane; v < 2 * nrows; v += 32) {  // X1 / X2 pi rows
+          const int arr = v >= nrows, row = v - arr * nrows;
+          const int pa_l = row / nm1, qi = row - pa_l * nm1, pa = pa0 + pa_l, q = qi + (qi >= pa);
+          const uint32_t off = (arr ? tb2 : tb1) + (uint32_t)lpair(pa, q) * esz;
+          bulk_g2s(B + (arr ? oP2 : 0) + row * R, P.piz + off, row_bytes, &full[s]);
+        }
+      }
+      if (lane == 31)
+        bulk_g2s(B + oU3, P.push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &full[s]);
+      const int g0 = pa0 / Gx;
+      const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx + (pa0 - g0 * Gx);
+      if (!pieces) {
+        if (lane == 30) bulk_g2s(B + oP3, P.x3buf + upi, (unsigned)c3 * 8u, &full[s]);
+      } else {
+        for (int e = lane; e < lpairs; e += 32) {
+          if constexpr (C == 2)
+            cp_async16(B + oP3 + e * C, P.x3buf + upi + (size_t)e * Gx);
+          else
+            cp_async8(B + oP3 + e, P.x3buf + upi + (size_t)e * Gx);
+        }
+      }
+      for (int e = lane; e < nrows; e += 32) {  // push rows of the (a,b) / (a,c) tiles
+        cp_async8(B + oU1 + e, P.push + (size_t)fab * lpairs + pa0 * nm1 + e);
+        cp_async8(B + oU2 + e, P.push + (size_t)fac * lpairs + pa0 * nm1 + e);
+      }
+      // this lane's arrival, triggered once its cp.async pieces have landed
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                       smem_u32(&full[s]))
+                   : "memory");
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const double kz = P.kz, phi = P.phi, omk = dsub(1.0, P.kz);
+  const int fast = P.fast;
+  double* __restrict__ d = P.d;
+  double* __restrict__ incz = P.incz;
+  double* __restrict__ d3 = P.d3;
+  WsCells cells;
+  int w = blockIdx.x, pos = (w / nch) * K;
+  int T = tri(pos), ch = w % nch;
+  ws_cells<C>(cells, n, ch * C, tid, R);
+  auto bases = [&](int T_, int ch_, uint32_t& tb1, uint32_t& tb2, uint32_t& tb3, size_t& ub) {
+    const int a = P.triples[3 * T_], b = P.triples[3 * T_ + 1], c = P.triples[3 * T_ + 2];
+    tb1 = (uint32_t)ix.fpair(a, b) * lpairs * esz + (uint32_t)(c - 2) * nm2;
+    tb2 = (uint32_t)ix.fpair(a, c) * lpairs * esz + (uint32_t)(b - 1) * nm2;
+    tb3 = (uint32_t)ix.fpair(b, c) * lpairs * esz + (uint32_t)a * nm2;
+    ub = ((size_t)(P.tri0 + T_) * nch + ch_) * lpairs * C;
+  };
+  // D' of this thread's cells of unit (T_, ch_) (cell pattern of ch_ in `cells`)
+  auto load_d = [&](int T_, int ch_, double (&D)[3 * kPipeSlots]) {
+    uint32_t tb1, tb2, tb3;
+    size_t ub;
+    bases(T_, ch_, tb1, tb2, tb3, ub);
+#pragma unroll
+    for (int k = 0; k < kPipeSlots; ++k) {
+      if (cells.rel[k] != 0xffffffffu) {
+        const uint32_t r = cells.rel[k] & 0x3fffffu;
+        D[k] = __ldcg(d + tb1 + r);
+        D[kPipeSlots + k] = __ldcg(d + tb2 + r);
+      }
+      if (cells.x3b[k] != 0xffffffffu) D[2 * kPipeSlots + k] = __ldcg(d3 + ub + tid + k * kWsCT);
+    }
+  };
+  auto fold = [&](int u, const double (&D)[3 * kPipeSlots]) {
+    const int s = u % S;
+    uint32_t tb1, tb2, tb3;
+    size_t ub;
+    bases(T, ch, tb1, tb2, tb3, ub);
+    mbar_wait(&full[s], (u / S) & 1);
+    const double* B = sm + (size_t)s * stage_sz;
+    const double* P1 = B;
+    const double* P2 = B + oP2;
+    const double* P3 = B + oP3;
+    const double* U1 = B + oU1;
+    const double* U2 = B + oU2;
+    const double* U3 = B + oU3;
+#pragma unroll
+    for (int k = 0; k < kPipeSlots; ++k) {  // X1 and X2 cells (rlt2.cpp:280-293)
+      if (cells.rel[k] == 0xffffffffu) continue;
+      const uint32_t r = cells.rel[k] & 0x3fffffu, jo = cells.rel[k] >> 22;
+      const uint32_t so = cells.sm[k] & 0xffffu, sp = cells.sm[k] >> 16;
+      const uint32_t l1 = cells.l12[k] & 0xffffu, l2 = cells.l12[k] >> 16;
+      {  // X1: (pb, pc) = (q, other)
+        const double p1 = P1[so], p2 = P2[sp], p3 = P3[l1];
+        const double s2 = dadd(dmul(kz, p2), U2[jo]);
+        const double s3 = dadd(dmul(kz, p3), U3[l1 / C]);
+        const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
+        d[tb1 + r] = dadd(D[k], dsub(gain, dmul(kz, p1)));
+        if (fast) incz[tb1 + r] = dadd(dmul(omk, p1), gain);
+      }
+      {  // X2: (pb, pc) = (other, q)
+        const double p2 = P2[so], p1 = P1[sp], p3 = P3[l2];
+        const double s1 = dadd(dmul(kz, p1), U1[jo]);
+        const double s3 = dadd(dmul(kz, p3), U3[l2 / C]);
+        const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
+        d[tb2 + r] = dadd(D[kPipeSlots + k], dsub(gain, dmul(kz, p2)));
+        if (fast) incz[tb2 + r] = dadd(dmul(omk, p2), gain);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPipeSlots; ++k) {  // X3 slots
+      if (cells.x3b[k] == 0xffffffffu) continue;
+      const int e = tid + k * kWsCT;
+      const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
+      const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
+      const double p3 = P3[e], p1 = P1[i1], p2 = P2[i2];
+      const double s1 = dadd(dmul(kz, p1), U1[i1 / (uint32_t)R]);
+      const double s2 = dadd(dmul(kz, p2), U2[i2 / (uint32_t)R]);
+      const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
+      const double dn = dadd(D[2 * kPipeSlots + k], dsub(gain, dmul(kz, p3)));
+      d3[ub + e] = dn;
+      const uint32_t o = tb3 + pair * esz + col;
+      if (fast)
+        incz[o] = dadd(dmul(omk, p3), gain);
+      else
+        d[o] = dn;
+    }
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
+                   : "memory");
+  };
+  // one unit: prefetch the next unit's D' (same chunk) into Dn, fold with Dc
+  int u = 0;
+  auto step = [&](const double (&Dc)[3 * kPipeSlots], double (&Dn)[3 * kPipeSlots]) {
+    int w2 = w, pos2 = pos;
+    advance(w2, pos2);
+    const bool more = w2 < nwork;
+    const int T2 = more ? tri(pos2) : 0, ch2 = w2 % nch;
+    const bool pre = more && ch2 == ch;
+    if (pre) load_d(T2, ch2, Dn);
+    fold(u, Dc);
+    if (!more) return false;
+    ++u;
+    w = w2;
+    pos = pos2;
+    T = T2;
+    if (!pre) {  // new chunk: new cell pattern, then its D'
+      ch = ch2;
+      ws_cells<C>(cells, n, ch * C, tid, R);
+      load_d(T, ch, Dn);
+    }
+    return true;
+  };
+  double DA[3 * kPipeSlots], DB[3 * kPipeSlots];
+  load_d(T, ch, DA);
+  while (step(DA, DB) && step(DB, DA)) {
+  }
+  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
+    P.sa_fac[tid] = 0.0;
+    P.sa_loc[tid] = 0.0;
+  }
+}
+
 // Phase 2, rlt2.cpp:344-381 with redistribute_family (rlt2.cpp:184-205):
 // every member's cost gets add[s] + share from its family's pi triple.
 __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
@@ -2031,6 +2324,33 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const size_t smem = fold_smem_bytes(p.m, p.chunk);
   const int n = p.m;
   const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
+  {  // warp-specialised fold (n even, chunk 1 or 2, single GPU)
+    const int C = p.chunk;
+    const int R = n, nrows = C * (n - 1), lp = n * (n - 1);
+    const size_t stage = (size_t)((2 * nrows * R + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) *
+                         sizeof(double);
+    const int S = std::min(kWsMaxStages, (int)((210 * 1024) / stage));
+    if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_WS", 1) &&
+        env_int("QAPB_FOLD_PIPE", 1) && n % 2 == 0 &&
+        (C == 1 || (C == 2 && p.x3_group % 2 == 0)) && nz < 4294967295.0 &&
+        C * (n - 1) * (n - 2) <= kPipeSlots * kWsCT && C * n * (n - 1) <= kPipeSlots * kWsCT &&
+        n < 64 && S >= 2 && (n - 2) * (n - 2) * n * (n - 1) < (1 << 22) && C * (n - 1) < 512) {
+      const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
+      const int nwork = (p.ntriples + K - 1) / K * p.nchunks;
+      const int grid = std::min(num_sms(), nwork);
+      const int St = std::max(2, std::min(S, env_int("QAPB_FOLD_WS_STAGES", S)));
+      if (C == 2) {
+        allow_max_smem(zfold_ws_kernel<2>);
+        zfold_ws_kernel<2><<<grid, kWsCT + 32, St * stage, st>>>(p, K, St,
+                                                                  env_int("QAPB_FOLD_WS_ROWS", 0));
+      } else {
+        allow_max_smem(zfold_ws_kernel<1>);
+        zfold_ws_kernel<1><<<grid, kWsCT + 32, St * stage, st>>>(p, K, St,
+                                                                  env_int("QAPB_FOLD_WS_ROWS", 0));
+      }
+      return cudaGetLastError();
+    }
+  }
   {  // pipelined bulk-staged fold (n even, chunk 1 or 2, single GPU)
     const int C = p.chunk;
     const size_t psmem = (size_t)(4 * C * (n - 1) * (n - 2) + 2 * C * n * (n - 1) +

@@ -59,10 +59,13 @@ def test_trace_bitwise(q, golden, key):
 
 
 # Fold kernel variants (kernels.cu launch_zfold): chunk 2 at n even selects the
-# pipelined bulk-staged fold; the environment switches select the others.
+# warp-specialised fold; the environment switches select the others.
 FOLD_VARIANTS = {
-    "pipe": {},
-    "pipe_chunk1": {"QAPB_FOLD_CHUNK": "1"},
+    "ws": {},
+    "ws_stages2": {"QAPB_FOLD_WS_STAGES": "2"},
+    "ws_chunk1": {"QAPB_FOLD_CHUNK": "1"},
+    "pipe": {"QAPB_FOLD_WS": "0"},
+    "pipe_chunk1": {"QAPB_FOLD_CHUNK": "1", "QAPB_FOLD_WS": "0"},
     "pipe_k1": {"QAPB_FOLD_PIPE_K": "1"},
     "pipe_blocked_order": {"QAPB_FOLD_ORDER_BLOCK": "3"},
     "bulk": {"QAPB_FOLD_PIPE": "0"},

@@ -103,3 +103,38 @@ def test_device_pointer_api(q):
     torch.cuda.synchronize()
     ref = q.solve_batch(q.LapBatch.from_costs(costs)).values
     assert (vals.cpu().numpy() == ref).all()
+
+
+def test_special_costs_and_large_m_bitwise(q):
+    """+inf, huge (|c| > 1e300), NaN and -0.0 costs (the exact safe path) and
+    m > 127 (the CTA-per-LAP path) against the reference LapSolver
+    (tests/golden/make_lap_special.py): optimum, assignment, both duals."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "lap_special.npz"))
+    oc = on = 0
+    for k, m in enumerate(z["m"]):
+        m = int(m)
+        cost = z["costs"][oc:oc + m * m].reshape(m, m)
+        r2c, u, v = z["r2c"][on:on + m], z["u"][on:on + m], z["v"][on:on + m]
+        oc += m * m
+        on += m
+        for count in (1, 3):  # a lone slot and a batch of identical slots
+            b = q.solve_batch(q.LapBatch.from_costs(np.stack([cost] * count)))
+            for s in range(count):
+                assert b.values[s].tobytes() == np.float64(z["values"][k]).tobytes(), (k, m)
+                assert (b.row_to_col[s] == r2c).all(), (k, m)
+                assert b.u[s].tobytes() == u.tobytes() and b.v[s].tobytes() == v.tobytes(), (k, m)
+
+
+def test_undefined_lap_raises(q):
+    """A row with no finite cost: LapSolver::solve reads p[-1] (lap.cpp:53,
+    undefined behaviour); the drop-in reports it instead of inventing a result."""
+    inf = np.inf
+    with pytest.raises(ValueError):
+        q.solve_lap(np.array([[inf, inf], [1.0, 2.0]]))
+    with pytest.raises(ValueError):  # the CTA-per-LAP path too
+        c = np.ones((130, 130))
+        c[5, :] = inf
+        q.solve_lap(c)
+    # the solver stays usable afterwards
+    assert q.solve_lap(np.array([[1.0, 2.0], [3.0, 0.0]])).value == 1.0
