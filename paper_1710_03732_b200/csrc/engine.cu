@@ -129,10 +129,16 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
   init_state();
   cuda_check(cudaMemcpyAsync(b_, b, nb_ * sizeof(double), cudaMemcpyDefault, st_), "H2D b");
   cuda_check(cudaMemcpyAsync(c_, c, nc_ * sizeof(double), cudaMemcpyDefault, st_), "H2D c");
-  if (d)
+  if (d && ri_) {  // reference layout in, RI layout on the device (pi(z) as scratch)
+    cuda_check(cudaMemcpyAsync(piz_, d, nd_ * sizeof(double), cudaMemcpyDefault, st_), "H2D d");
+    cuda_check(launch_z_relayout(m_, piz_, d_, 1, st_), "relayout d");
+    ++launches_;
+    cuda_check(cudaMemsetAsync(piz_, 0, nd_ * sizeof(double), st_), "memset");
+  } else if (d) {
     cuda_check(cudaMemcpyAsync(d_, d, nd_ * sizeof(double), cudaMemcpyDefault, st_), "H2D d");
-  else
+  } else {
     cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
+  }
   split_gather();
   hS_.offset = offset;
   push_scalars();
@@ -225,6 +231,18 @@ void Engine::alloc() {
     x3_ngroups_ = (range + x3_group_ - 1) / x3_group_;
     salloc(st_, &x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
     salloc(st_, &d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
+  }
+  // RI layout for the single-GPU 1-phase split engine (the warp-specialised
+  // fold + tensor-map Z-LAPs); QAPB_ZLAYOUT=0 keeps the reference tile layout
+  ri_ = world_ == 1 && split_ && split_mode_ == 2 && stage_ev_.size() == 1 &&
+        env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3_group_);
+  if (ri_) {
+    unsigned char h[3 * 128];
+    encode_z_tmap(h, d_, m);
+    if (incz_) encode_z_tmap(h + 128, incz_, m);
+    encode_z_tmap(h + 256, piz_, m);
+    dalloc(&tmaps_, sizeof h);  // cudaMalloc: 256-byte aligned
+    cuda_check(cudaMemcpy(tmaps_, h, sizeof h, cudaMemcpyHostToDevice), "H2D tensor maps");
   }
   // every rank of a sharded engine holds the same b, best and RNG stream, so
   // each runs the same SA step and the replicated state stays identical
@@ -328,6 +346,7 @@ Engine::~Engine() {
     cudaStreamSynchronize(st_);
   }
   for (auto* p : xbufs_) cudaFree(p);
+  if (tmaps_) cudaFree(tmaps_);
   if (shard_dev_) cudaFree(shard_dev_);
   if (feas_bad_) cudaFree(feas_bad_);
   if (rows_before_) cudaFree(rows_before_);
@@ -589,7 +608,7 @@ void Engine::plan_pipeline() {
 void Engine::split_gather() {
   if (!split_) return;
   cuda_check(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
-                            p_lo_, p_hi_, d_, d3_, 1, st_),
+                            p_lo_, p_hi_, d_, d3_, 1, st_, ri_ ? 1 : 0),
              "x3 gather");
   d_stale_ = false;
 }
@@ -598,7 +617,7 @@ void Engine::split_gather() {
 void Engine::split_scatter() const {
   if (!split_ || !d_stale_) return;
   cuda_check(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
-                            p_lo_, p_hi_, d_, d3_, 0, st_),
+                            p_lo_, p_hi_, d_, d3_, 0, st_, ri_ ? 1 : 0),
              "x3 scatter");
   cuda_check(cudaStreamSynchronize(st_), "x3 scatter");
   d_stale_ = false;
@@ -620,6 +639,12 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
   p.theta_ref = theta_ref ? theta_ref + t0 : nullptr;
   p.err_tile = &S_->err_tile;
   p.tile_base = t0;
+  if (ri_) {  // tiles by global index through the tensor maps
+    p.costs = costs;
+    p.pi = piz_;
+    p.tmap_cost = tmaps_ + (costs == d_ ? 0 : 128);
+    p.tmap_pi = tmaps_ + 256;
+  }
   if (split_) {  // X3 split (FoldParams::x3buf)
     p.x3buf = x3buf_;
     p.costs_w = costs + (size_t)t0 * esz;
@@ -660,6 +685,7 @@ FoldParams Engine::fold_params(int stage) const {
     f.x3_ngroups = x3_ngroups_;
   }
   if (f.tri0 == 0 && f.ntriples == ntriples_) f.order = order_;
+  f.ri = ri_ ? 1 : 0;
   return f;
 }
 
@@ -779,6 +805,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   xs.feas_bad = feas_bad_;
   xs.zp_lo = p_lo_;
   xs.zp_hi = p_hi_;
+  xs.ri = ri_ ? 1 : 0;
   kbegin(QAPB_K_XSTAGE, st_);
   cuda_check(launch_xstage(xs, st_), "x-stage");
   if (world_ > 1)  // feasibility needs every rank's pi(z) tiles
@@ -1035,6 +1062,18 @@ void Engine::get_array(int which, double* dst, size_t count) const {
     case QAPB_ARR_INCZ: src = incz_; break;
   }
   // dst may be host or device memory (device snapshots, store.cu)
+  if (n && ri_ && (which == QAPB_ARR_PI_Z || which == QAPB_ARR_STORE_D || which == QAPB_ARR_INCZ)) {
+    // back to the reference layout (StoreIndex) on the way out
+    cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+    double* tmp = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(double), st_),
+               "cudaMallocAsync");
+    cuda_check(launch_z_relayout(m_, src, tmp, 0, st_), "relayout");
+    cuda_check(cudaMemcpyAsync(dst, tmp, n * sizeof(double), cudaMemcpyDefault, st_), "D2H array");
+    cuda_check(cudaFreeAsync(tmp, st_), "cudaFreeAsync");
+    cuda_check(cudaStreamSynchronize(st_), "D2H array");
+    return;
+  }
   if (n) cuda_check(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault), "D2H array");
 }
 

@@ -126,6 +126,10 @@ class Engine {
   void split_scatter() const;
   bool split_ = false;
   int split_mode_ = 0;
+  // z arrays in the row-interleaved layout (kernels.h z_ri_offset); Z-LAP
+  // tiles move by 3-D TMA tensor copies: tmaps_ = {d, incz, pi(z)} maps
+  bool ri_ = false;
+  unsigned char* tmaps_ = nullptr;
   bool cost_scatter_ = false;  // sharded: scatter remote X3 costs before the Z-LAPs
   int x3_group_ = 0, x3_ngroups_ = 0;
   mutable bool d_stale_ = false;

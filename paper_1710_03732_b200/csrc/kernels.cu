@@ -11,6 +11,12 @@
 // contiguous.  See DESIGN.md for the roofline of each kernel.
 #include <climits>
 #include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdlib>
 #include <mutex>
 #include <set>
@@ -1107,7 +1113,7 @@ struct WsCells {
   uint32_t x3a[kPipeSlots], x3b[kPipeSlots];
 };
 
-template <int C>
+template <int C, bool RI>
 __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, int R) {
   const int nm1 = n - 1, nm2 = n - 2;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
@@ -1124,7 +1130,9 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
       const int pa = pa0 + pa_l, q = qi + (qi >= pa);
       const int other = skip2(r, min(pa, q), max(pa, q));
       const int jo = pa_l * nm1 + other - (other > pa);
-      w.rel[k] = ((uint32_t)lpair(pa, q) * esz + r) | ((uint32_t)jo << 22);
+      // offset of the cell from the unit's X1 / X2 base: its tile's row (tile
+      // layout), or simply e (RI: the unit's rows are one contiguous block)
+      w.rel[k] = (RI ? (uint32_t)e : ((uint32_t)lpair(pa, q) * esz + r)) | ((uint32_t)jo << 22);
       w.sm[k] = (uint32_t)((pa_l * nm1 + qi) * R + r) |
                 ((uint32_t)(jo * R + colskip(q, pa, other)) << 16);
       w.l12[k] = (uint32_t)(lpair(q, other) * C + pa_l) |
@@ -1146,23 +1154,30 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
   }
 }
 
-template <int C>
+template <int C, bool RI, bool DSM>
 __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, int K, int S,
-                                                                 int rows_async) {
+                                                                 int rows_async, int R,
+                                                                 int skip_x3w) {
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
   const int n = P.m, nm1 = n - 1, nm2 = n - 2;
   const int lpairs = n * nm1;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
-  const int R = n;  // smem row pitch: nm2 + 2 doubles
+  // R = smem row pitch: nm2 + 2 (rows copied one by one; 2-way bank conflicts
+  // on the transposed partner reads) or nm2 (RI: one copy per unit and array)
   const int nch = P.nchunks;
   const int nrows = C * nm1, nrows_p = (nrows + 1) & ~1;
+  const uint32_t pstride = RI ? (uint32_t)nm2 : esz;  // tile -> tile along lp, same row
   const int c3 = lpairs * C;
   // stage: P1 rows | P2 rows | P3 (fold order) | U1 | U2 | U3 (all 16-byte aligned)
   const int oP2 = nrows * R, oP3 = 2 * nrows * R, oU1 = oP3 + c3, oU2 = oU1 + nrows_p,
             oU3 = oU2 + nrows_p;
-  const int stage_sz = (oU3 + lpairs + 15) & ~15;
+  // DSM (RI only): the unit's D' blocks (X1 / X2 rows, d3) staged too, dense
+  const int c12 = C * nm1 * nm2;
+  const int oV1 = (oU3 + lpairs + 15) & ~15, oV2 = oV1 + ((c12 + 15) & ~15),
+            oV3 = oV2 + ((c12 + 15) & ~15);
+  const int stage_sz = DSM ? (oV3 + c3 + 15) & ~15 : (oU3 + lpairs + 15) & ~15;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = (P.ntriples + K - 1) / K, nwork = nblk * nch, G = gridDim.x;
   if ((int)blockIdx.x >= nwork) return;
@@ -1192,7 +1207,8 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   if (warp == kWsCW) {  // ---------------- producer warp ----------------
     const unsigned row_bytes = (unsigned)nm2 * 8u;
     const unsigned tx = (rows_async ? 0u : 2u * nrows * row_bytes) + (unsigned)lpairs * 8u +
-                        (pieces ? 0u : (unsigned)c3 * 8u);
+                        (pieces ? 0u : (unsigned)c3 * 8u) +
+                        (DSM ? (unsigned)(2 * c12 + c3) * 8u : 0u);
     int w = blockIdx.x, pos = (w / nch) * K;
     for (int u = 0; w < nwork; ++u, advance(w, pos)) {
       const int s = u % S;
@@ -1200,30 +1216,45 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       const int T = tri(pos), ch = w % nch, pa0 = ch * C;
       const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
       const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
-      const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
-      const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+      // the unit's first X1 / X2 row (location pair (pa0, ...))
+      const uint32_t tb1 = RI ? ((uint32_t)(fab * nm2 + c - 2) * lpairs + pa0 * nm1) * nm2
+                              : (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2 +
+                                    (uint32_t)(pa0 * nm1) * esz;
+      const uint32_t tb2 = RI ? ((uint32_t)(fac * nm2 + b - 1) * lpairs + pa0 * nm1) * nm2
+                              : (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2 +
+                                    (uint32_t)(pa0 * nm1) * esz;
       double* B = sm + (size_t)s * stage_sz;
       if (lane == 0) mbar_expect_tx_only(&full[s], tx);
       __syncwarp();
-      if (rows_async) {  // X1 / X2 pi rows as 16-byte cp.async pieces
+      // X1 / X2 pi rows: row `row` (= (pa_l, qi) = location pair lpair(pa0,..) + row)
+      // sits at tb + row * pstride
+      if (RI && R == nm2) {  // one copy per array: the unit's rows are contiguous
+        if (lane == 0) bulk_g2s(B, P.piz + tb1, (unsigned)nrows * row_bytes, &full[s]);
+        if (lane == 1) bulk_g2s(B + oP2, P.piz + tb2, (unsigned)nrows * row_bytes, &full[s]);
+      } else if (rows_async) {  // 16-byte cp.async pieces
         const int pr = nm2 / 2;
         for (int v = lane; v < 2 * nrows * pr; v += 32) {
           const int rr = v / pr, x = v - rr * pr;
           const int arr = rr >= nrows, row = rr - arr * nrows;
-          const int pa_l = row / nm1, qi = row - pa_l * nm1, pa = pa0 + pa_l, q = qi + (qi >= pa);
-          const uint32_t off = (arr ? tb2 : tb1) + (uint32_t)lpair(pa, q) * esz + 2 * x;
+          const uint32_t off = (arr ? tb2 : tb1) + (uint32_t)row * pstride + 2 * x;
           cp_async16(B + (arr ? oP2 : 0) + row * R + 2 * x, P.piz + off);
         }
       } else {
-        for (int v = lane; v < 2 * nrows; v += 32) {  // X1 / X2 pi rows
+        for (int v = lane; v < 2 * nrows; v += 32) {
           const int arr = v >= nrows, row = v - arr * nrows;
-          const int pa_l = row / nm1, qi = row - pa_l * nm1, pa = pa0 + pa_l, q = qi + (qi >= pa);
-          const uint32_t off = (arr ? tb2 : tb1) + (uint32_t)lpair(pa, q) * esz;
+          const uint32_t off = (arr ? tb2 : tb1) + (uint32_t)row * pstride;
           bulk_g2s(B + (arr ? oP2 : 0) + row * R, P.piz + off, row_bytes, &full[s]);
         }
       }
       if (lane == 31)
         bulk_g2s(B + oU3, P.push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &full[s]);
+      if constexpr (DSM) {  // D' of the unit: X1 / X2 row blocks and its d3 block
+        if (lane == 29) bulk_g2s(B + oV1, P.d + tb1, (unsigned)c12 * 8u, &full[s]);
+        if (lane == 28) bulk_g2s(B + oV2, P.d + tb2, (unsigned)c12 * 8u, &full[s]);
+        if (lane == 27)
+          bulk_g2s(B + oV3, P.d3 + ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C,
+                   (unsigned)c3 * 8u, &full[s]);
+      }
       const int g0 = pa0 / Gx;
       const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx + (pa0 - g0 * Gx);
       if (!pieces) {
@@ -1257,16 +1288,26 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   WsCells cells;
   int w = blockIdx.x, pos = (w / nch) * K;
   int T = tri(pos), ch = w % nch;
-  ws_cells<C>(cells, n, ch * C, tid, R);
+  ws_cells<C, RI>(cells, n, ch * C, tid, R);
+  // X1 / X2: base of the unit's rows (RI) or of its tiles' rows (cells add the
+  // tile offset); X3: row a of the (b,c) tiles, + pair * pstride + col
   auto bases = [&](int T_, int ch_, uint32_t& tb1, uint32_t& tb2, uint32_t& tb3, size_t& ub) {
     const int a = P.triples[3 * T_], b = P.triples[3 * T_ + 1], c = P.triples[3 * T_ + 2];
-    tb1 = (uint32_t)ix.fpair(a, b) * lpairs * esz + (uint32_t)(c - 2) * nm2;
-    tb2 = (uint32_t)ix.fpair(a, c) * lpairs * esz + (uint32_t)(b - 1) * nm2;
-    tb3 = (uint32_t)ix.fpair(b, c) * lpairs * esz + (uint32_t)a * nm2;
+    const int pa0 = ch_ * C;
+    if (RI) {
+      tb1 = ((uint32_t)(ix.fpair(a, b) * nm2 + c - 2) * lpairs + pa0 * nm1) * nm2;
+      tb2 = ((uint32_t)(ix.fpair(a, c) * nm2 + b - 1) * lpairs + pa0 * nm1) * nm2;
+      tb3 = (uint32_t)(ix.fpair(b, c) * nm2 + a) * lpairs * nm2;
+    } else {
+      tb1 = (uint32_t)ix.fpair(a, b) * lpairs * esz + (uint32_t)(c - 2) * nm2;
+      tb2 = (uint32_t)ix.fpair(a, c) * lpairs * esz + (uint32_t)(b - 1) * nm2;
+      tb3 = (uint32_t)ix.fpair(b, c) * lpairs * esz + (uint32_t)a * nm2;
+    }
     ub = ((size_t)(P.tri0 + T_) * nch + ch_) * lpairs * C;
   };
   // D' of this thread's cells of unit (T_, ch_) (cell pattern of ch_ in `cells`)
   auto load_d = [&](int T_, int ch_, double (&D)[3 * kPipeSlots]) {
+    if constexpr (DSM) return;  // D' arrives with the stage
     uint32_t tb1, tb2, tb3;
     size_t ub;
     bases(T_, ch_, tb1, tb2, tb3, ub);
@@ -1274,10 +1315,10 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     for (int k = 0; k < kPipeSlots; ++k) {
       if (cells.rel[k] != 0xffffffffu) {
         const uint32_t r = cells.rel[k] & 0x3fffffu;
-        D[k] = __ldcg(d + tb1 + r);
-        D[kPipeSlots + k] = __ldcg(d + tb2 + r);
+        D[k] = d[tb1 + r];
+        D[kPipeSlots + k] = d[tb2 + r];
       }
-      if (cells.x3b[k] != 0xffffffffu) D[2 * kPipeSlots + k] = __ldcg(d3 + ub + tid + k * kWsCT);
+      if (cells.x3b[k] != 0xffffffffu) D[2 * kPipeSlots + k] = d3[ub + tid + k * kWsCT];
     }
   };
   auto fold = [&](int u, const double (&D)[3 * kPipeSlots]) {
@@ -1293,6 +1334,9 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     const double* U1 = B + oU1;
     const double* U2 = B + oU2;
     const double* U3 = B + oU3;
+    const double* V1 = B + oV1;
+    const double* V2 = B + oV2;
+    const double* V3 = B + oV3;
 #pragma unroll
     for (int k = 0; k < kPipeSlots; ++k) {  // X1 and X2 cells (rlt2.cpp:280-293)
       if (cells.rel[k] == 0xffffffffu) continue;
@@ -1304,7 +1348,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         const double s2 = dadd(dmul(kz, p2), U2[jo]);
         const double s3 = dadd(dmul(kz, p3), U3[l1 / C]);
         const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
-        d[tb1 + r] = dadd(D[k], dsub(gain, dmul(kz, p1)));
+        d[tb1 + r] = dadd(DSM ? V1[r] : D[k], dsub(gain, dmul(kz, p1)));
         if (fast) incz[tb1 + r] = dadd(dmul(omk, p1), gain);
       }
       {  // X2: (pb, pc) = (other, q)
@@ -1312,7 +1356,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         const double s1 = dadd(dmul(kz, p1), U1[jo]);
         const double s3 = dadd(dmul(kz, p3), U3[l2 / C]);
         const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
-        d[tb2 + r] = dadd(D[kPipeSlots + k], dsub(gain, dmul(kz, p2)));
+        d[tb2 + r] = dadd(DSM ? V2[r] : D[kPipeSlots + k], dsub(gain, dmul(kz, p2)));
         if (fast) incz[tb2 + r] = dadd(dmul(omk, p2), gain);
       }
     }
@@ -1326,9 +1370,10 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       const double s1 = dadd(dmul(kz, p1), U1[i1 / (uint32_t)R]);
       const double s2 = dadd(dmul(kz, p2), U2[i2 / (uint32_t)R]);
       const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
-      const double dn = dadd(D[2 * kPipeSlots + k], dsub(gain, dmul(kz, p3)));
+      const double dn = dadd(DSM ? V3[e] : D[2 * kPipeSlots + k], dsub(gain, dmul(kz, p3)));
       d3[ub + e] = dn;
-      const uint32_t o = tb3 + pair * esz + col;
+      const uint32_t o = tb3 + pair * pstride + col;
+      if (skip_x3w) continue;  // timing experiment only (wrong results)
       if (fast)
         incz[o] = dadd(dmul(omk, p3), gain);
       else
@@ -1356,7 +1401,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     T = T2;
     if (!pre) {  // new chunk: new cell pattern, then its D'
       ch = ch2;
-      ws_cells<C>(cells, n, ch * C, tid, R);
+      ws_cells<C, RI>(cells, n, ch * C, tid, R);
       load_d(T, ch, Dn);
     }
     return true;
@@ -1530,11 +1575,17 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
   auto gtile = [&](int t) {  // launch tile -> global tile (run mapping, multi-GPU)
     return P.run_len ? (t / P.run_len) * P.run_stride + P.run_off + t % P.run_len : t;
   };
+  const int nm2 = m, lpairs = (m + 2) * (m + 1);
   auto issue = [&](double* dst, int tile, uint64_t* b) {  // lane 0 only
     if (store_bulk) bulk_wait_read0();  // the previous pi store has left dst
     fence_proxy_async();
     mbar_expect_tx(b, bytes);
-    bulk_g2s(dst, P.costs + (size_t)gtile(tile) * esz, bytes, b);
+    if (P.tmap_cost) {  // RI layout: the tile's rows through the 3-D tensor map
+      const int g = P.tile_base + gtile(tile), f = g / lpairs;
+      tma_load_3d(dst, P.tmap_cost, 0, g - f * lpairs, f * nm2, b);
+    } else {
+      bulk_g2s(dst, P.costs + (size_t)gtile(tile) * esz, bytes, b);
+    }
   };
   if (use_bulk && lane == 0) {
     mbar_init(&bar[0], 1);
@@ -1634,7 +1685,12 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
         fence_proxy_async();  // this lane's generic writes -> the async proxy
         __syncwarp();
         if (lane == 0) {
-          bulk_s2g(out, cb, bytes);
+          if (P.tmap_pi) {
+            const int g = P.tile_base + tg, f = g / lpairs;
+            tma_store_3d(P.tmap_pi, 0, g - f * lpairs, f * nm2, cb);
+          } else {
+            bulk_s2g(out, cb, bytes);
+          }
           bulk_commit();
         }
       } else {
@@ -1887,7 +1943,10 @@ __global__ void __launch_bounds__(1024) xstage_kernel(XStageParams P) {
       if (!(i < j) || k == i || k == j) continue;
       if (sx[i] < P.zp_lo || sx[i] >= P.zp_hi) continue;  // tile held by another rank
       const int t = ix.tile(i, j, sx[i], sx[j]);
-      if (P.piz[(size_t)t * esz + ix.cell(i, j, sx[i], sx[j], k, sx[k])] > tol) feas_bad = 1;
+      const int cl = ix.cell(i, j, sx[i], sx[j], k, sx[k]);
+      const size_t o = P.ri ? z_ri_offset(m, (size_t)t, cl / (m - 2), cl % (m - 2))
+                            : (size_t)t * esz + cl;
+      if (P.piz[o] > tol) feas_bad = 1;
     }
   }
   __syncthreads();
@@ -1949,7 +2008,7 @@ __global__ void xfinish_kernel(XStageParams P) {
 // rank's local split cells (the whole range on one GPU).
 __global__ void x3_sync_kernel(int n, int C, int nch, const int* __restrict__ triples,
                                int p_lo, int p_hi, double* __restrict__ d,
-                               double* __restrict__ d3, size_t total, int to_d3) {
+                               double* __restrict__ d3, size_t total, int to_d3, int ri) {
   const int nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
   const size_t esz = (size_t)nm2 * nm2;
   const DIdx ix(n);
@@ -1962,11 +2021,35 @@ __global__ void x3_sync_kernel(int n, int C, int nch, const int* __restrict__ tr
     if (pa >= p_hi || pa == pb || pa == pc || pb < p_lo || pb >= p_hi) continue;
     const int a = triples[3 * T], b = triples[3 * T + 1], c = triples[3 * T + 2];
     const int lo = min(pb, pc), hi = max(pb, pc), col = pa - (pa > lo) - (pa > hi);
-    const size_t g = ((size_t)ix.fpair(b, c) * lpairs + pair) * esz + (size_t)a * nm2 + col;
+    const size_t t = (size_t)ix.fpair(b, c) * lpairs + pair;
+    const size_t g = ri ? z_ri_offset(n, t, a, col) : t * esz + (size_t)a * nm2 + col;
     if (to_d3)
       d3[i] = d[g];
     else
       d[g] = d3[i];
+  }
+}
+
+// z array layout conversion (kernels.h z_ri_offset): thread per element,
+// consecutive threads take consecutive columns of one row on both sides.
+__global__ void z_relayout_kernel(int n, const double* __restrict__ src, double* __restrict__ dst,
+                                  size_t total, int to_ri) {
+  const int nm2 = n - 2;
+  const size_t esz = (size_t)nm2 * nm2;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    // i enumerates the RI layout: ((f*nm2 + k)*lpairs + lp)*nm2 + r
+    const size_t lpairs = (size_t)n * (n - 1);
+    const int r = (int)(i % nm2);
+    const size_t q = i / nm2;
+    const size_t lp = q % lpairs, fk = q / lpairs;
+    const size_t f = fk / nm2;
+    const int k = (int)(fk - f * nm2);
+    const size_t g = (f * lpairs + lp) * esz + (size_t)k * nm2 + r;  // reference layout
+    if (to_ri)
+      dst[i] = src[g];
+    else
+      dst[g] = src[i];
   }
 }
 
@@ -2326,27 +2409,37 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
   {  // warp-specialised fold (n even, chunk 1 or 2, single GPU)
     const int C = p.chunk;
-    const int R = n, nrows = C * (n - 1), lp = n * (n - 1);
-    const size_t stage = (size_t)((2 * nrows * R + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) *
-                         sizeof(double);
+    const bool dense = p.ri && env_int("QAPB_FOLD_WS_DENSE", 0);
+    const bool dsm = p.ri && env_int("QAPB_FOLD_WS_DSM", 1);
+    const int R = dense ? n - 2 : n, nrows = C * (n - 1), lp = n * (n - 1);
+    const int c12p = (C * (n - 1) * (n - 2) + 15) & ~15;
+    const size_t stage =
+        (size_t)((((2 * nrows * R + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) +
+                  (dsm ? 2 * c12p + lp * C : 0) + 15) & ~15) * sizeof(double);
     const int S = std::min(kWsMaxStages, (int)((210 * 1024) / stage));
-    if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_WS", 1) &&
-        env_int("QAPB_FOLD_PIPE", 1) && n % 2 == 0 &&
+    if (p.x3buf && p.x3mode == 2 && !p.shard &&
+        (p.ri || (env_int("QAPB_FOLD_WS", 0) && env_int("QAPB_FOLD_PIPE", 1))) && n % 2 == 0 &&
         (C == 1 || (C == 2 && p.x3_group % 2 == 0)) && nz < 4294967295.0 &&
         C * (n - 1) * (n - 2) <= kPipeSlots * kWsCT && C * n * (n - 1) <= kPipeSlots * kWsCT &&
         n < 64 && S >= 2 && (n - 2) * (n - 2) * n * (n - 1) < (1 << 22) && C * (n - 1) < 512) {
       const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
       const int nwork = (p.ntriples + K - 1) / K * p.nchunks;
       const int grid = std::min(num_sms(), nwork);
-      const int St = std::max(2, std::min(S, env_int("QAPB_FOLD_WS_STAGES", S)));
+      // measured at n=30 (RI): two stages beat three and four; with D' staged,
+      // 16-byte cp.async rows beat TMA bulk row copies (2.18 vs 2.41 ms)
+      const int St = std::max(2, std::min(S, env_int("QAPB_FOLD_WS_STAGES", 2)));
+      const int ra = env_int("QAPB_FOLD_WS_ROWS", dsm ? 1 : 0);
+      auto go = [&](auto kern) {
+        allow_max_smem(kern);
+        kern<<<grid, kWsCT + 32, St * stage, st>>>(p, K, St, ra, R,
+                                                   env_int("QAPB_FOLD_SKIP_X3W", 0));
+      };
       if (C == 2) {
-        allow_max_smem(zfold_ws_kernel<2>);
-        zfold_ws_kernel<2><<<grid, kWsCT + 32, St * stage, st>>>(p, K, St,
-                                                                  env_int("QAPB_FOLD_WS_ROWS", 0));
+        if (dsm) go(zfold_ws_kernel<2, true, true>);
+        else p.ri ? go(zfold_ws_kernel<2, true, false>) : go(zfold_ws_kernel<2, false, false>);
       } else {
-        allow_max_smem(zfold_ws_kernel<1>);
-        zfold_ws_kernel<1><<<grid, kWsCT + 32, St * stage, st>>>(p, K, St,
-                                                                  env_int("QAPB_FOLD_WS_ROWS", 0));
+        if (dsm) go(zfold_ws_kernel<1, true, true>);
+        else p.ri ? go(zfold_ws_kernel<1, true, false>) : go(zfold_ws_kernel<1, false, false>);
       }
       return cudaGetLastError();
     }
@@ -2423,6 +2516,8 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const bool aligned = (((uintptr_t)p.costs) & 15) == 0;
   const bool use_bulk = (tile_bytes % 16 == 0) && aligned;
   const bool store_bulk = use_bulk && p.pi && (((uintptr_t)p.pi) & 15) == 0;
+  if ((p.tmap_cost || p.tmap_pi) && (!use_bulk || !store_bulk || p.sh || !p.x3buf || p.patch))
+    return cudaErrorInvalidValue;  // the RI path is the single-GPU split Z stage only
   const size_t buf_elems = align_up(esz, 16);  // 128-byte aligned buffers
   // tile buffers per warp: 1 (more resident warps) unless QAPB_LAP_NBUF=2
   int nbuf = use_bulk ? std::max(1, std::min(2, env_int("QAPB_LAP_NBUF", 1))) : 1;
@@ -2515,10 +2610,11 @@ cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
-                           int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st) {
+                           int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st,
+                           int ri) {
   const size_t total = (size_t)ntriples * nchunks * n * (n - 1) * chunk;
   x3_sync_kernel<<<4 * num_sms(), 256, 0, st>>>(n, chunk, nchunks, triples, p_lo, p_hi, d, d3,
-                                                total, to_d3);
+                                                total, to_d3, ri);
   return cudaGetLastError();
 }
 
@@ -2526,6 +2622,65 @@ cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaStat
                              double* sa_fac, double* sa_loc, cudaStream_t stream) {
   if (p.m > 128) return cudaErrorInvalidValue;
   sa_device_kernel<<<1, 32, 0, stream>>>(p, b, S, st, sa_fac, sa_loc);
+  return cudaGetLastError();
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+}  // namespace
+
+// 3-D view of an RI z array (z_ri_offset): dim 0 = column r (n-2), dim 1 =
+// location pair lp (lpairs), dim 2 = facility pair x row (fpairs*(n-2));
+// box {n-2, 1, n-2} = one Z-LAP tile, landing row-major in shared memory.
+void encode_z_tmap(void* out128, const double* base, int n) {
+  auto fn = tmap_encoder();
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled is not available");
+  const cuuint64_t nm2 = (cuuint64_t)(n - 2), lp = (cuuint64_t)n * (n - 1),
+                   fp = (cuuint64_t)n * (n - 1) / 2;
+  const cuuint64_t dims[3] = {nm2, lp, fp * nm2};
+  const cuuint64_t strides[2] = {nm2 * 8, lp * nm2 * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)nm2, 1, (cuuint32_t)nm2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  std::memcpy(out128, &m, sizeof m);
+}
+
+bool ri_supported(int n, int chunk, int x3_group) {
+  if (n % 2 || n >= 64 || n < 4) return false;
+  if (!(chunk == 1 || (chunk == 2 && x3_group % 2 == 0))) return false;
+  const double nz = (double)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
+  if (nz >= 4294967295.0) return false;
+  const int C = chunk, nrows = C * (n - 1), lp = n * (n - 1);
+  if (C * (n - 1) * (n - 2) > kPipeSlots * kWsCT || C * lp > kPipeSlots * kWsCT) return false;
+  if ((n - 2) * (n - 2) * lp >= (1 << 22) || nrows >= 512) return false;
+  const size_t stage =
+      (size_t)((2 * nrows * n + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) * sizeof(double);
+  if ((210 * 1024) / stage < 2) return false;
+  return tmap_encoder() != nullptr;
+}
+
+cudaError_t launch_z_relayout(int n, const double* src, double* dst, int to_ri, cudaStream_t st) {
+  const size_t total = (size_t)n * (n - 1) / 2 * n * (n - 1) * (n - 2) * (n - 2);
+  z_relayout_kernel<<<8 * num_sms(), 256, 0, st>>>(n, src, dst, total, to_ri);
   return cudaGetLastError();
 }
 

@@ -74,6 +74,11 @@ struct BatchLapParams {
   double* x3buf;
   double* costs_w;
   int x3_group, x3_ngroups;
+  // RI layout (z_ri_offset): tiles move by 3-D TMA tensor copies through
+  // these tensor maps (device memory, 64-byte aligned CUtensorMap; costs and
+  // pi are then base pointers and tile_base + t the global tile index)
+  const void* tmap_cost;
+  const void* tmap_pi;
 };
 
 constexpr int kMaxRanks = 8;
@@ -156,7 +161,26 @@ struct FoldParams {
   // of 0..ntriples-1 in blocks of a, b and c for DRAM row locality); null =
   // lexicographic.  Only the processing order changes, never a buffer index.
   const int* order;
+  // z arrays (d, piz, incz) in the row-interleaved device layout (see
+  // z_ri_offset below) instead of the reference tile layout
+  int ri;
 };
+
+// Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
+// single-GPU 1-phase engine: element (tile t = f*lpairs + lp, row k, col r)
+// of the reference layout (StoreIndex, rlt2.hpp:43-52) lives at
+//   ((f*(n-2) + k)*lpairs + lp)*(n-2) + r,
+// i.e. row k of all lpairs tiles of facility pair f is one contiguous block.
+// The fold's X1 / X2 rows of a unit (row c or b of 2(n-1) consecutive tiles)
+// are then one contiguous 13 KB run instead of 224-byte pieces 6 KB apart
+// (tools/layout_probe.cu: 3.4 vs 4.9+ TB/s for the same bytes), and a Z-LAP
+// tile is one 3-D TMA tensor copy whose rows, across the warps working on
+// consecutive tiles, are again contiguous in DRAM.
+__host__ __device__ inline size_t z_ri_offset(int n, size_t t, int k, int r) {
+  const size_t lpairs = (size_t)n * (n - 1), nm2 = (size_t)(n - 2);
+  const size_t f = t / lpairs, lp = t - f * lpairs;
+  return ((f * nm2 + k) * lpairs + lp) * nm2 + r;
+}
 
 struct XYFoldParams {
   int m;
@@ -204,6 +228,7 @@ struct XStageParams {
   int es_window, iter_limit;
   int* feas_bad;           // device flag: 1 if any induced slack > 1e-7
   int zp_lo, zp_hi;        // first locations of the pi(z) tiles this rank checks
+  int ri;                  // pi(z) in the RI layout (z_ri_offset)
 };
 
 // ---- launches (all asynchronous on `st`) ----
@@ -217,10 +242,19 @@ cudaError_t launch_lap_batch(const BatchLapParams& p, cudaStream_t st);
 cudaError_t launch_ystage(const YStageParams& p, cudaStream_t st);
 cudaError_t launch_xstage(const XStageParams& p, cudaStream_t st);
 cudaError_t launch_xfinish(const XStageParams& p, cudaStream_t st);
+// z array layout conversion: reference tile layout <-> RI (to_ri = 1: src is
+// in the reference layout).  Out of place.
+cudaError_t launch_z_relayout(int n, const double* src, double* dst, int to_ri, cudaStream_t st);
+// The RI path's kernels exist for this (n, fold chunk, x3 group): even n, the
+// warp-specialised fold, TMA tensor maps available.
+bool ri_supported(int n, int chunk, int x3_group);
+// CUtensorMap (128 bytes) of an RI z array for the Z-LAP tile copies
+void encode_z_tmap(void* out128, const double* base, int n);
 // theta of every rank's tile runs <-> one contiguous buffer (rank segments)
 // single-GPU X3 split: D' of the X3 members, tile layout <-> fold order
 cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
-                           int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st);
+                           int p_lo, int p_hi, double* d, double* d3, int to_d3, cudaStream_t st,
+                           int ri = 0);
 // one SA step on the device after an iteration (no-op unless that iteration's
 // X stage ran, when a certificate exists, or when best <= 0)
 cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,
