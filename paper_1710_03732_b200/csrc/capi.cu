@@ -71,38 +71,9 @@ void need(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
 }
 
-// ---- host-side store helpers (reference API, not on the hot path) -------
-struct HIdx {  // StoreIndex, rlt2.hpp:25-69
-  int m, lpairs, esz;
-  explicit HIdx(int m_) : m(m_), lpairs(m_ * (m_ - 1)), esz((m_ - 2) * (m_ - 2)) {}
-  int fpair(int i, int j) const { return i * m - i * (i + 1) / 2 + (j - i - 1); }
-  int lpair(int p, int q) const { return p * (m - 1) + q - (q > p); }
-  int tile(int i, int j, int p, int q) const { return fpair(i, j) * lpairs + lpair(p, q); }
-  int cell(int i, int j, int p, int q, int k, int r) const {
-    const int kl = k - (k > i) - (k > j);
-    const int lo = p < q ? p : q, hi = p < q ? q : p;
-    return kl * (m - 2) + (r - (r > lo) - (r > hi));
-  }
-  void uncell(int i, int j, int p, int q, int c, int* k, int* r) const {
-    int kk = c / (m - 2), rr = c % (m - 2);
-    if (kk >= i) ++kk;
-    if (kk >= j) ++kk;
-    const int lo = p < q ? p : q, hi = p < q ? q : p;
-    if (rr >= lo) ++rr;
-    if (rr >= hi) ++rr;
-    *k = kk;
-    *r = rr;
-  }
-  size_t cidx(int i, int p, int j, int q) const {
-    return ((size_t)i * m + p) * (m - 1) * (m - 1) + (size_t)(j - (j > i)) * (m - 1) +
-           (q - (q > p));
-  }
-  int tiles() const { return (m * (m - 1) / 2) * lpairs; }
-};
-
 size_t nb_of(int m) { return (size_t)m * m; }
 size_t nc_of(int m) { return (size_t)m * m * (m - 1) * (m - 1); }
-size_t nd_of(int m) { return m >= 3 ? (size_t)HIdx(m).tiles() * (m - 2) * (m - 2) : 0; }
+size_t nd_of(int m) { return store_nd(m); }
 }  // namespace
 
 namespace {
@@ -283,134 +254,65 @@ QAPB_API qapb_status qapb_init_coefficients(int n, const double* flow, const dou
   });
 }
 
-// store_evaluate, rlt2.cpp:91-107 (host, O(n^3): an exactness oracle of the API)
+// The reference's store helpers (store_evaluate, collapse_store,
+// redistribute_family) run on the device (store.cu); host arrays are staged
+// into a temporary device store on the calling thread's current device.
+namespace {
+int current_device() {
+  int dev = 0;
+  qapb::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  return dev;
+}
+std::unique_ptr<DeviceStore> stage_store(int m, const double* b, const double* c, const double* d,
+                                         double offset) {
+  auto s = std::make_unique<DeviceStore>(m, current_device());
+  qapb::cuda_check(cudaMemcpyAsync(s->b, b, store_nb(m) * 8, cudaMemcpyDefault, s->stream), "H2D b");
+  qapb::cuda_check(cudaMemcpyAsync(s->c, c, store_nc(m) * 8, cudaMemcpyDefault, s->stream), "H2D c");
+  if (m >= 3 && d)
+    qapb::cuda_check(cudaMemcpyAsync(s->d, d, store_nd(m) * 8, cudaMemcpyDefault, s->stream),
+                     "H2D d");
+  else if (m >= 3)
+    qapb::cuda_check(cudaMemsetAsync(s->d, 0, store_nd(m) * 8, s->stream), "memset d");
+  s->offset = offset;
+  return s;
+}
+}  // namespace
+
+// store_evaluate, rlt2.cpp:91-107 (device, qapb::store_evaluate_device)
 QAPB_API qapb_status qapb_store_evaluate(int m, const double* b, const double* c,
                                          const double* d, double offset, const int* perm,
                                          double* value) {
   return guard([&] {
     need(m >= 3, "store_evaluate: m >= 3 required");
-    HIdx ix(m);
-    double v = offset;
-    for (int i = 0; i < m; ++i) v += b[(size_t)i * m + perm[i]];
-    for (int i = 0; i < m; ++i)
-      for (int j = 0; j < m; ++j)
-        if (j != i) v += c[ix.cidx(i, perm[i], j, perm[j])];
-    for (int i = 0; i < m; ++i)
-      for (int j = i + 1; j < m; ++j) {
-        const double* tl = d + (size_t)ix.tile(i, j, perm[i], perm[j]) * ix.esz;
-        for (int k = 0; k < m; ++k)
-          if (k != i && k != j) v += tl[ix.cell(i, j, perm[i], perm[j], k, perm[k])];
-      }
-    *value = v;
+    auto s = stage_store(m, b, c, d, offset);
+    *value = qapb::store_evaluate_device(*s, perm);
   });
 }
 
-// collapse_store, rlt2.cpp:109-182 (host; the device version is SURVEY §8f #1)
+// collapse_store, rlt2.cpp:109-182 (device, qapb::collapse_store_device)
 QAPB_API qapb_status qapb_collapse_store(int m, const double* b, const double* c,
                                          const double* d, double offset, int fac, int loc,
                                          double* ob, double* oc, double* od, double* ooffset) {
   return guard([&] {
+    need(m - 1 >= 2, "collapse_store: store too small");  // rlt2.cpp:111
+    auto s = stage_store(m, b, c, d, offset);
+    auto o = collapse_store_device(*s, fac, loc);
     const int mc = m - 1;
-    need(mc >= 2, "collapse_store: store too small");
-    HIdx ix(m), ox(mc);
-    *ooffset = offset + b[(size_t)fac * m + loc];
-    auto fm = [&](int i) { return i - (i > fac); };
-    auto lm = [&](int p) { return p - (p > loc); };
-    for (int i = 0; i < m; ++i) {
-      if (i == fac) continue;
-      for (int p = 0; p < m; ++p) {
-        if (p == loc) continue;
-        ob[(size_t)fm(i) * mc + lm(p)] =
-            b[(size_t)i * m + p] + c[ix.cidx(i, p, fac, loc)] + c[ix.cidx(fac, loc, i, p)];
-      }
-    }
-    std::memset(oc, 0, nc_of(mc) * sizeof(double));
-    for (int i = 0; i < m; ++i) {
-      if (i == fac) continue;
-      for (int p = 0; p < m; ++p) {
-        if (p == loc) continue;
-        for (int j = 0; j < m; ++j) {
-          if (j == i || j == fac) continue;
-          for (int q = 0; q < m; ++q) {
-            if (q == p || q == loc) continue;
-            oc[ox.cidx(fm(i), lm(p), fm(j), lm(q))] = c[ix.cidx(i, p, j, q)];
-          }
-        }
-      }
-    }
-    if (mc >= 3 && od) std::memset(od, 0, nd_of(mc) * sizeof(double));
-    if (m < 3) return;
-    const int tiles = ix.tiles();
-    for (int t = 0; t < tiles; ++t) {
-      const int fp = t / ix.lpairs, lp = t % ix.lpairs;
-      int i = 0, j = 0;
-      for (int a = 0, acc = 0; a < m; ++a) {
-        if (fp < acc + (m - 1 - a)) {
-          i = a;
-          j = a + 1 + (fp - acc);
-          break;
-        }
-        acc += m - 1 - a;
-      }
-      const int p = lp / (m - 1), qq = lp % (m - 1), q = qq + (qq >= p);
-      const double* tl = d + (size_t)t * ix.esz;
-      if (i == fac || j == fac) {
-        const bool first = (i == fac);
-        if ((first ? p : q) != loc) continue;
-        const int oi = first ? j : i, op = first ? q : p;
-        for (int cc = 0; cc < ix.esz; ++cc) {
-          if (tl[cc] == 0) continue;
-          int k, r;
-          ix.uncell(i, j, p, q, cc, &k, &r);
-          if (r == loc) continue;
-          oc[ox.cidx(fm(oi), lm(op), fm(k), lm(r))] += tl[cc];
-        }
-        continue;
-      }
-      if (p == loc || q == loc) continue;
-      for (int cc = 0; cc < ix.esz; ++cc) {
-        const double v = tl[cc];
-        int k, r;
-        ix.uncell(i, j, p, q, cc, &k, &r);
-        if (k == fac) {
-          if (r == loc) oc[ox.cidx(fm(i), lm(p), fm(j), lm(q))] += v;
-          continue;
-        }
-        if (r == loc) continue;
-        if (v == 0) continue;
-        if (od)
-          od[(size_t)ox.tile(fm(i), fm(j), lm(p), lm(q)) * ox.esz +
-             ox.cell(fm(i), fm(j), lm(p), lm(q), fm(k), lm(r))] += v;
-      }
-    }
+    qapb::cuda_check(cudaMemcpyAsync(ob, o->b, store_nb(mc) * 8, cudaMemcpyDefault, o->stream), "D2H");
+    qapb::cuda_check(cudaMemcpyAsync(oc, o->c, store_nc(mc) * 8, cudaMemcpyDefault, o->stream), "D2H");
+    if (mc >= 3 && od)
+      qapb::cuda_check(cudaMemcpyAsync(od, o->d, store_nd(mc) * 8, cudaMemcpyDefault, o->stream),
+                       "D2H");
+    o->synchronize();
+    *ooffset = o->offset;
   });
 }
 
-// redistribute_family, rlt2.cpp:184-205
+// redistribute_family, rlt2.cpp:184-205 (device, the phase-2 kernel's rule)
 QAPB_API qapb_status qapb_redistribute_family(const double pi[3], double add[3],
                                               int virtual_slots, double tol, int* ok) {
   return guard([&] {
-    int nb = virtual_slots;
-    double total = 0;
-    for (int s = 0; s < 3; ++s) {
-      if (pi[s] > tol)
-        total += pi[s];
-      else
-        ++nb;
-    }
-    if (total <= 0) {
-      add[0] = add[1] = add[2] = 0;
-      *ok = 1;
-      return;
-    }
-    if (nb == 0) {
-      add[0] = add[1] = add[2] = 0;
-      *ok = 0;
-      return;
-    }
-    const double share = total / nb;
-    for (int s = 0; s < 3; ++s) add[s] = (pi[s] > tol) ? -pi[s] : share;
-    *ok = 1;
+    *ok = qapb::redistribute_family_device(pi, add, virtual_slots, tol, current_device()) ? 1 : 0;
   });
 }
 

@@ -122,6 +122,7 @@ ncclComm_t cached_comm(const ncclUniqueId& id, int world, int rank, int dev) {
 Engine::Engine(int m, const double* b, const double* c, const double* d, double offset,
                const qapb_config& cfg)
     : m_(m), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
+  const DeviceGuard dg(dev_);
   if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");  // rlt2.cpp:209
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
   alloc();
@@ -148,6 +149,7 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
 Engine::Engine(int n, const double* flow, const double* dist, const double* linear,
                const qapb_config& cfg, int rank, int world, const unsigned char* nccl_id)
     : rank_(rank), world_(world), m_(n), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
+  const DeviceGuard dg(dev_);
   if (n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
   if (world_ < 1 || world_ > kMaxRanks || rank_ < 0 || rank_ >= world_)
@@ -324,6 +326,9 @@ void Engine::init_state() {
 }
 
 Engine::~Engine() {
+  int prev = -1;  // DeviceGuard without throwing from a destructor
+  cudaGetDevice(&prev);
+  if (prev != dev_) cudaSetDevice(dev_);
   if (st_) cudaStreamSynchronize(st_);
   if (graph_) cudaGraphExecDestroy(graph_);
   for (auto& pe : pending_) {
@@ -356,6 +361,7 @@ Engine::~Engine() {
   if (join_ev_) cudaEventDestroy(join_ev_);
   if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
+  if (prev >= 0 && prev != dev_) cudaSetDevice(prev);
 }
 
 void Engine::ensure_hist(int need) {
@@ -891,7 +897,7 @@ void Engine::sa_perturb() {
 }
 
 double Engine::iterate() {
-  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  const DeviceGuard dg(dev_);
   hS_.run_mode = 0;
   hS_.stop = 0;
   push_scalars();
@@ -936,7 +942,7 @@ void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) cons
 }
 
 void Engine::run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<int>* cert) {
-  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  const DeviceGuard dg(dev_);
   const auto t0 = std::chrono::steady_clock::now();
   const int from = hS_.iter;
   hS_.run_mode = 1;
@@ -986,6 +992,7 @@ void Engine::run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<i
 }
 
 std::vector<int> Engine::certificate() const {
+  const DeviceGuard dg(dev_);
   std::vector<int> out;
   if (!hS_.has_cert) return out;
   out.resize(m_);
@@ -994,6 +1001,7 @@ std::vector<int> Engine::certificate() const {
 }
 
 std::vector<int> Engine::x_assignment() const {
+  const DeviceGuard dg(dev_);
   std::vector<int> out(m_);
   cuda_check(cudaMemcpy(out.data(), xrow_, m_ * sizeof(int), cudaMemcpyDeviceToHost), "D2H xrow");
   return out;
@@ -1018,7 +1026,7 @@ size_t Engine::array_size(int which) const {
 // shard_state_mask_kernel): assemble the full array on every rank.  Collective:
 // every rank must call it for the same array.
 void Engine::assemble_sharded(int which, double* dst) const {
-  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  const DeviceGuard dg(dev_);
   cuda_check(cudaStreamSynchronize(st_), "assemble");
   double* src = which == QAPB_ARR_PI_Z ? piz_ : (which == QAPB_ARR_INCZ ? incz_ : d_);
   if (which == QAPB_ARR_STORE_D) {
@@ -1039,6 +1047,7 @@ void Engine::assemble_sharded(int which, double* dst) const {
 }
 
 void Engine::get_array(int which, double* dst, size_t count) const {
+  const DeviceGuard dg(dev_);
   const size_t n = array_size(which);
   if (count != n) throw std::invalid_argument("array size mismatch");
   if (world_ > 1 && n &&
@@ -1064,7 +1073,6 @@ void Engine::get_array(int which, double* dst, size_t count) const {
   // dst may be host or device memory (device snapshots, store.cu)
   if (n && ri_ && (which == QAPB_ARR_PI_Z || which == QAPB_ARR_STORE_D || which == QAPB_ARR_INCZ)) {
     // back to the reference layout (StoreIndex) on the way out
-    cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
     double* tmp = nullptr;
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(double), st_),
                "cudaMallocAsync");
@@ -1122,8 +1130,8 @@ void Engine::collect_events() {
 }
 
 void Engine::enqueue(int iters) {
-  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
-  if (cfg_.sa_enabled)
+  const DeviceGuard dg(dev_);
+  if (cfg_.sa_enabled && !sa_dev_)
     throw std::invalid_argument("enqueue: SA needs a host step per iteration; use iterate()");
   if (iters <= 0) return;
   if (hS_.run_mode || hS_.stop) {
@@ -1137,12 +1145,14 @@ void Engine::enqueue(int iters) {
 }
 
 void Engine::synchronize() {
+  const DeviceGuard dg(dev_);
   pull_scalars();
   if (profiling_) collect_events();
   check_phase2();
 }
 
 void Engine::history(int from, int count, double* bounds, double* best) const {
+  const DeviceGuard dg(dev_);
   if (from < 0 || count < 0 || from + count > hS_.iter)
     throw std::invalid_argument("history: range outside completed iterations");
   if (!count) return;
@@ -1153,7 +1163,7 @@ void Engine::history(int from, int count, double* bounds, double* best) const {
 }
 
 double Engine::time_kernel(int kind, int reps) {
-  cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+  const DeviceGuard dg(dev_);
   cuda_check(cudaStreamSynchronize(st_), "sync");
   cudaEvent_t a, b;
   cuda_check(cudaEventCreate(&a), "event");
@@ -1197,6 +1207,7 @@ double Engine::time_kernel(int kind, int reps) {
 }
 
 void Engine::set_profiling(bool on) {
+  const DeviceGuard dg(dev_);
   if (on == profiling_) return;
   cuda_check(cudaStreamSynchronize(st_), "sync");
   if (profiling_) collect_events();
@@ -1204,6 +1215,7 @@ void Engine::set_profiling(bool on) {
 }
 
 void Engine::kernel_times(double* ms, long long* launches, bool reset) {
+  const DeviceGuard dg(dev_);
   cuda_check(cudaStreamSynchronize(st_), "sync");
   cuda_check(cudaStreamSynchronize(st2_), "sync");
   collect_events();

@@ -27,6 +27,24 @@ struct CudaError : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Sets the engine's device for the scope of an entry point and restores the
+// caller's current device afterwards (engines of several devices may be
+// driven from one thread).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 class Engine {
  public:
   // AscentEngine(CoefficientStore, cfg) (rlt2.cpp:207-230); d == nullptr

@@ -82,13 +82,6 @@ size_t nd_of(int m) {
   return (size_t)(m * (m - 1) / 2) * (m * (m - 1)) * (m - 2) * (m - 2);
 }
 
-std::string slurp(const std::string& path) {
-  std::ifstream f(path);
-  if (!f) throw std::runtime_error("cannot open " + path);
-  std::ostringstream ss;
-  ss << f.rdbuf();
-  return ss.str();
-}
 
 BoundReport report_from(const qapb_report& r, std::vector<qapb_record>& recs,
                         const std::vector<int>& cert, const AscentConfig& cfg) {
@@ -113,159 +106,27 @@ BoundReport report_from(const qapb_report& r, std::vector<qapb_record>& recs,
 }  // namespace
 
 // ---------------------------------------------------------------- instance
-QAP_API double evaluate_objective(const QapInstance& inst, const std::vector<int>& perm) {
+// QAPLIB I/O, generators and manifests (instance.hpp) are outside the
+// drop-in boundary: they stay the reference's own
+// src/instance.cpp, linked next to this library.  The
+// engine needs only the objective of a certificate (run_ascent,
+// rlt2.cpp:594-595), summed in the reference's order (instance.cpp:11-26:
+// per facility, the linear term, then its row of flow x distance products).
+namespace {
+double certificate_objective(const QapInstance& inst, const std::vector<int>& perm) {
   const int n = inst.n;
-  if ((int)perm.size() != n) throw std::invalid_argument("perm size != n");
-  std::vector<char> seen(n, 0);
+  const bool lin = !inst.linear.empty();
+  double sum = 0;
   for (int i = 0; i < n; ++i) {
-    if (perm[i] < 0 || perm[i] >= n || seen[perm[i]])
-      throw std::invalid_argument("not a permutation");
-    seen[perm[i]] = 1;
+    const int pi = perm[i];
+    sum += lin ? inst.linear[(size_t)i * n + pi] : 0.0;
+    const double* frow = inst.flow.data() + (size_t)i * n;
+    const double* drow = inst.dist.data() + (size_t)pi * n;
+    for (int j = 0; j < n; ++j) sum += frow[j] * drow[perm[j]];
   }
-  double v = 0;
-  for (int i = 0; i < n; ++i) {
-    v += inst.b(i, perm[i]);
-    for (int j = 0; j < n; ++j) v += inst.f(i, j) * inst.d(perm[i], perm[j]);
-  }
-  return v;
+  return sum;
 }
-
-QAP_API QapInstance parse_qaplib(const std::string& text, bool swap_order,
-                                 const std::string& name) {
-  std::istringstream in(text);
-  QapInstance inst;
-  inst.name = name;
-  if (!(in >> inst.n) || inst.n <= 0) throw std::runtime_error("bad instance size");
-  const int nn = inst.n * inst.n;
-  auto block = [&](const char* what) {
-    std::vector<double> out(nn);
-    for (double& x : out)
-      if (!(in >> x)) throw std::runtime_error(std::string("truncated input reading ") + what);
-    return out;
-  };
-  std::vector<double> a = block("first matrix");
-  std::vector<double> b = block("second matrix");
-  inst.flow = swap_order ? b : a;
-  inst.dist = swap_order ? a : b;
-  double probe;
-  if (in >> probe) {
-    inst.linear.resize(nn);
-    inst.linear[0] = probe;
-    for (int i = 1; i < nn; ++i)
-      if (!(in >> inst.linear[i])) throw std::runtime_error("truncated linear-cost matrix");
-  } else {
-    inst.linear.assign(nn, 0.0);
-  }
-  return inst;
-}
-
-QAP_API QapInstance load_qaplib_file(const std::string& path, bool swap_order) {
-  std::string base = path.substr(path.find_last_of('/') == std::string::npos
-                                     ? 0
-                                     : path.find_last_of('/') + 1);
-  const size_t dot = base.find_last_of('.');
-  if (dot != std::string::npos) base = base.substr(0, dot);
-  return parse_qaplib(slurp(path), swap_order, base);
-}
-
-QAP_API std::vector<int> parse_solution(const std::string& text, int expect_n, double* value) {
-  std::istringstream in(text);
-  int n;
-  double v;
-  if (!(in >> n >> v)) throw std::runtime_error("bad solution header");
-  if (n != expect_n) throw std::runtime_error("solution size mismatch");
-  std::vector<int> perm(n);
-  for (int& p : perm) {
-    if (!(in >> p)) throw std::runtime_error("truncated permutation");
-    p -= 1;
-  }
-  std::vector<char> seen(n, 0);
-  for (int p : perm) {
-    if (p < 0 || p >= n || seen[p]) throw std::runtime_error("solution is not a permutation");
-    seen[p] = 1;
-  }
-  if (value) *value = v;
-  return perm;
-}
-
-QAP_API std::vector<int> load_solution_file(const std::string& path, int expect_n,
-                                            double* value) {
-  return parse_solution(slurp(path), expect_n, value);
-}
-
-QAP_API std::string format_qaplib(const QapInstance& inst) {
-  std::ostringstream out;
-  out << inst.n << "\n\n";
-  for (const auto* mtx : {&inst.flow, &inst.dist}) {
-    for (int i = 0; i < inst.n; ++i) {
-      for (int j = 0; j < inst.n; ++j) {
-        const double v = (*mtx)[(size_t)i * inst.n + j];
-        if (j) out << ' ';
-        if (v == std::floor(v))
-          out << (long long)v;
-        else
-          out << v;
-      }
-      out << "\n";
-    }
-    out << "\n";
-  }
-  return out.str();
-}
-
-QAP_API QapInstance generate_instance(int n, std::uint64_t seed, int max_entry) {
-  if (n < 2) throw std::invalid_argument("n must be >= 2");
-  QapInstance inst;
-  inst.n = n;
-  inst.flow.assign((size_t)n * n, 0.0);
-  inst.dist.assign((size_t)n * n, 0.0);
-  inst.linear.assign((size_t)n * n, 0.0);
-  inst.name = "rand" + std::to_string(n) + "-" + std::to_string(seed);
-  std::mt19937_64 rng(seed);
-  auto draw = [&]() { return (double)(rng() % (std::uint64_t)(max_entry + 1)); };
-  for (int i = 0; i < n; ++i)
-    for (int j = i + 1; j < n; ++j) inst.flow[(size_t)i * n + j] = inst.flow[(size_t)j * n + i] = draw();
-  for (int p = 0; p < n; ++p)
-    for (int q = p + 1; q < n; ++q) inst.dist[(size_t)p * n + q] = inst.dist[(size_t)q * n + p] = draw();
-  return inst;
-}
-
-QAP_API std::vector<ManifestEntry> parse_manifest(const std::string& text) {
-  std::vector<ManifestEntry> out;
-  std::istringstream in(text);
-  std::string line;
-  while (std::getline(in, line)) {
-    const size_t h = line.find('#');
-    if (h != std::string::npos) line.erase(h);
-    std::istringstream ls(line);
-    ManifestEntry e;
-    if (!(ls >> e.path)) continue;
-    std::string tok;
-    while (ls >> tok) {
-      if (tok == "swap")
-        e.swap_order = true;
-      else if (tok.rfind("opt=", 0) == 0)
-        e.best_known = std::stod(tok.substr(4));
-      else if (tok.rfind("sln=", 0) == 0)
-        e.sln_path = tok.substr(4);
-      else
-        throw std::runtime_error("unknown manifest token: " + tok);
-    }
-    out.push_back(e);
-  }
-  return out;
-}
-
-QAP_API std::vector<ManifestEntry> load_manifest_file(const std::string& path) {
-  auto entries = parse_manifest(slurp(path));
-  const size_t slash = path.find_last_of('/');
-  const std::string dir = slash == std::string::npos ? "" : path.substr(0, slash + 1);
-  for (auto& e : entries) {
-    if (!e.path.empty() && e.path[0] != '/') e.path = dir + e.path;
-    if (!e.sln_path.empty() && e.sln_path[0] != '/') e.sln_path = dir + e.sln_path;
-  }
-  return entries;
-}
+}  // namespace
 
 // ---------------------------------------------------------------- LAP
 QAP_API void LapSolver::reserve(int m) { max_m_ = std::max(max_m_, m); }
@@ -572,7 +433,8 @@ QAP_API BoundReport run_ascent(const QapInstance& inst, const AscentConfig& cfg)
                         (int)recs.size(), cert.data()));
   BoundReport rep = report_from(r, recs, cert, cfg);
   rep.instance = inst.name;
-  if (!rep.certificate.empty()) rep.certificate_value = evaluate_objective(inst, rep.certificate);
+  if (!rep.certificate.empty())
+    rep.certificate_value = certificate_objective(inst, rep.certificate);
   return rep;
 }
 

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -115,6 +116,62 @@ __global__ void collapse_d_kernel(int m, int fac, int loc, const double* __restr
   }
 }
 
+// store_evaluate (rlt2.cpp:91-107): the terms in the reference's summation
+// order -- b[i,perm i] (i ascending), C'[i,perm i,j,perm j] (i, then j != i),
+// D' cells (i<j lexicographic, then k != i,j ascending) -- gathered in
+// parallel into `terms`; one thread then adds them in that order from offset.
+__global__ void store_terms_kernel(int m, const double* __restrict__ b,
+                                   const double* __restrict__ c, const double* __restrict__ d,
+                                   const int* __restrict__ perm, double* __restrict__ terms) {
+  const DIdx ix(m);
+  const int nb = m, ncl = m * (m - 1);
+  const int nd = m >= 3 ? m * (m - 1) / 2 * (m - 2) : 0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nb + ncl + nd;
+       e += gridDim.x * blockDim.x) {
+    double v;
+    if (e < nb) {
+      v = b[(size_t)e * m + perm[e]];
+    } else if (e < nb + ncl) {
+      const int x = e - nb, i = x / (m - 1), jj = x - i * (m - 1), j = jj + (jj >= i);
+      v = c[ix.cidx(i, perm[i], j, perm[j])];
+    } else {
+      const int x = e - nb - ncl, pair = x / (m - 2), kk = x - pair * (m - 2);
+      int i, j;
+      unfpair(m, pair, &i, &j);  // pairs in fpair (lexicographic) order
+      const int k = kk + (kk >= i) + (kk + (kk >= i) >= j);
+      const int t = ix.tile(i, j, perm[i], perm[j]);
+      v = d[(size_t)t * ix.esz + ix.cell(i, j, perm[i], perm[j], k, perm[k])];
+    }
+    terms[e] = v;
+  }
+}
+__global__ void ordered_sum_kernel(const double* __restrict__ terms, int count, double offset,
+                                   double* out) {
+  double v = offset;
+  for (int e = 0; e < count; ++e) v = dadd(v, terms[e]);
+  *out = v;
+}
+
+// redistribute_family (rlt2.cpp:184-205) on the device: the same rule the
+// phase-2 kernel applies per family, exposed for the reference API
+__global__ void redistribute_kernel(const double* pi, double* add, int vslots, double tol,
+                                    int* ok) {
+  int nb = vslots;
+  double total = 0.0;
+  double a[3];
+  for (int s = 0; s < 3; ++s) {
+    if (pi[s] > tol)
+      total = dadd(total, pi[s]);
+    else
+      ++nb;
+  }
+  const bool zero = total <= 0.0 || nb == 0;
+  const double share = zero ? 0.0 : __ddiv_rn(total, (double)nb);
+  for (int s = 0; s < 3; ++s) a[s] = zero ? 0.0 : ((pi[s] > tol) ? -pi[s] : share);
+  for (int s = 0; s < 3; ++s) add[s] = a[s];
+  *ok = (total <= 0.0 || nb != 0) ? 1 : 0;
+}
+
 int sms() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -127,6 +184,20 @@ void check(cudaError_t e, const char* what) {
     throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+// the calling thread's current device, restored on scope exit
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 }  // namespace
 
 size_t store_nb(int m) { return (size_t)m * m; }
@@ -135,40 +206,104 @@ size_t store_nd(int m) {
   return m >= 3 ? (size_t)m * (m - 1) / 2 * m * (m - 1) * (m - 2) * (m - 2) : 0;
 }
 
+// Each store owns a stream and takes its arrays from the device's
+// stream-ordered pool: creating, folding and freeing the stores of several
+// branch-and-bound banks never serialises the device (cudaMalloc/cudaFree and
+// legacy-stream work would).
 DeviceStore::DeviceStore(int m_, int device_) : m(m_), device(device_) {
-  check(cudaSetDevice(device), "cudaSetDevice");
-  check(cudaMalloc(&b, std::max<size_t>(1, store_nb(m)) * sizeof(double)), "cudaMalloc b");
-  check(cudaMalloc(&c, std::max<size_t>(1, store_nc(m)) * sizeof(double)), "cudaMalloc c");
-  check(cudaMalloc(&d, std::max<size_t>(1, store_nd(m)) * sizeof(double)), "cudaMalloc d");
+  DeviceGuard g(device);
+  check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  check(cudaMallocAsync(&b, std::max<size_t>(1, store_nb(m)) * sizeof(double), stream), "alloc b");
+  check(cudaMallocAsync(&c, std::max<size_t>(1, store_nc(m)) * sizeof(double), stream), "alloc c");
+  check(cudaMallocAsync(&d, std::max<size_t>(1, store_nd(m)) * sizeof(double), stream), "alloc d");
+  synchronize();  // usable from any stream from here on
 }
 
 DeviceStore::~DeviceStore() {
-  cudaSetDevice(device);
-  cudaFree(b);
-  cudaFree(c);
-  cudaFree(d);
+  DeviceGuard g(device);
+  cudaFreeAsync(b, stream);
+  cudaFreeAsync(c, stream);
+  cudaFreeAsync(d, stream);
+  cudaStreamSynchronize(stream);
+  cudaStreamDestroy(stream);
 }
+
+void DeviceStore::synchronize() const { check(cudaStreamSynchronize(stream), "store stream"); }
 
 std::unique_ptr<DeviceStore> collapse_store_device(const DeviceStore& s, int fac, int loc) {
   const int m = s.m, mc = m - 1;
   if (mc < 2) throw std::invalid_argument("collapse_store: store too small");  // rlt2.cpp:111
   if (fac < 0 || fac >= m || loc < 0 || loc >= m)
     throw std::invalid_argument("collapse_store: facility/location out of range");
+  DeviceGuard g(s.device);
   auto out = std::make_unique<DeviceStore>(mc, s.device);
+  // the child's stream follows everything already queued on the parent's
+  cudaEvent_t ev;
+  check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  check(cudaEventRecord(ev, s.stream), "event");
+  check(cudaStreamWaitEvent(out->stream, ev, 0), "wait");
+  cudaEventDestroy(ev);
   double bfl = 0.0;
-  check(cudaMemcpy(&bfl, s.b + (size_t)fac * m + loc, sizeof(double), cudaMemcpyDeviceToHost),
+  check(cudaMemcpyAsync(&bfl, s.b + (size_t)fac * m + loc, sizeof(double),
+                        cudaMemcpyDeviceToHost, out->stream),
         "D2H b");
-  out->offset = s.offset + bfl;  // rlt2.cpp:116
-  collapse_b_kernel<<<(mc * mc + 255) / 256, 256>>>(m, fac, loc, s.b, s.c, out->b);
+  collapse_b_kernel<<<(mc * mc + 255) / 256, 256, 0, out->stream>>>(m, fac, loc, s.b, s.c, out->b);
   check(cudaGetLastError(), "collapse b");
-  collapse_c_kernel<<<4 * sms(), 256>>>(m, fac, loc, s.c, s.d, out->c);
+  collapse_c_kernel<<<4 * sms(), 256, 0, out->stream>>>(m, fac, loc, s.c, s.d, out->c);
   check(cudaGetLastError(), "collapse c");
   if (mc >= 3) {
-    collapse_d_kernel<<<8 * sms(), 256>>>(m, fac, loc, s.d, out->d);
+    collapse_d_kernel<<<8 * sms(), 256, 0, out->stream>>>(m, fac, loc, s.d, out->d);
     check(cudaGetLastError(), "collapse d");
   }
-  check(cudaDeviceSynchronize(), "collapse_store");
+  out->synchronize();
+  out->offset = s.offset + bfl;  // rlt2.cpp:116
   return out;
+}
+
+double store_evaluate_device(const DeviceStore& s, const int* perm) {
+  const int m = s.m;
+  if (m < 3) throw std::invalid_argument("store_evaluate: m >= 3 required");
+  DeviceGuard g(s.device);
+  const int count = m + m * (m - 1) + m * (m - 1) / 2 * (m - 2);
+  int* dperm = nullptr;
+  double *terms = nullptr, *dv = nullptr;
+  check(cudaMallocAsync(reinterpret_cast<void**>(&dperm), m * sizeof(int), s.stream), "alloc");
+  check(cudaMallocAsync(reinterpret_cast<void**>(&terms), count * sizeof(double), s.stream),
+        "alloc");
+  check(cudaMallocAsync(reinterpret_cast<void**>(&dv), sizeof(double), s.stream), "alloc");
+  check(cudaMemcpyAsync(dperm, perm, m * sizeof(int), cudaMemcpyHostToDevice, s.stream), "H2D");
+  store_terms_kernel<<<std::max(1, std::min(4 * sms(), (count + 255) / 256)), 256, 0, s.stream>>>(
+      m, s.b, s.c, s.d, dperm, terms);
+  check(cudaGetLastError(), "store terms");
+  ordered_sum_kernel<<<1, 1, 0, s.stream>>>(terms, count, s.offset, dv);
+  check(cudaGetLastError(), "ordered sum");
+  double v = 0.0;
+  check(cudaMemcpyAsync(&v, dv, sizeof(double), cudaMemcpyDeviceToHost, s.stream), "D2H");
+  cudaFreeAsync(dperm, s.stream);
+  cudaFreeAsync(terms, s.stream);
+  cudaFreeAsync(dv, s.stream);
+  s.synchronize();
+  return v;
+}
+
+bool redistribute_family_device(const double pi[3], double add[3], int virtual_slots, double tol,
+                                int device) {
+  DeviceGuard g(device);
+  cudaStream_t st = cudaStreamPerThread;
+  double* buf = nullptr;
+  check(cudaMallocAsync(reinterpret_cast<void**>(&buf), 7 * sizeof(double), st), "alloc");
+  check(cudaMemcpyAsync(buf, pi, 3 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+  redistribute_kernel<<<1, 1, 0, st>>>(buf, buf + 3, virtual_slots, tol,
+                                       reinterpret_cast<int*>(buf + 6));
+  check(cudaGetLastError(), "redistribute");
+  double h[7];
+  check(cudaMemcpyAsync(h, buf, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+  cudaFreeAsync(buf, st);
+  check(cudaStreamSynchronize(st), "redistribute");
+  for (int k = 0; k < 3; ++k) add[k] = h[3 + k];
+  int ok = 0;
+  std::memcpy(&ok, &h[6], sizeof ok);
+  return ok != 0;
 }
 
 }  // namespace qapb

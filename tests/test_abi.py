@@ -49,8 +49,9 @@ def test_variant_names_and_parse():
         q.parse_variant("X9")
 
 
+@pytest.mark.gpu
 def test_redistribute_family_known_answers():
-    """test_rlt2.cpp:207-247."""
+    """test_rlt2.cpp:207-247 (the device rule of the phase-2 kernel, store.cu)."""
     from paper_1710_03732_b200 import redistribute_family as rf
     ok, add = rf([10.0, 0.0, 0.0])
     assert ok and list(add) == [-10.0, 2.0, 2.0]
@@ -66,9 +67,11 @@ def test_redistribute_family_known_answers():
     assert ok and list(add) == [-5.0, 1.0, 1.0]
 
 
+@pytest.mark.gpu
 @pytest.mark.skipif(not available("port"), reason="oracle port not built")
 def test_store_helpers_exact():
-    """store_evaluate / collapse_store exactness (test_rlt2.cpp:94-107, 313-355)."""
+    """store_evaluate / collapse_store exactness (test_rlt2.cpp:94-107, 313-355), both
+    on the device (store.cu)."""
     import itertools
     from paper_1710_03732_b200 import CoefficientStore, collapse_store, store_evaluate
     from paper_1710_03732_b200.instance import evaluate_objective, generate_instance
@@ -92,6 +95,26 @@ def test_store_helpers_exact():
         assert abs(store_evaluate(child, cp) - evaluate_objective(inst, full)) < 1e-9
 
 
+@pytest.mark.gpu
+@pytest.mark.skipif(not available("ref"), reason="reference build absent")
+def test_store_evaluate_bitwise_vs_reference():
+    """store_evaluate (rlt2.cpp:91-107) on the device, summed in the reference's order."""
+    from paper_1710_03732_b200 import CoefficientStore, store_evaluate
+    ref = Oracle("ref")
+    rng = np.random.default_rng(11)
+    for m in (3, 5, 8):
+        nb, nc, nd = abi.store_sizes(m)
+        b, c, d = rng.normal(size=nb), rng.normal(size=nc), rng.normal(size=nd)
+        st = CoefficientStore(m, b, c, d, 0.25)
+        for _ in range(20):
+            perm = rng.permutation(m).astype(np.int32)
+            want = ctypes.c_double()
+            assert ref.lib.qref_store_evaluate(m, abi.dptr(b), abi.dptr(c), abi.dptr(d), 0.25,
+                                               abi.iptr(perm), ctypes.byref(want)) == 0
+            assert store_evaluate(st, list(perm)) == want.value
+
+
+@pytest.mark.gpu
 @pytest.mark.skipif(not available("ref"), reason="reference build absent")
 def test_collapse_store_bitwise_vs_reference():
     from paper_1710_03732_b200 import CoefficientStore, collapse_store
