@@ -317,6 +317,27 @@ QAPB_API qapb_status qapb_store_destroy(qapb_store* s);
 QAPB_API qapb_status qapb_engine_create_from_store(const qapb_store* s,
                                                    const qapb_config* cfg,
                                                    qapb_engine** out);
+/* As above with the store's constant term given explicitly (the facade's
+ * CoefficientStore::offset is host-side and may be changed after the device
+ * data was made, e.g. bnb.cpp:203 cold_store). */
+QAPB_API qapb_status qapb_engine_create_from_store_offset(const qapb_store* s, double offset,
+                                                          const qapb_config* cfg,
+                                                          qapb_engine** out);
+/* collapse_store with the parent's constant term given explicitly
+ * (child offset = offset + b[fac, loc], rlt2.cpp:116). */
+QAPB_API qapb_status qapb_store_collapse_offset(const qapb_store* s, double offset, int fac,
+                                                int loc, qapb_store** out);
+/* free / total bytes of a device (cudaMemGetInfo) */
+QAPB_API qapb_status qapb_device_memory(int device, size_t* free_bytes, size_t* total_bytes);
+/* the CUDA device a store lives on */
+QAPB_API qapb_status qapb_store_device(const qapb_store* s, int* device);
+/* init_coefficients(inst), rlt2.cpp:66-89, built in HBM (D' = 0). */
+QAPB_API qapb_status qapb_store_init(int n, const double* flow, const double* dist,
+                                     const double* linear, int device, qapb_store** out);
+/* store_evaluate(st, perm), rlt2.cpp:91-107, on a device store; `offset`
+ * replaces the store's constant term. */
+QAPB_API qapb_status qapb_store_evaluate_device(const qapb_store* s, double offset,
+                                                const int* perm, double* value);
 
 #ifdef __cplusplus
 }

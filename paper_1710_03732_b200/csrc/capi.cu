@@ -4,9 +4,12 @@
 // exception type the reference would throw (SURVEY.md §8b "Errors") onto a
 // status code and a thread-local message.
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <limits>
+#include <cstdlib>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -40,8 +43,21 @@ struct qapb_store {
 namespace {
 thread_local std::string g_err;
 
+// Debugging aid (QAPB_SERIALIZE=1): one C-ABI call at a time in the process,
+// so concurrent callers (branch-and-bound banks) cannot interleave GPU work.
+std::recursive_mutex& serial_mutex() {
+  static std::recursive_mutex mu;
+  return mu;
+}
+bool serialize_calls() {
+  static const bool on = std::getenv("QAPB_SERIALIZE") != nullptr;
+  return on;
+}
+
 template <class F>
 qapb_status guard(F&& f) {
+  std::unique_lock<std::recursive_mutex> lk(serial_mutex(), std::defer_lock);
+  if (serialize_calls()) lk.lock();
   try {
     f();
     return QAPB_OK;
@@ -285,7 +301,7 @@ QAPB_API qapb_status qapb_store_evaluate(int m, const double* b, const double* c
   return guard([&] {
     need(m >= 3, "store_evaluate: m >= 3 required");
     auto s = stage_store(m, b, c, d, offset);
-    *value = qapb::store_evaluate_device(*s, perm);
+    *value = qapb::store_evaluate_device(*s, perm, s->offset);
   });
 }
 
@@ -544,13 +560,17 @@ QAPB_API qapb_status qapb_store_upload(int m, const double* b, const double* c,
     need(b && c && (m < 3 || d) && out, "store_upload: null pointer");
     auto h = std::make_unique<qapb_store>();
     h->s = std::make_unique<DeviceStore>(m, device);
-    auto up = [](double* dst, const double* src, size_t n) {
-      if (n && cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault) != cudaSuccess)
+    // on the store's stream, completed before return (a legacy-stream
+    // cudaMemcpy from pageable memory may return before its DMA lands)
+    auto up = [&](double* dst, const double* src, size_t n) {
+      if (n && cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, h->s->stream) !=
+                   cudaSuccess)
         throw CudaError("store_upload: copy failed");
     };
     up(h->s->b, b, store_nb(m));
     up(h->s->c, c, store_nc(m));
     if (m >= 3) up(h->s->d, d, store_nd(m));
+    h->s->synchronize();
     h->s->offset = offset;
     *out = h.release();
   });
@@ -597,14 +617,17 @@ QAPB_API qapb_status qapb_store_download(const qapb_store* s, double* b, double*
   return guard([&] {
     need(s, "store_download: null store");
     const int m = s->s->m;
-    auto down = [](double* dst, const double* src, size_t n) {
-      if (dst && n && cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault) != cudaSuccess)
+    auto down = [&](double* dst, const double* src, size_t n) {
+      if (dst && n &&
+          cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, s->s->stream) !=
+              cudaSuccess)
         throw CudaError("store_download: copy failed");
     };
     cuda_check_set(s->s->device);
     down(b, s->s->b, store_nb(m));
     down(c, s->s->c, store_nc(m));
     down(d, s->s->d, store_nd(m));
+    s->s->synchronize();
     if (offset) *offset = s->s->offset;
   });
 }
@@ -614,17 +637,96 @@ QAPB_API qapb_status qapb_store_destroy(qapb_store* s) {
 }
 
 // AscentEngine(CoefficientStore, cfg), rlt2.cpp:207-230, device-to-device
-QAPB_API qapb_status qapb_engine_create_from_store(const qapb_store* s, const qapb_config* cfg,
-                                                   qapb_engine** out) {
+QAPB_API qapb_status qapb_engine_create_from_store_offset(const qapb_store* s, double offset,
+                                                          const qapb_config* cfg,
+                                                          qapb_engine** out) {
   return guard([&] {
     need(s && out, "engine_create_from_store: null pointer");
     qapb_config c0;
     qapb_config_init(&c0);
     qapb_config cc = cfg ? *cfg : c0;
     need(cc.device == s->s->device, "engine_create_from_store: cfg.device must be the store's");
+    need(s->s->m >= 3, "AscentEngine: m >= 3 required");  // rlt2.cpp:209
     auto h = std::make_unique<qapb_engine>();
-    h->e = std::make_unique<Engine>(s->s->m, s->s->b, s->s->c, s->s->m >= 3 ? s->s->d : nullptr,
-                                    s->s->offset, cc);
+    h->e = std::make_unique<Engine>(s->s->m, s->s->b, s->s->c, s->s->d, offset, cc);
     *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_engine_create_from_store(const qapb_store* s, const qapb_config* cfg,
+                                                   qapb_engine** out) {
+  if (!s) {
+    g_err = "engine_create_from_store: null pointer";
+    return QAPB_EINVAL;
+  }
+  return qapb_engine_create_from_store_offset(s, s->s->offset, cfg, out);
+}
+
+QAPB_API qapb_status qapb_store_collapse_offset(const qapb_store* s, double offset, int fac,
+                                                int loc, qapb_store** out) {
+  return guard([&] {
+    need(s && out, "store_collapse: null pointer");
+    auto h = std::make_unique<qapb_store>();
+    h->s = collapse_store_device(*s->s, fac, loc, offset);
+    *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_device_memory(int device, size_t* free_bytes, size_t* total_bytes) {
+  return guard([&] {
+    qapb::DeviceGuard dg(device);
+    size_t f = 0, t = 0;
+    qapb::cuda_check(cudaMemGetInfo(&f, &t), "cudaMemGetInfo");
+    // the stream-ordered pool keeps freed blocks cached (engine.cu
+    // keep_pool_cached): count them as free
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      std::uint64_t reserved = 0, used = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      if (reserved > used) f += (size_t)(reserved - used);
+    }
+    if (free_bytes) *free_bytes = f;
+    if (total_bytes) *total_bytes = t;
+  });
+}
+
+QAPB_API qapb_status qapb_store_device(const qapb_store* s, int* device) {
+  return guard([&] {
+    need(s && device, "store_device: null pointer");
+    *device = s->s->device;
+  });
+}
+
+QAPB_API qapb_status qapb_store_init(int n, const double* flow, const double* dist,
+                                     const double* linear, int device, qapb_store** out) {
+  return guard([&] {
+    need(out, "store_init: null pointer");
+    need(n >= 3, "init_coefficients: n >= 3 required by RLT2");  // rlt2.cpp:67-68
+    auto h = std::make_unique<qapb_store>();
+    h->s = std::make_unique<DeviceStore>(n, device);
+    qapb::DeviceGuard dg(device);
+    cudaStream_t st = h->s->stream;
+    const size_t nn = (size_t)n * n;
+    DevBuf df(nn * 8, st), dd(nn * 8, st), dl(linear ? nn * 8 : 0, st);
+    qapb::cuda_check(cudaMemcpyAsync(df.p, flow, nn * 8, cudaMemcpyDefault, st), "H2D flow");
+    qapb::cuda_check(cudaMemcpyAsync(dd.p, dist, nn * 8, cudaMemcpyDefault, st), "H2D dist");
+    if (linear)
+      qapb::cuda_check(cudaMemcpyAsync(dl.p, linear, nn * 8, cudaMemcpyDefault, st), "H2D lin");
+    qapb::cuda_check(qapb::launch_init_store(n, df.as<double>(), dd.as<double>(),
+                                             dl.as<double>(), h->s->b, h->s->c, st),
+                     "init_store");
+    qapb::cuda_check(cudaMemsetAsync(h->s->d, 0, store_nd(n) * 8, st), "memset d");
+    h->s->offset = 0.0;
+    h->s->synchronize();
+    *out = h.release();
+  });
+}
+
+QAPB_API qapb_status qapb_store_evaluate_device(const qapb_store* s, double offset,
+                                                const int* perm, double* value) {
+  return guard([&] {
+    need(s && perm && value, "store_evaluate: null pointer");
+    *value = qapb::store_evaluate_device(*s->s, perm, offset);
   });
 }

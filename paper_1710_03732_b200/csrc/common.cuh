@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #define QAPB_FULL 0xffffffffu
@@ -55,6 +56,29 @@ __device__ __forceinline__ int skip2(int r, int lo, int hi) {
   if (r >= lo) ++r;
   if (r >= hi) ++r;
   return r;
+}
+
+// Debug builds (make EXTRA=-DQAPB_BOUNDS): index checks that print and trap.
+#ifdef QAPB_BOUNDS
+#define QAPB_CHECK(cond, tag, v, lim)                                                        \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("QAPB_BOUNDS %s: %llu >= %llu (block %d thread %d)\n", tag,                     \
+             (unsigned long long)(v), (unsigned long long)(lim), (int)blockIdx.x,           \
+             (int)threadIdx.x);                                                             \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define QAPB_CHECK(cond, tag, v, lim) \
+  do {                                \
+  } while (0)
+#endif
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 // ---- async copy / mbarrier primitives (TMA bulk path) ----

@@ -50,6 +50,37 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 namespace {
+// Debugging aid (QAPB_SYNC_CHECK=1, eager mode): every engine kernel launch
+// is followed by a synchronisation of the current device, so a faulting
+// kernel is named by the error it raises.
+bool sync_check_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("QAPB_SYNC_CHECK");
+    return v && *v && std::strcmp(v, "0") != 0;
+  }();
+  return on;
+}
+// QAPB_SYNC_CHECK=<substring>: only launches whose label contains it
+bool sync_check_matches(const char* what) {
+  static const std::string sel = [] {
+    const char* v = std::getenv("QAPB_SYNC_CHECK");
+    return std::string(v ? v : "");
+  }();
+  return sel == "1" || std::string(what).find(sel) != std::string::npos;
+}
+}  // namespace
+
+// a kernel launch of this engine; under QAPB_SYNC_CHECK its streams are
+// synchronised right away (other engines' kernels keep running concurrently)
+void Engine::kcheck(cudaError_t e, const char* what) const {
+  cuda_check(e, what);
+  if (sync_check_enabled() && sync_check_matches(what)) {
+    cuda_check(cudaStreamSynchronize(st_), what);
+    if (st2_) cuda_check(cudaStreamSynchronize(st2_), what);
+  }
+}
+
+namespace {
 constexpr double kInf = std::numeric_limits<double>::infinity();
 
 template <class T>
@@ -67,6 +98,11 @@ void dfree(T*& p) {
 // destroying engines (one per branch-and-bound node, several banks at once,
 // bnb.cpp:549-556) must not serialise the device the way cudaMalloc/cudaFree
 // do, and freed blocks stay cached for the next engine.
+bool env_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v && std::strcmp(v, "0") != 0;
+}
+
 void keep_pool_cached(int dev) {
   static std::mutex mu;
   static std::set<int> done;
@@ -76,6 +112,11 @@ void keep_pool_cached(int dev) {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     std::uint64_t keep = ~std::uint64_t{0};
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (env_flag("QAPB_POOL_NO_XSTREAM")) {  // debugging aid: no cross-stream reuse
+      int off = 0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &off);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &off);
+    }
   }
 }
 template <class T>
@@ -94,10 +135,6 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
-bool env_flag(const char* name) {
-  const char* v = std::getenv(name);
-  return v && *v && std::strcmp(v, "0") != 0;
-}
 
 // One NCCL communicator per (unique id, rank, device) for the process
 // lifetime: engines created again with the same id (a B&B bank, repeated
@@ -132,7 +169,7 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
   cuda_check(cudaMemcpyAsync(c_, c, nc_ * sizeof(double), cudaMemcpyDefault, st_), "H2D c");
   if (d && ri_) {  // reference layout in, RI layout on the device (pi(z) as scratch)
     cuda_check(cudaMemcpyAsync(piz_, d, nd_ * sizeof(double), cudaMemcpyDefault, st_), "H2D d");
-    cuda_check(launch_z_relayout(m_, piz_, d_, 1, st_), "relayout d");
+    kcheck(launch_z_relayout(m_, piz_, d_, 1, st_), "relayout d");
     ++launches_;
     cuda_check(cudaMemsetAsync(piz_, 0, nd_ * sizeof(double), st_), "memset");
   } else if (d) {
@@ -169,7 +206,7 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
   cuda_check(cudaMemcpyAsync(dd, dist, nn * 8, cudaMemcpyHostToDevice, st_), "H2D dist");
   if (linear)
     cuda_check(cudaMemcpyAsync(dl, linear, nn * 8, cudaMemcpyHostToDevice, st_), "H2D lin");
-  cuda_check(launch_init_store(n, df, dd, dl, b_, c_, st_), "init_store");
+  kcheck(launch_init_store(n, df, dd, dl, b_, c_, st_), "init_store");
   ++launches_;
   cuda_check(cudaMemsetAsync(d_, 0, nd_ * sizeof(double), st_), "memset d");
   split_gather();
@@ -219,9 +256,15 @@ void Engine::alloc() {
   salloc(st_, &fpair_ij_, fpairs_);
   plan_pipeline();
   split_mode_ = env_int("QAPB_X3SPLIT", 2);
-  // sharded engines split only their local X3 members, in hybrid mode
-  split_ = !is_two_phase() &&
-           (world_ == 1 ? split_mode_ != 0 : split_mode_ == 2);
+  // sharded engines split only their local X3 members, in hybrid mode; the
+  // 2-phase variants take the split only together with the RI layout (their
+  // phase-2 kernel, phase2_ri_kernel, exists for that layout alone)
+  const int x3g = std::max(1, env_int("QAPB_X3_GROUP", 4) / chunk_) * chunk_;
+  if (!is_two_phase())
+    split_ = world_ == 1 ? split_mode_ != 0 : split_mode_ == 2;
+  else
+    split_ = world_ == 1 && split_mode_ == 2 && stage_ev_.size() == 1 &&
+             env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3g);
   if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
     int range = m;
     if (world_ > 1) {
@@ -229,7 +272,7 @@ void Engine::alloc() {
       range = pb[rank_ + 1] - pb[rank_];
     }
     const int nch = (range + chunk_ - 1) / chunk_;
-    x3_group_ = std::max(1, env_int("QAPB_X3_GROUP", 4) / chunk_) * chunk_;
+    x3_group_ = x3g;
     x3_ngroups_ = (range + x3_group_ - 1) / x3_group_;
     salloc(st_, &x3buf_, (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_);
     salloc(st_, &d3_, (size_t)ntriples_ * nch * lpairs_ * chunk_);
@@ -244,7 +287,9 @@ void Engine::alloc() {
     if (incz_) encode_z_tmap(h + 128, incz_, m);
     encode_z_tmap(h + 256, piz_, m);
     dalloc(&tmaps_, sizeof h);  // cudaMalloc: 256-byte aligned
-    cuda_check(cudaMemcpy(tmaps_, h, sizeof h, cudaMemcpyHostToDevice), "H2D tensor maps");
+    cuda_check(cudaMemcpyAsync(tmaps_, h, sizeof h, cudaMemcpyHostToDevice, st_),
+               "H2D tensor maps");
+    cuda_check(cudaStreamSynchronize(st_), "H2D tensor maps");
   }
   // every rank of a sharded engine holds the same b, best and RNG stream, so
   // each runs the same SA step and the replicated state stays identical
@@ -273,7 +318,12 @@ void Engine::alloc() {
   for (int i = 0; i < m; ++i)
     for (int j = i + 1; j < m; ++j) fp[i * m - i * (i + 1) / 2 + (j - i - 1)] = i | (j << 16);
   cuda_check(cudaStreamSynchronize(st_), "stream-ordered allocations");
-  cuda_check(cudaMemcpy(triples_, tr.data(), tr.size() * sizeof(int), cudaMemcpyHostToDevice),
+  // H2D copies of engine tables go through the engine's stream: a legacy-stream
+  // cudaMemcpy from pageable memory may return before its DMA lands, and the
+  // engine's kernels run on non-blocking streams that do not wait for it (a
+  // branch-and-bound run with 8-16 banks read half-written fpair tables)
+  cuda_check(cudaMemcpyAsync(triples_, tr.data(), tr.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             st_),
              "H2D triples");
   // fold processing order: triples in blocks of B values of a, b and c, so the
   // units in flight together read several adjacent rows of each tile they touch
@@ -293,11 +343,14 @@ void Engine::alloc() {
                 ord.push_back(lex[((size_t)a * m + b) * m + c]);
     if ((int)ord.size() != ntriples_) throw std::logic_error("fold order: not a permutation");
     salloc(st_, &order_, ord.size());
-    cuda_check(cudaMemcpy(order_, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice),
+    cuda_check(cudaMemcpyAsync(order_, ord.data(), ord.size() * sizeof(int),
+                               cudaMemcpyHostToDevice, st_),
                "H2D fold order");
   }
-  cuda_check(cudaMemcpy(fpair_ij_, fp.data(), fp.size() * sizeof(int), cudaMemcpyHostToDevice),
+  cuda_check(cudaMemcpyAsync(fpair_ij_, fp.data(), fp.size() * sizeof(int),
+                             cudaMemcpyHostToDevice, st_),
              "H2D fpairs");
+  cuda_check(cudaStreamSynchronize(st_), "H2D tables");
   ensure_hist(std::max(cfg_.iter_limit, 64) + 1);
 }
 
@@ -344,6 +397,7 @@ Engine::~Engine() {
   sfree(st_, S_);
   sfree(st_, sa_state_);
   dfree(hist_bound_); dfree(hist_best_);
+  if (hist_t_) cudaFree(hist_t_);
   if (hSpin_) cudaFreeHost(hSpin_);
   for (void* p : peer_maps_) cudaIpcCloseMemHandle(p);
   if (comm_ && barrier_) {  // no peer may still map my receive buffers
@@ -368,19 +422,28 @@ void Engine::ensure_hist(int need) {
   if (need <= hist_cap_) return;
   int cap = std::max(need, 2 * hist_cap_);
   double *nb = nullptr, *nbest = nullptr;
+  unsigned long long* nt = nullptr;
   dalloc(&nb, cap);
   dalloc(&nbest, cap);
+  dalloc(&nt, 4 * (size_t)cap);
+  cuda_check(cudaMemsetAsync(nt, 0, 4 * (size_t)cap * sizeof(unsigned long long), st_),
+             "memset");
   if (hist_cap_) {
     cuda_check(cudaMemcpyAsync(nb, hist_bound_, hist_cap_ * 8, cudaMemcpyDeviceToDevice, st_),
                "hist");
     cuda_check(cudaMemcpyAsync(nbest, hist_best_, hist_cap_ * 8, cudaMemcpyDeviceToDevice, st_),
                "hist");
+    cuda_check(cudaMemcpyAsync(nt, hist_t_, 4 * (size_t)hist_cap_ * 8, cudaMemcpyDeviceToDevice,
+                               st_),
+               "hist");
     cuda_check(cudaStreamSynchronize(st_), "hist");
   }
   dfree(hist_bound_);
   dfree(hist_best_);
+  if (hist_t_) cudaFree(hist_t_);
   hist_bound_ = nb;
   hist_best_ = nbest;
+  hist_t_ = nt;
   hist_cap_ = cap;
   if (graph_) {  // the captured X stage writes the history arrays
     cudaGraphExecDestroy(graph_);
@@ -424,7 +487,8 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   for (int i = 0, f = 0; i < m; ++i)
     for (int j = i + 1; j < m; ++j, ++f) rb[f + 1] = rb[f] + i;
   dalloc(&rows_before_, rb.size());
-  cuda_check(cudaMemcpy(rows_before_, rb.data(), rb.size() * 4, cudaMemcpyHostToDevice), "H2D");
+  cuda_check(cudaMemcpyAsync(rows_before_, rb.data(), rb.size() * 4, cudaMemcpyHostToDevice, st_),
+             "H2D");
   shard_.rows_before = rows_before_;
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
@@ -450,7 +514,8 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
     shard_.cost_recv[p] = gr;
     shard_.d3[p] = d3;
     // sharded engines start from init_coefficients (D' = 0, rlt2.cpp:87)
-    cuda_check(cudaMemset(d3, 0, shard_cost_count(shard_, m, rank_, p) * sizeof(double)),
+    cuda_check(cudaMemsetAsync(d3, 0, shard_cost_count(shard_, m, rank_, p) * sizeof(double),
+                               st_),
                "memset d3");
     cuda_check(cudaIpcGetMemHandle(&mine[2 * p], sr), "cudaIpcGetMemHandle");
     cuda_check(cudaIpcGetMemHandle(&mine[2 * p + 1], gr), "cudaIpcGetMemHandle");
@@ -462,7 +527,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   unsigned char *dh = nullptr, *dall = nullptr;
   dalloc(&dh, hb);
   dalloc(&dall, hb * world_);
-  cuda_check(cudaMemcpy(dh, mine.data(), hb, cudaMemcpyHostToDevice), "H2D handles");
+  cuda_check(cudaMemcpyAsync(dh, mine.data(), hb, cudaMemcpyHostToDevice, st_), "H2D handles");
   nccl_check(nccl().AllGather(dh, dall, hb, ncclUint8, comm_, st_), "allgather handles");
   std::vector<cudaIpcMemHandle_t> all(2 * world_ * world_);
   cuda_check(cudaMemcpyAsync(all.data(), dall, hb * world_, cudaMemcpyDeviceToHost, st_), "D2H");
@@ -486,7 +551,9 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   dalloc(&barrier_, 1);
   dalloc(&theta_buf_, tiles_);
   dalloc(&shard_dev_, 1);
-  cuda_check(cudaMemcpy(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice), "H2D shard");
+  cuda_check(cudaMemcpyAsync(shard_dev_, &shard_, sizeof shard_, cudaMemcpyHostToDevice, st_),
+             "H2D shard");
+  cuda_check(cudaStreamSynchronize(st_), "H2D shard");
 }
 
 // Cross-rank barrier on the engine stream: after it, every rank's earlier
@@ -514,7 +581,7 @@ void Engine::enqueue_sharded_z(int it) {
     f.nchunks = chunks_me_;
     f.shard = shard_dev_;
     kbegin(QAPB_K_ZFOLD, st_);
-    cuda_check(launch_zfold(f, st_), "z-fold");
+    kcheck(launch_zfold(f, st_), "z-fold");
     kend(st_);
     kbegin(QAPB_K_XCHG, st_);
     barrier();  // costs have landed in every X3 owner's buffer
@@ -522,7 +589,7 @@ void Engine::enqueue_sharded_z(int it) {
     ++launches_;
     if (cost_scatter_) {  // into the tile layout the Z-LAPs load (else they patch per row)
       kbegin(QAPB_K_XCHG, st_);
-      cuda_check(launch_x3_cost_scatter(m_, shard_, triples_, costs, st_), "x3 cost scatter");
+      kcheck(launch_x3_cost_scatter(m_, shard_, triples_, costs, st_), "x3 cost scatter");
       kend(st_);
       ++launches_;
     }
@@ -551,12 +618,12 @@ void Engine::enqueue_sharded_z(int it) {
       p.x3_ngroups = x3_ngroups_;
     }
     kbegin(QAPB_K_ZLAP, st_);
-    cuda_check(launch_lap_batch(p, st_), "z-stage");
+    kcheck(launch_lap_batch(p, st_), "z-stage");
     kend(st_);
     ++launches_;
   }
   kbegin(QAPB_K_XCHG, st_);
-  cuda_check(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 1, st_), "theta pack");
+  kcheck(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 1, st_), "theta pack");
   nccl_check(nccl().GroupStart(), "group");
   for (int r = 0, seg = 0; r < world_; ++r) {
     const int c = fpairs_ * (shard_.pbound[r + 1] - shard_.pbound[r]) * (m_ - 1);
@@ -565,7 +632,7 @@ void Engine::enqueue_sharded_z(int it) {
     seg += c;
   }
   nccl_check(nccl().GroupEnd(), "group");
-  cuda_check(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 0, st_), "theta unpack");
+  kcheck(launch_theta_xfer(m_, theta_, theta_buf_, shard_, 0, st_), "theta unpack");
   kend(st_);
   launches_ += 2;
 }
@@ -613,7 +680,7 @@ void Engine::plan_pipeline() {
 
 void Engine::split_gather() {
   if (!split_) return;
-  cuda_check(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
+  kcheck(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
                             p_lo_, p_hi_, d_, d3_, 1, st_, ri_ ? 1 : 0),
              "x3 gather");
   d_stale_ = false;
@@ -622,7 +689,7 @@ void Engine::split_gather() {
 // the tile-layout D' of the X3 members is stale after a split fold
 void Engine::split_scatter() const {
   if (!split_ || !d_stale_) return;
-  cuda_check(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
+  kcheck(launch_x3_sync(m_, chunk_, world_ > 1 ? chunks_me_ : nchunks_, triples_, ntriples_,
                             p_lo_, p_hi_, d_, d3_, 0, st_, ri_ ? 1 : 0),
              "x3 scatter");
   cuda_check(cudaStreamSynchronize(st_), "x3 scatter");
@@ -645,6 +712,10 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
   p.theta_ref = theta_ref ? theta_ref + t0 : nullptr;
   p.err_tile = &S_->err_tile;
   p.tile_base = t0;
+  if (t0 == 0 && !theta_ref) {  // the iteration's first Z-LAP launch: z_ms starts here
+    p.tstamp = hist_t_;
+    p.iter = &S_->iter;
+  }
   if (ri_) {  // tiles by global index through the tensor maps
     p.costs = costs;
     p.pi = piz_;
@@ -652,6 +723,7 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
     p.tmap_pi = tmaps_ + 256;
   }
   if (split_) {  // X3 split (FoldParams::x3buf)
+    p.nx3 = (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_;
     p.x3buf = x3buf_;
     p.costs_w = costs + (size_t)t0 * esz;
     p.x3_group = x3_group_;
@@ -660,7 +732,7 @@ void Engine::enqueue_zlap(double* costs, int t0, int count, double* values,
     p.patch = (cur_iter_ > 0 && split_mode_ == 1) ? 1 : 0;
   }
   kbegin(QAPB_K_ZLAP, st);
-  cuda_check(launch_lap_batch(p, st), "z-stage");
+  kcheck(launch_lap_batch(p, st), "z-stage");
   kend(st);
   ++launches_;
 }
@@ -692,6 +764,12 @@ FoldParams Engine::fold_params(int stage) const {
   }
   if (f.tri0 == 0 && f.ntriples == ntriples_) f.order = order_;
   f.ri = ri_ ? 1 : 0;
+  f.nz = nd_;
+  if (split_) {
+    const int nch = world_ > 1 ? chunks_me_ : nchunks_;
+    f.nx3 = (size_t)ntriples_ * x3_ngroups_ * lpairs_ * x3_group_;
+    f.nd3 = (size_t)ntriples_ * nch * lpairs_ * chunk_;
+  }
   return f;
 }
 
@@ -707,7 +785,7 @@ void Engine::enqueue_stage_z(int it) {
       if (stage_tiles_[k] > 0) {  // z-level fold of this stage, rlt2.cpp:269-298
         const FoldParams f = fold_params(k);
         kbegin(QAPB_K_ZFOLD, st_);
-        cuda_check(launch_zfold(f, st_), "z-fold");
+        kcheck(launch_zfold(f, st_), "z-fold");
         kend(st_);
         ++launches_;
       }
@@ -724,7 +802,7 @@ void Engine::enqueue_stage_z(int it) {
     FoldParams f = fold_params(-1);
     f.costs = costs;
     kbegin(QAPB_K_PHASE2, st_);
-    cuda_check(launch_phase2(f, st_), "phase-2");
+    cuda_check(ri_ ? launch_phase2_ri(f, costs == d_, st_) : launch_phase2(f, st_), "phase-2");
     kend(st_);
     ++launches_;
     enqueue_zlap(costs, 0, tiles_, theta_, theta1_, S + 1, st_);
@@ -742,7 +820,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     return;
   }
   const bool capture = steady && it >= 2 && !graph_ && !profiling_ && world_ == 1 &&
-                       !env_flag("QAPB_NO_GRAPH");
+                       !env_flag("QAPB_NO_GRAPH") && !sync_check_enabled();
   cudaGraph_t g = nullptr;
   const long long l0 = launches_;
   if (capture)
@@ -765,7 +843,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     x.fpair_ij = fpair_ij_;
     x.stop = &S_->stop;
     kbegin(QAPB_K_XYFOLD, st_);
-    cuda_check(launch_xyfold(x, tiles_, st_), "xy-fold");
+    kcheck(launch_xyfold(x, tiles_, st_), "xy-fold");
     kend(st_);
     ++launches_;
   }
@@ -783,8 +861,10 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   y.delta = delta_;
   y.piy = piy_;
   y.stop = &S_->stop;
+  y.tstamp = hist_t_;
+  y.iter = &S_->iter;
   kbegin(QAPB_K_YSTAGE, st_);
-  cuda_check(launch_ystage(y, st_), "y-stage");
+  kcheck(launch_ystage(y, st_), "y-stage");
   kend(st_);
   ++launches_;
   XStageParams xs{};
@@ -812,11 +892,12 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
   xs.zp_lo = p_lo_;
   xs.zp_hi = p_hi_;
   xs.ri = ri_ ? 1 : 0;
+  xs.tstamp = hist_t_;
   kbegin(QAPB_K_XSTAGE, st_);
-  cuda_check(launch_xstage(xs, st_), "x-stage");
+  kcheck(launch_xstage(xs, st_), "x-stage");
   if (world_ > 1)  // feasibility needs every rank's pi(z) tiles
     nccl_check(nccl().AllReduce(feas_bad_, feas_bad_, 1, ncclInt, ncclMax, comm_, st_), "allreduce");
-  cuda_check(launch_xfinish(xs, st_), "x-finish");
+  kcheck(launch_xfinish(xs, st_), "x-finish");
   kend(st_);
   launches_ += 2;
   if (sa_dev_) {  // rlt2.cpp:521-523 on the device (kernels.cu sa_device_kernel)
@@ -828,7 +909,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     sp.kappa_cap = cfg_.sa_kappa_lb_cap;
     sp.cool_factor = cfg_.sa_cool_factor;
     sp.upper_bound = cfg_.upper_bound;
-    cuda_check(launch_sa_device(sp, b_, S_, sa_state_, sa_fac_, sa_loc_, st_), "sa step");
+    kcheck(launch_sa_device(sp, b_, S_, sa_state_, sa_fac_, sa_loc_, st_), "sa step");
     ++launches_;
   }
   if (capture) {
@@ -889,7 +970,7 @@ void Engine::sa_perturb() {
   for (int i = 0; i < m; ++i) drained += fac[i] + loc[i];
   cuda_check(cudaMemcpyAsync(sa_fac_, fac.data(), m * 8, cudaMemcpyHostToDevice, st_), "H2D sa");
   cuda_check(cudaMemcpyAsync(sa_loc_, loc.data(), m * 8, cudaMemcpyHostToDevice, st_), "H2D sa");
-  cuda_check(launch_sa_apply(m, b_, sa_fac_, sa_loc_, S_, drained, is_fast(), st_), "sa");
+  kcheck(launch_sa_apply(m, b_, sa_fac_, sa_loc_, S_, drained, is_fast(), st_), "sa");
   ++launches_;
   const int iter_before = hS_.iter - 1;  // sa_perturb runs before ++iter_
   if ((iter_before + 1) % cfg_.sa_cool_period == 0) temp_ *= cfg_.sa_cool_factor;
@@ -908,13 +989,30 @@ double Engine::iterate() {
   check_phase2();
   if (cfg_.sa_enabled && !sa_dev_ && !hS_.has_cert) sa_perturb();
   last_rec_ = qapb_record{hS_.iter, hS_.last_bound, gap(), 0, 0, 0};
-  const int k = hS_.iter - 1;
-  if ((int)stage_ms_.size() >= 3 * (k + 1)) {
-    last_rec_.z_ms = stage_ms_[3 * k];
-    last_rec_.y_ms = stage_ms_[3 * k + 1];
-    last_rec_.x_ms = stage_ms_[3 * k + 2];
-  }
+  stage_times(hS_.iter - 1, &last_rec_.z_ms, &last_rec_.y_ms, &last_rec_.x_ms);
   return hS_.last_bound;
+}
+
+// IterationRecord::{z,y,x}_ms of iteration k (0-based), as rlt2.cpp:302-448
+// times stage_z / stage_y / stage_x: the CUDA-event timings when profiling is
+// on, else the device timestamps the stage kernels store (kernels.h tstamp).
+void Engine::stage_times(int k, double* z, double* y, double* x) const {
+  if (k < 0) return;
+  if ((int)stage_ms_.size() >= 3 * (k + 1)) {
+    *z = stage_ms_[3 * k];
+    *y = stage_ms_[3 * k + 1];
+    *x = stage_ms_[3 * k + 2];
+    return;
+  }
+  if (!hist_t_ || k >= hist_cap_) return;
+  unsigned long long t[4] = {0, 0, 0, 0};
+  cuda_check(cudaMemcpy(t, hist_t_ + 4 * (size_t)k, sizeof t, cudaMemcpyDeviceToHost), "D2H t");
+  auto ms = [](unsigned long long a, unsigned long long b) {
+    return (a && b && b >= a) ? (double)(b - a) * 1e-6 : 0.0;
+  };
+  *z = ms(t[0], t[1]);
+  *y = ms(t[1], t[2]);
+  *x = ms(t[2], t[3]);
 }
 
 void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) const {
@@ -924,6 +1022,13 @@ void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) cons
              "D2H hist");
   cuda_check(cudaMemcpy(bst.data(), hist_best_ + from, (to - from) * 8, cudaMemcpyDeviceToHost),
              "D2H hist");
+  std::vector<unsigned long long> ts;  // device stage timestamps of these iterations
+  if (hist_t_ && to <= hist_cap_) {
+    ts.resize(4 * (size_t)(to - from));
+    cuda_check(cudaMemcpy(ts.data(), hist_t_ + 4 * (size_t)from, ts.size() * 8,
+                          cudaMemcpyDeviceToHost),
+               "D2H stage times");
+  }
   for (int k = from; k < to; ++k) {
     qapb_record r{};
     r.iteration = k + 1;
@@ -936,6 +1041,14 @@ void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) cons
       r.z_ms = stage_ms_[3 * k];
       r.y_ms = stage_ms_[3 * k + 1];
       r.x_ms = stage_ms_[3 * k + 2];
+    } else if (!ts.empty()) {
+      const unsigned long long* t = ts.data() + 4 * (size_t)(k - from);
+      auto ms = [](unsigned long long a, unsigned long long b) {
+        return (a && b && b >= a) ? (double)(b - a) * 1e-6 : 0.0;
+      };
+      r.z_ms = ms(t[0], t[1]);
+      r.y_ms = ms(t[1], t[2]);
+      r.x_ms = ms(t[2], t[3]);
     }
     recs->push_back(r);
   }
@@ -1031,14 +1144,14 @@ void Engine::assemble_sharded(int which, double* dst) const {
   double* src = which == QAPB_ARR_PI_Z ? piz_ : (which == QAPB_ARR_INCZ ? incz_ : d_);
   if (which == QAPB_ARR_STORE_D) {
     split_scatter();  // local split D' -> tiles
-    cuda_check(launch_shard_state_scatter(m_, shard_, triples_, d_, 0, st_), "d3 scatter");
+    kcheck(launch_shard_state_scatter(m_, shard_, triples_, d_, 0, st_), "d3 scatter");
   } else if (which == QAPB_ARR_INCZ && hS_.iter >= 2) {  // a fold has stored costs
-    cuda_check(launch_shard_state_scatter(m_, shard_, triples_, incz_, 1, st_), "cost scatter");
+    kcheck(launch_shard_state_scatter(m_, shard_, triples_, incz_, 1, st_), "cost scatter");
   }
   unsigned long long* buf = nullptr;
   cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), nd_ * sizeof(double), st_),
              "cudaMallocAsync");
-  cuda_check(launch_shard_state_mask(m_, shard_, src, buf, which == QAPB_ARR_STORE_D ? 1 : 0, st_),
+  kcheck(launch_shard_state_mask(m_, shard_, src, buf, which == QAPB_ARR_STORE_D ? 1 : 0, st_),
              "state mask");
   nccl_check(nccl().AllReduce(buf, buf, nd_, ncclUint64, ncclSum, comm_, st_), "assemble");
   cuda_check(cudaMemcpyAsync(dst, buf, nd_ * sizeof(double), cudaMemcpyDefault, st_), "D2H");
@@ -1076,13 +1189,19 @@ void Engine::get_array(int which, double* dst, size_t count) const {
     double* tmp = nullptr;
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(double), st_),
                "cudaMallocAsync");
-    cuda_check(launch_z_relayout(m_, src, tmp, 0, st_), "relayout");
+    kcheck(launch_z_relayout(m_, src, tmp, 0, st_), "relayout");
     cuda_check(cudaMemcpyAsync(dst, tmp, n * sizeof(double), cudaMemcpyDefault, st_), "D2H array");
     cuda_check(cudaFreeAsync(tmp, st_), "cudaFreeAsync");
     cuda_check(cudaStreamSynchronize(st_), "D2H array");
     return;
   }
-  if (n) cuda_check(cudaMemcpy(dst, src, n * sizeof(double), cudaMemcpyDefault), "D2H array");
+  // on the engine's stream and completed before return: dst may be device
+  // memory (a device store), where a legacy-stream copy would return early
+  if (n) {
+    cuda_check(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, st_),
+               "D2H array");
+    cuda_check(cudaStreamSynchronize(st_), "D2H array");
+  }
 }
 
 // ---- measurement hooks ---------------------------------------------------
@@ -1177,13 +1296,13 @@ double Engine::time_kernel(int kind, int reps) {
     switch (kind) {
       case QAPB_K_ZFOLD: {
         FoldParams f = fold_params(-1);
-        cuda_check(launch_zfold(f, st_), "z-fold");
+        kcheck(launch_zfold(f, st_), "z-fold");
         break;
       }
       case QAPB_K_PHASE2: {
         FoldParams f = fold_params(-1);
         f.costs = costs;
-        cuda_check(launch_phase2(f, st_), "phase-2");
+        kcheck(launch_phase2(f, st_), "phase-2");
         break;
       }
       case QAPB_K_ZLAP:

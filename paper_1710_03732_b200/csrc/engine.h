@@ -182,7 +182,10 @@ class Engine {
   int *fpair_ij_ = nullptr, *counter_ = nullptr;  // counter_: one per Z launch
   DevScalars* S_ = nullptr;
   double *hist_bound_ = nullptr, *hist_best_ = nullptr;
+  unsigned long long* hist_t_ = nullptr;  // 4 device timestamps per iteration (kernels.h)
   int hist_cap_ = 0;
+  void stage_times(int k, double* z, double* y, double* x) const;
+  void kcheck(cudaError_t e, const char* what) const;
   DevScalars* hSpin_ = nullptr;  // pinned mirror for async copies
   DevScalars hS_{};
   std::mt19937_64 rng_;  // host SA (QAPB_HOST_SA=1); the device SA keeps its own state

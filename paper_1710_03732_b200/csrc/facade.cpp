@@ -206,40 +206,75 @@ QAP_API StoreIndex::StoreIndex(int m_) : m(m_) {
       }
 }
 
-QAP_API CoefficientStore init_coefficients(const QapInstance& inst) {
-  if (inst.n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
-  const int m = inst.n;
+namespace {
+int bank_device(int requested);
+
+std::shared_ptr<qapb_store> own_store(qapb_store* p) {
+  return std::shared_ptr<qapb_store>(p, [](qapb_store* q) { qapb_store_destroy(q); });
+}
+
+// A store in HBM with host-empty b, c, d (rlt2.hpp CoefficientStore::device)
+CoefficientStore device_store(qapb_store* p, int m, double offset) {
   CoefficientStore st;
   st.m = m;
   st.idx = StoreIndex(m);
-  st.b.resize((size_t)m * m);
-  st.c.resize(nc_of(m));
-  st.d.assign(nd_of(m), 0.0);
-  const double* lin = inst.linear.empty() ? nullptr : inst.linear.data();
-  check(qapb_init_coefficients(m, inst.flow.data(), inst.dist.data(), lin, st.b.data(),
-                               st.c.data(), nullptr));
+  st.offset = offset;
+  st.device = own_store(p);
   return st;
 }
 
+// the store as a device store (uploads a host store)
+std::shared_ptr<qapb_store> on_device(const CoefficientStore& st, int device) {
+  if (st.device) return st.device;
+  qapb_store* p = nullptr;
+  check(qapb_store_upload(st.m, st.b.data(), st.c.data(), st.m >= 3 ? st.d.data() : nullptr,
+                          st.offset, device, &p));
+  return own_store(p);
+}
+}  // namespace
+
+// rlt2.cpp:66-89: built in HBM by the init kernel (D' = 0), kept there
+QAP_API CoefficientStore init_coefficients(const QapInstance& inst) {
+  if (inst.n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
+  const double* lin = inst.linear.empty() ? nullptr : inst.linear.data();
+  qapb_store* p = nullptr;
+  check(qapb_store_init(inst.n, inst.flow.data(), inst.dist.data(), lin, bank_device(0), &p));
+  return device_store(p, inst.n, 0.0);
+}
+
+QAP_API CoefficientStore& host_view(CoefficientStore& st) {
+  if (!st.device) return st;
+  st.b.resize((size_t)st.m * st.m);
+  st.c.resize(nc_of(st.m));
+  st.d.resize(nd_of(st.m));
+  double off = 0;
+  check(qapb_store_download(st.device.get(), st.b.data(), st.c.data(), st.d.data(), &off));
+  return st;
+}
+
+// rlt2.cpp:91-107, on the device (terms in the reference's order)
 QAP_API double store_evaluate(const CoefficientStore& st, const std::vector<int>& perm) {
   double v = 0;
-  check(qapb_store_evaluate(st.m, st.b.data(), st.c.data(), st.d.data(), st.offset, perm.data(),
-                            &v));
+  if (st.device) {
+    check(qapb_store_evaluate_device(st.device.get(), st.offset, perm.data(), &v));
+  } else {
+    check(qapb_store_evaluate(st.m, st.b.data(), st.c.data(), st.d.data(), st.offset,
+                              perm.data(), &v));
+  }
   return v;
 }
 
+// rlt2.cpp:109-182, device to device; the child stays in HBM
 QAP_API CoefficientStore collapse_store(const CoefficientStore& st, int fac, int loc) {
   const int mc = st.m - 1;
   if (mc < 2) throw std::invalid_argument("collapse_store: store too small");
-  CoefficientStore out;
-  out.m = mc;
-  out.idx = StoreIndex(mc);
-  out.b.resize((size_t)mc * mc);
-  out.c.resize(nc_of(mc));
-  out.d.assign(nd_of(mc), 0.0);
-  check(qapb_collapse_store(st.m, st.b.data(), st.c.data(), st.d.data(), st.offset, fac, loc,
-                            out.b.data(), out.c.data(), out.d.data(), &out.offset));
-  return out;
+  std::shared_ptr<qapb_store> src = on_device(st, bank_device(0));
+  qapb_store* p = nullptr;
+  check(qapb_store_collapse_offset(src.get(), st.offset, fac, loc, &p));
+  int m = 0;
+  double off = 0;
+  check(qapb_store_info(p, &m, &off));  // st.offset + b[fac, loc] (rlt2.cpp:116)
+  return device_store(p, mc, off);
 }
 
 QAP_API bool redistribute_family(const double pi[3], double add[3], int virtual_slots,
@@ -279,6 +314,15 @@ QAP_API AscentEngine::AscentEngine(CoefficientStore store, const AscentConfig& c
   if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");
   cfg_.device = bank_device(cfg.device);
   const qapb_config c = to_c(cfg_);
+  if (store.device) {  // device-to-device (snapshots, collapsed children, init_coefficients)
+    int dev = -1;
+    check(qapb_store_device(store.device.get(), &dev));
+    if (dev == cfg_.device) {
+      check(qapb_engine_create_from_store_offset(store.device.get(), store.offset, &c, &h_));
+      return;
+    }
+    host_view(store);  // another GPU: through the host
+  }
   check(qapb_engine_create(store.m, store.b.data(), store.c.data(), store.d.data(), store.offset,
                            &c, &h_));
 }
@@ -358,15 +402,31 @@ QAP_API const CoefficientStore& AscentEngine::store() const {
   return st_;
 }
 
+// rlt2.cpp:537-542, kept in HBM (std::logic_error for F variants).  A search
+// tree can hold many snapshots at once (bnb.cpp keeps each branching node's
+// store for its children, also while they wait in the master heap): when the
+// device has less than a quarter of its memory free, the snapshot goes to the
+// host instead (host-resident store; collapse_store uploads it again).
 QAP_API CoefficientStore AscentEngine::snapshot() const {
-  CoefficientStore s;
-  s.m = m_;
-  s.idx = StoreIndex(m_);
-  s.b.resize((size_t)m_ * m_);
-  s.c.resize(nc_of(m_));
-  s.d.resize(nd_of(m_));
-  check(qapb_engine_snapshot(h_, s.b.data(), s.c.data(), s.d.data(), &s.offset));
-  return s;
+  size_t free_b = 0, total_b = 0;
+  check(qapb_device_memory(cfg_.device, &free_b, &total_b));
+  const size_t need = (nc_of(m_) + nd_of(m_) + (size_t)m_ * m_) * sizeof(double);
+  if (free_b < total_b / 4 + need || std::getenv("QAPB_SNAPSHOT_HOST")) {
+    CoefficientStore s;
+    s.m = m_;
+    s.idx = StoreIndex(m_);
+    s.b.resize((size_t)m_ * m_);
+    s.c.resize(nc_of(m_));
+    s.d.resize(nd_of(m_));
+    check(qapb_engine_snapshot(h_, s.b.data(), s.c.data(), s.d.data(), &s.offset));
+    return s;
+  }
+  qapb_store* p = nullptr;
+  check(qapb_store_from_engine(h_, &p));
+  int m = 0;
+  double off = 0;
+  check(qapb_store_info(p, &m, &off));
+  return device_store(p, m, off);
 }
 
 QAP_API bool AscentEngine::has_certificate() const { return !certificate().empty(); }

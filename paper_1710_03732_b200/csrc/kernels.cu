@@ -581,6 +581,9 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       if (rel12[k] == 0xffffffffu) continue;
       const int e = tid + k * bd;
       const uint32_t o1 = tb1 + rel12[k], o2 = tb2 + rel12[k];
+      QAPB_CHECK(o1 < P.nz && o2 < P.nz, "lean o12", o1 > o2 ? o1 : o2, P.nz);
+      QAPB_CHECK((fi12[k] & 0xffffu) < (unsigned)cube && (fi12[k] >> 16) < (unsigned)cube,
+                 "lean fi12", fi12[k], cube);
       cp_async8(S + (fi12[k] & 0xffffu), piz + o1);
       cp_async8(V + e, d + o1);
       cp_async8(S + cube + (fi12[k] >> 16), piz + o2);
@@ -603,6 +606,9 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
           continue;
         }
       }
+      QAPB_CHECK(upi + pr * G + pl < P.nx3, "lean x3buf", upi + pr * G + pl, P.nx3);
+      QAPB_CHECK(ub + pr * C + pl < P.nd3, "lean d3", ub + pr * C + pl, P.nd3);
+      QAPB_CHECK((x3a[k] & 0xfffu) < (unsigned)cube, "lean x3 fi", x3a[k] & 0xfffu, cube);
       cp_async8(S + 2 * cube + (x3a[k] & 0xfffu), x3buf + upi + pr * G + pl);
       cp_async8(V + base3 + e, d3 + ub + pr * C + pl);
     }
@@ -664,6 +670,7 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       }
       d3[ub + pair * C + pl] = dn;
       const uint32_t o = tb3 + pair * esz + ((x3a[k] >> 12) & 63u);
+      QAPB_CHECK(o < P.nz, "lean x3 store", o, P.nz);
       if (fast)
         incz[o] = dadd(dmul(omk, p3), gain);
       else
@@ -1446,6 +1453,87 @@ __global__ void __launch_bounds__(256) phase2_kernel(FoldParams P) {
   });
 }
 
+// Phase 2 (rlt2.cpp:344-381) on the RI layout with the X3 split: one CTA per
+// fold unit (triple, pa chunk).  pi(z) of the X1 / X2 rows (contiguous RI
+// blocks) and of the X3 members (fold order, x3buf) is staged with cp.async;
+// each thread then updates the solve cost of its own cells with its family's
+// add[s] + share (redistribute_family + the mirror shares, rlt2.cpp:360-378),
+// the family triple ordered (X1, X2, X3) = (A, B, C) as the reference's.
+template <int C>
+__global__ void __launch_bounds__(kWsCT) phase2_ri_kernel(FoldParams P, int costs_are_d) {
+  if (P.stop && *P.stop) return;
+  extern __shared__ __align__(16) double sm[];
+  const int n = P.m, nm1 = n - 1, nm2 = n - 2, lpairs = n * nm1;
+  const int R = n, nrows = C * nm1, c3 = lpairs * C, nch = P.nchunks;
+  double* P1 = sm;
+  double* P2 = sm + nrows * R;
+  double* P3 = sm + 2 * nrows * R;
+  const int unit = blockIdx.x, T = unit / nch, ch = unit - T * nch, pa0 = ch * C;
+  const int tid = threadIdx.x;
+  const DIdx ix(n);
+  const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+  const uint32_t tb1 = ((uint32_t)(ix.fpair(a, b) * nm2 + c - 2) * lpairs + pa0 * nm1) * nm2;
+  const uint32_t tb2 = ((uint32_t)(ix.fpair(a, c) * nm2 + b - 1) * lpairs + pa0 * nm1) * nm2;
+  const uint32_t tb3 = (uint32_t)(ix.fpair(b, c) * nm2 + a) * lpairs * nm2;
+  const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;
+  const int Gx = P.x3_group, g0 = pa0 / Gx;
+  const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx + (pa0 - g0 * Gx);
+  const int pr = nm2 / 2;  // 16-byte pieces per row
+  for (int v = tid; v < 2 * nrows * pr; v += blockDim.x) {
+    const int rr = v / pr, x = v - rr * pr, arr = rr >= nrows, row = rr - arr * nrows;
+    cp_async16((arr ? P2 : P1) + row * R + 2 * x, P.piz + (arr ? tb2 : tb1) + row * nm2 + 2 * x);
+  }
+  for (int e = tid; e < lpairs; e += blockDim.x) {
+    if constexpr (C == 2)
+      cp_async16(P3 + e * C, P.x3buf + upi + (size_t)e * Gx);
+    else
+      cp_async8(P3 + e, P.x3buf + upi + (size_t)e * Gx);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  WsCells cells;
+  ws_cells<C, true>(cells, n, pa0, tid, R);
+  const double tol = 1e-9;
+  // cost += add[own] + share for the family (p1, p2, p3) = (X1, X2, X3)
+  auto delta = [&](double p1, double p2, double p3, int own) {
+    double total = 0.0;
+    int nb = 3;
+    if (p1 > tol) total = dadd(total, p1); else ++nb;
+    if (p2 > tol) total = dadd(total, p2); else ++nb;
+    if (p3 > tol) total = dadd(total, p3); else ++nb;
+    const double share = __ddiv_rn(total, (double)nb);
+    const double po = own == 0 ? p1 : (own == 1 ? p2 : p3);
+    const double add = (total <= 0.0) ? 0.0 : ((po > tol) ? -po : share);
+    return dadd(add, share);
+  };
+  double* __restrict__ costs = P.costs;
+#pragma unroll
+  for (int k = 0; k < kPipeSlots; ++k) {
+    if (cells.rel[k] == 0xffffffffu) continue;
+    const uint32_t r = cells.rel[k] & 0x3fffffu;
+    const uint32_t so = cells.sm[k] & 0xffffu, sp = cells.sm[k] >> 16;
+    const uint32_t l1 = cells.l12[k] & 0xffffu, l2 = cells.l12[k] >> 16;
+    costs[tb1 + r] = dadd(costs[tb1 + r], delta(P1[so], P2[sp], P3[l1], 0));  // X1
+    costs[tb2 + r] = dadd(costs[tb2 + r], delta(P1[sp], P2[so], P3[l2], 1));  // X2
+  }
+#pragma unroll
+  for (int k = 0; k < kPipeSlots; ++k) {
+    if (cells.x3b[k] == 0xffffffffu) continue;
+    const int e = tid + k * kWsCT;
+    const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
+    const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
+    const uint32_t o = tb3 + pair * nm2 + col;
+    const double dl = delta(P1[i1], P2[i2], P3[e], 2);
+    if (costs_are_d) {  // D' of the X3 members: d3 is authoritative, the tile copy follows
+      const double v = dadd(P.d3[ub + e], dl);
+      P.d3[ub + e] = v;
+      costs[o] = v;
+    } else {
+      costs[o] = dadd(costs[o], dl);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Batched LAPs, one warp per LAP (Z stage and the public batch API).
 // Persistent CTAs; each warp pulls tiles from a global counter and
@@ -1522,16 +1610,19 @@ __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, i
   const int lo = min(pb, pc), hi = max(pb, pc);
   tb = c3u(n) - (n - b) * (n - b - 1) / 2 + (c - b - 1);
   const int G = P.x3_group;
+  const size_t gstride = (size_t)P.x3_ngroups * lpairs * G;
 #pragma unroll
   for (int s = 0; s < CPL; ++s) {
     const int j = lap_col<CPL>(s, lane);
     X[s].gsrc = nullptr;
     X[s].sdst = nullptr;
     if (j >= m) continue;
-    const int pa = skip2(j, lo, hi), g = pa / G;
-    X[s].sdst = P.x3buf + ((size_t)g * lpairs + lp) * G + (pa - g * G);
+    const int pa = skip2(j, lo, hi);
+    // slot ((g*lpairs + lp)*G + pa%G), g = pa/G: shifts for the usual G = 4
+    const int g = G == 4 ? (pa >> 2) : pa / G, pr = G == 4 ? (pa & 3) : pa - g * G;
+    X[s].sdst = P.x3buf + ((size_t)g * lpairs + lp) * G + pr;
     X[s].gsrc = X[s].sdst;
-    X[s].gstride = (size_t)P.x3_ngroups * lpairs * G;
+    X[s].gstride = gstride;
   }
 }
 
@@ -1545,6 +1636,8 @@ template <int CPL, int MODE>
 __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchLapParams P, unsigned warp_smem,
                                                         int buf_elems, int flags, int nbuf) {
   if (P.stop && *P.stop) return;
+  if (P.tstamp && blockIdx.x == 0 && threadIdx.x == 0)
+    P.tstamp[4 * (size_t)*P.iter] = globaltimer_ns();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool use_bulk = flags & 1, store_bulk = flags & 2;
@@ -1673,8 +1766,18 @@ __global__ void __launch_bounds__(256, CPL == 1 ? 4 : 1) lap_batch_kernel(BatchL
             const double sl = cb[a * m + j];
             if constexpr (MODE == 1)  // peer row segment, or the local split slot (nA == 0)
               X[s].sdst[X[s].nA ? (size_t)a * X[s].nA : (size_t)T * X[s].gstride] = sl;
-            else
+            else {
+#ifdef QAPB_BOUNDS
+              if ((size_t)(X[s].sdst + (size_t)T * X[s].gstride - P.x3buf) >= P.nx3) {
+                printf("QAPB_BOUNDS lap x3 emit: n=%d tg=%d base=%d xb=%d tb=%d a=%d T=%d "
+                       "gstride=%llu base_off=%lld count=%d\n",
+                       m + 2, tg, P.tile_base, xb, tb, a, T, (unsigned long long)X[s].gstride,
+                       (long long)(X[s].sdst - P.x3buf), P.count);
+                __trap();
+              }
+#endif
               X[s].sdst[(size_t)T * X[s].gstride] = sl;
+            }
           }
           T += k * (k - 1) / 2;  // C(n-a-2, 2)
           --k;
@@ -1857,6 +1960,8 @@ __global__ void __launch_bounds__(256) lap_block_kernel(BatchLapParams P) {
 template <int CPL>
 __global__ void __launch_bounds__(128) ystage_kernel(YStageParams P, int warps_per_block) {
   if (P.stop && *P.stop) return;
+  if (P.tstamp && blockIdx.x == 0 && threadIdx.x == 0)
+    P.tstamp[4 * (size_t)*P.iter + 1] = globaltimer_ns();
   extern __shared__ double ysm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int m = P.m, my = m - 1;
@@ -1897,6 +2002,7 @@ template <int CPL>
 __global__ void __launch_bounds__(1024) xstage_kernel(XStageParams P) {
   DevScalars* S = P.S;
   if (S->stop) return;
+  if (P.tstamp && threadIdx.x == 0) P.tstamp[4 * (size_t)S->iter + 2] = globaltimer_ns();
   extern __shared__ double xsm[];
   __shared__ int feas_bad;
   __shared__ int sx[128];
@@ -1942,6 +2048,8 @@ __global__ void __launch_bounds__(1024) xstage_kernel(XStageParams P) {
       const int i = e / (m * m), rem = e - i * m * m, j = rem / m, k = rem - j * m;
       if (!(i < j) || k == i || k == j) continue;
       if (sx[i] < P.zp_lo || sx[i] >= P.zp_hi) continue;  // tile held by another rank
+      QAPB_CHECK(sx[i] != sx[j] && sx[i] >= 0 && sx[i] < m && sx[j] >= 0 && sx[j] < m,
+                 "xstage sx", sx[i], sx[j]);
       const int t = ix.tile(i, j, sx[i], sx[j]);
       const int cl = ix.cell(i, j, sx[i], sx[j], k, sx[k]);
       const size_t o = P.ri ? z_ri_offset(m, (size_t)t, cl / (m - 2), cl % (m - 2))
@@ -1972,6 +2080,7 @@ __global__ void xfinish_kernel(XStageParams P) {
     const int it = S->iter;
     P.hist_bound[it] = S->last_bound;
     P.hist_best[it] = S->best;
+    if (P.tstamp) P.tstamp[4 * (size_t)it + 3] = globaltimer_ns();
     S->iter = it + 1;
     S->sa_pending = 1;  // the device SA step (if any) follows this iteration
     if (S->run_mode) {
@@ -2495,6 +2604,21 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
   }
   allow_max_smem(zfold_kernel);
   zfold_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t st) {
+  if (p.ntriples <= 0) return cudaSuccess;
+  const int n = p.m, C = p.chunk;
+  const size_t smem = (size_t)(2 * C * (n - 1) * n + n * (n - 1) * C) * sizeof(double);
+  const int units = p.ntriples * p.nchunks;
+  if (C == 2) {
+    allow_max_smem(phase2_ri_kernel<2>);
+    phase2_ri_kernel<2><<<units, kWsCT, smem, st>>>(p, costs_are_d ? 1 : 0);
+  } else {
+    allow_max_smem(phase2_ri_kernel<1>);
+    phase2_ri_kernel<1><<<units, kWsCT, smem, st>>>(p, costs_are_d ? 1 : 0);
+  }
   return cudaGetLastError();
 }
 

@@ -79,6 +79,12 @@ struct BatchLapParams {
   // pi are then base pointers and tile_base + t the global tile index)
   const void* tmap_cost;
   const void* tmap_pi;
+  size_t nx3;  // element count of x3buf (bounds checks of a -DQAPB_BOUNDS build)
+  // per-stage device timestamps (IterationRecord::z_ms, rlt2.cpp:302,337):
+  // block 0 of the iteration's first Z-LAP launch stores %globaltimer in
+  // tstamp[4 * *iter + 0]
+  unsigned long long* tstamp;
+  const int* iter;
 };
 
 constexpr int kMaxRanks = 8;
@@ -164,6 +170,8 @@ struct FoldParams {
   // z arrays (d, piz, incz) in the row-interleaved device layout (see
   // z_ri_offset below) instead of the reference tile layout
   int ri;
+  // element counts of d / x3buf / d3 (bounds checks of a -DQAPB_BOUNDS build)
+  size_t nz, nx3, nd3;
 };
 
 // Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
@@ -208,6 +216,8 @@ struct YStageParams {
   double* delta;
   double* piy;
   const int* stop;
+  unsigned long long* tstamp;  // [4 * *iter + 1]: Y stage start (rlt2.cpp:384)
+  const int* iter;
 };
 
 struct XStageParams {
@@ -229,6 +239,7 @@ struct XStageParams {
   int* feas_bad;           // device flag: 1 if any induced slack > 1e-7
   int zp_lo, zp_hi;        // first locations of the pi(z) tiles this rank checks
   int ri;                  // pi(z) in the RI layout (z_ri_offset)
+  unsigned long long* tstamp;  // [4 * iter + 2]: X stage start, [+3]: its end (rlt2.cpp:429,448)
 };
 
 // ---- launches (all asynchronous on `st`) ----
@@ -237,6 +248,10 @@ cudaError_t launch_init_store(int n, const double* flow, const double* dist,
 cudaError_t launch_xyfold(const XYFoldParams& p, int tiles, cudaStream_t st);
 cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st);
 cudaError_t launch_phase2(const FoldParams& p, cudaStream_t st);
+// phase 2 on the RI + X3-split layout (single GPU); costs_are_d: the solve
+// costs are the store's D' (S variants, and iteration 0), whose X3 members
+// also live in d3
+cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t st);
 // Z-stage and the public batch API: one warp per LAP, TMA bulk tile loads.
 cudaError_t launch_lap_batch(const BatchLapParams& p, cudaStream_t st);
 cudaError_t launch_ystage(const YStageParams& p, cudaStream_t st);

@@ -125,22 +125,29 @@ __device__ __forceinline__ int bfind_u32(unsigned x) {
   return r;
 }
 
-// True (warp-uniform) iff every cost is finite with |c| <= 1e300: the fast
-// solvers then never meet inf/NaN (|u|,|v| stay below 2m * 1e300).
+// True (warp-uniform) iff every cost is finite with |c| < 2^997 (~1.3e300):
+// the fast solvers then never meet inf/NaN (|u|,|v| stay below 2m * 2^997).
+// Which tiles take the safe solver does not change any result -- both do the
+// same arithmetic when nothing overflows -- so the test only has to be
+// sufficient: an integer max over the high words (sign dropped) of the
+// exponent/mantissa, two integer ops per element.
 __device__ __forceinline__ bool lap_tile_finite(const double* __restrict__ cost, int m, int lane) {
-  bool ok = true;
+  constexpr unsigned kLimit = 0x7E400000u;  // high word of 2^997
+  unsigned mx = 0;
   const int mm = m * m;
   if ((reinterpret_cast<uintptr_t>(cost) & 15) == 0) {  // Z tiles: 16-byte reads
-    const double2* __restrict__ c2 = reinterpret_cast<const double2*>(cost);
+    const uint4* __restrict__ c4 = reinterpret_cast<const uint4*>(cost);
     for (int e = lane; e < (mm >> 1); e += 32) {
-      const double2 x = c2[e];
-      ok = ok && (fabs(x.x) <= 1e300) && (fabs(x.y) <= 1e300);
+      const uint4 x = c4[e];  // {lo0, hi0, lo1, hi1}
+      mx = max(mx, max(x.y & 0x7fffffffu, x.w & 0x7fffffffu));
     }
-    if ((mm & 1) && lane == 0) ok = ok && (fabs(cost[mm - 1]) <= 1e300);
+    if ((mm & 1) && lane == 0)
+      mx = max(mx, (unsigned)(__double_as_longlong(cost[mm - 1]) >> 32) & 0x7fffffffu);
   } else {
-    for (int e = lane; e < mm; e += 32) ok = ok && (fabs(cost[e]) <= 1e300);
+    for (int e = lane; e < mm; e += 32)
+      mx = max(mx, (unsigned)(__double_as_longlong(cost[e]) >> 32) & 0x7fffffffu);
   }
-  return __all_sync(QAPB_FULL, ok);
+  return __reduce_max_sync(QAPB_FULL, mx) < kLimit;
 }
 
 // value = sum_j cost[p[j]][j] in column order from 0.0 (lap.cpp:75-80).

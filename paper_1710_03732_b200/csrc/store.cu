@@ -231,6 +231,11 @@ DeviceStore::~DeviceStore() {
 void DeviceStore::synchronize() const { check(cudaStreamSynchronize(stream), "store stream"); }
 
 std::unique_ptr<DeviceStore> collapse_store_device(const DeviceStore& s, int fac, int loc) {
+  return collapse_store_device(s, fac, loc, s.offset);
+}
+
+std::unique_ptr<DeviceStore> collapse_store_device(const DeviceStore& s, int fac, int loc,
+                                                   double offset) {
   const int m = s.m, mc = m - 1;
   if (mc < 2) throw std::invalid_argument("collapse_store: store too small");  // rlt2.cpp:111
   if (fac < 0 || fac >= m || loc < 0 || loc >= m)
@@ -256,11 +261,11 @@ std::unique_ptr<DeviceStore> collapse_store_device(const DeviceStore& s, int fac
     check(cudaGetLastError(), "collapse d");
   }
   out->synchronize();
-  out->offset = s.offset + bfl;  // rlt2.cpp:116
+  out->offset = offset + bfl;  // rlt2.cpp:116
   return out;
 }
 
-double store_evaluate_device(const DeviceStore& s, const int* perm) {
+double store_evaluate_device(const DeviceStore& s, const int* perm, double offset) {
   const int m = s.m;
   if (m < 3) throw std::invalid_argument("store_evaluate: m >= 3 required");
   DeviceGuard g(s.device);
@@ -275,7 +280,7 @@ double store_evaluate_device(const DeviceStore& s, const int* perm) {
   store_terms_kernel<<<std::max(1, std::min(4 * sms(), (count + 255) / 256)), 256, 0, s.stream>>>(
       m, s.b, s.c, s.d, dperm, terms);
   check(cudaGetLastError(), "store terms");
-  ordered_sum_kernel<<<1, 1, 0, s.stream>>>(terms, count, s.offset, dv);
+  ordered_sum_kernel<<<1, 1, 0, s.stream>>>(terms, count, offset, dv);
   check(cudaGetLastError(), "ordered sum");
   double v = 0.0;
   check(cudaMemcpyAsync(&v, dv, sizeof(double), cudaMemcpyDeviceToHost, s.stream), "D2H");

@@ -29,8 +29,11 @@ struct DeviceStore {
 
 // collapse_store, rlt2.cpp:109-182, bitwise, on the store's device
 std::unique_ptr<DeviceStore> collapse_store_device(const DeviceStore& s, int fac, int loc);
+// the same with the parent's constant term given (the child's is offset + b[fac, loc])
+std::unique_ptr<DeviceStore> collapse_store_device(const DeviceStore& s, int fac, int loc,
+                                                   double offset);
 // store_evaluate, rlt2.cpp:91-107, bitwise (terms in the reference's order)
-double store_evaluate_device(const DeviceStore& s, const int* perm);
+double store_evaluate_device(const DeviceStore& s, const int* perm, double offset);
 // redistribute_family, rlt2.cpp:184-205
 bool redistribute_family_device(const double pi[3], double add[3], int virtual_slots, double tol,
                                 int device);

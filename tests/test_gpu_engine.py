@@ -75,7 +75,8 @@ FOLD_VARIANTS = {
 
 
 @pytest.mark.parametrize("fold", sorted(FOLD_VARIANTS))
-@pytest.mark.parametrize("key", ["nug12_F1", "nug12_S1", "rand20_F1", "nug12_F1_SA"])
+@pytest.mark.parametrize("key", ["nug12_F1", "nug12_S1", "rand20_F1", "nug12_F1_SA", "nug12_F2",
+                                 "nug12_S2", "nug12_F2_SA"])
 def test_fold_variants_bitwise(q, golden, key, fold, monkeypatch):
     monkeypatch.setenv("QAPB_FOLD_CHUNK", "2")  # n even, chunk 2: the pipelined fold
     for k, v in FOLD_VARIANTS[fold].items():

@@ -42,6 +42,7 @@ int main(int argc, char** argv) {
   qap::BnbConfig cfg;
   cfg.banks = argc > next ? std::atoi(argv[next]) : 1;
   cfg.node_iter_limit = argc > next + 1 ? std::atoi(argv[next + 1]) : 500;
+  if (const char* sa = std::getenv("BNB_SA")) cfg.sa_enabled = std::atoi(sa) != 0;
   const auto t0 = std::chrono::steady_clock::now();
   const qap::BnbResult r = qap::branch_and_bound(inst, cfg);
   const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
