@@ -39,18 +39,30 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 GRID_SHAPES = {12: (3, 4), 20: (4, 5), 30: (5, 6), 42: (6, 7)}
 
 
-def workload(n: int):
+def workload(n: int, shape: str = "grid"):
+    """nug{n}-shaped (grid) or tai{n}a-shaped (rand: generate_instance(n, 1, 99))."""
+    if shape == "rand":
+        from paper_1710_03732_b200.instance import generate_instance
+        return generate_instance(n, 1, 99)
     from paper_1710_03732_b200.instance import grid_instance
     r, c = GRID_SHAPES[n]
     return grid_instance(r, c, flow_seed=1, max_flow=10, name=f"nug{n}-shaped")
 
 
-def workload_reference(orc, n: int):
+def shape_name(args) -> str:
+    if args.shape == "rand":
+        return f"tai{args.n}a-shaped (generate_instance({args.n}, 1, 99): U{{0..99}} flows and distances)"
+    return f"nug{args.n}-shaped (Manhattan grid, flows U{{0..10}} seed 1)"
+
+
+def workload_reference(orc, n: int, shape: str = "grid"):
     """The same nug{n}-shaped instance built without importing the product
     package: flows from the reference's own generate_instance(n, 1, 10)
     (instance.cpp:131-150, via oracle/_ref), Manhattan grid distances as
     tests/test_bnb.cpp:35-44 grid_instance."""
     import numpy as np
+    if shape == "rand":
+        return orc.generate_instance(n, 1, 99)
     r, c = GRID_SHAPES[n]
     flow, _ = orc.generate_instance(n, 1, 10)
     a = np.arange(n)
@@ -96,10 +108,12 @@ def kernel_bytes(n: int, variant: str):
     }
 
 
-def iteration_bytes(n: int):
-    """B = 32 N_z + 32 N_y + 16 tiles per 1-phase iteration."""
+def iteration_bytes(n: int, variant: str = "F1"):
+    """SURVEY.md §8(d): B = 32 N_z + 32 N_y + 16 tiles per 1-phase iteration;
+    2-phase variants (F2/S2) add 32 N_z (pi_1 write + read, cost read + write)."""
     s = sizes(n)
-    return 32 * s["n_z"] + 32 * s["n_y"] + 16 * s["tiles"]
+    b = 32 * s["n_z"] + 32 * s["n_y"] + 16 * s["tiles"]
+    return b + (32 * s["n_z"] if variant.upper().endswith("2") else 0)
 
 
 def peaks():
@@ -166,7 +180,7 @@ class ClockSampler:
                 if any(r[3].replace(".", "").isdigit() for r in rows) else None}
 
 
-def cpu_reference_run(n, variant, warmup, steps, threads=None):
+def cpu_reference_run(n, variant, warmup, steps, threads=None, shape="grid"):
     """Time the reference CPU implementation (oracle/_ref; the C port if the
     reference build is absent) on this host: engine built untimed, `warmup`
     untimed iterations, then `steps` timed iterations.  Returns (it/s, kind,
@@ -177,7 +191,7 @@ def cpu_reference_run(n, variant, warmup, steps, threads=None):
     threads = threads or os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     orc = Oracle(kind)
-    flow, dist = workload_reference(orc, n)
+    flow, dist = workload_reference(orc, n, shape)
     eng = orc.engine_from_instance(flow, dist, cfg=default_config(
         variant=variant, iter_limit=10 ** 6, workers=threads, record_history=0))
     for _ in range(warmup):
@@ -200,7 +214,8 @@ def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    its, kind, threads, dt = cpu_reference_run(args.n, args.variant, args.warmup, args.steps)
+    its, kind, threads, dt = cpu_reference_run(args.n, args.variant, args.warmup, args.steps,
+                                               shape=args.shape)
     s = sizes(args.n)
     laps = s["tiles"] + args.n * args.n + 1
     line = {
@@ -227,8 +242,8 @@ def run_reference_arm(args):
 
 def config_block(args, world, sharded=False):
     s = sizes(args.n)
-    return {"workload": f"nug{args.n}-shaped (Manhattan grid, flows U{{0..10}} seed 1), "
-                        f"variant {args.variant}, SA off, steady-state iterations",
+    return {"workload": f"{shape_name(args)}, variant {args.variant}, SA off, steady-state "
+                        "iterations",
             "n": args.n, "variant": args.variant, "z_laps_per_iteration": s["tiles"],
             "laps_per_iteration": s["tiles"] + args.n * args.n + 1,
             "z_cells": s["n_z"],
@@ -251,7 +266,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    inst = workload(args.n)
+    inst = workload(args.n, args.shape)
     cfg = q.AscentConfig(variant=args.variant, iter_limit=10 ** 6, record_history=False,
                          device=local)
     if sharded:
@@ -296,9 +311,15 @@ def run_ours(args):
     with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
         gold = _json.load(fh)
     parity = None
-    key = f"grid{args.n}_{args.variant}"
-    if key in gold["traces"]:
-        want = [float.fromhex(x) for x in gold["traces"][key]["bounds"]]
+    with open(os.path.join(ROOT, "tests", "golden", "long_traces.json")) as fh:
+        long_tr = _json.load(fh)["traces"]
+    pre = "grid" if args.shape == "grid" else "rand"
+    cands = [gold["traces"].get(f"{pre}{args.n}_{args.variant}")] + \
+        [v for k, v in sorted(long_tr.items()) if k.startswith(f"{pre}{args.n}_{args.variant}_")]
+    cands = [c for c in cands if c]
+    if cands:  # the longest reference trace of this workload (tests/golden)
+        tr = max(cands, key=lambda c: len(c["bounds"]))
+        want = [float.fromhex(x) for x in tr["bounds"]]
         k = min(len(want), eng.iteration())
         got, _ = eng.history(0, k)
         parity = {"reference_pins": k, "bitwise": bool(list(got) == want[:k])}
@@ -347,12 +368,13 @@ def run_ours(args):
         roofline["issue_active_pct"] = idb.get("zlap")
     if "zfold" in kernels and dom != "zfold":
         roofline["roofline_fold"] = kernel_roofline("zfold")
-    ib = iteration_bytes(args.n)
+    ib = iteration_bytes(args.n, args.variant)
     per_gpu_its = its / world if not sharded else its  # sharded: bytes split over world GPUs
     agg_peak = peak * (world if sharded else 1)
     iteration_roofline = {"alg_bytes": ib, "achieved_gbs": ib * per_gpu_its / 1e9,
                           "frac": ib * per_gpu_its / 1e9 / agg_peak,
-                          "note": "SURVEY.md §8(d) B=32Nz+32Ny+16tiles per 1-phase iteration"}
+                          "note": "SURVEY.md §8(d) B=32Nz+32Ny+16tiles per 1-phase iteration "
+                                  "(+32Nz for 2-phase variants)"}
 
     # e2e: the user's call (run_ascent through the C-ABI, host instance in,
     # host report out), 100 iterations = the reference's default iter_limit
@@ -388,7 +410,7 @@ def run_ours(args):
            "d2h_bytes_per_step": rec_bytes + ctypes.sizeof(q.abi.Report) / rep.iterations,
            "call": (("qapb_engine_create_instance_sharded + qapb_engine_run on every rank "
                      "(NCCL communicator reused from the timed engine)") if sharded else
-                    "qapb_run_ascent") + f"(nug{args.n}-shaped, {args.variant}, iter_limit=100): "
+                    "qapb_run_ascent") + f"({pre}{args.n}, {args.variant}, iter_limit=100): "
                    "engine build on device, 100 iterations, report + records to host",
            "seconds": e2e_s, "final_bound": rep.best_bound}
     e2e["all_seconds"] = runs
@@ -400,7 +422,8 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         try:
             cw, cs = 3, 10
-            cits, kind, threads, dt = cpu_reference_run(args.n, args.variant, cw, cs)
+            cits, kind, threads, dt = cpu_reference_run(args.n, args.variant, cw, cs,
+                                                        shape=args.shape)
             cpu = {"value": cits, "unit": "iterations/s", "cores": threads, "kind": kind,
                    "cpu_model": cpu_model(),
                    "sample": f"{cs} steady-state iterations (after {cw} untimed) of the same "
@@ -436,6 +459,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", "--size", dest="n", type=int, default=30)  # --size under torchrun
     ap.add_argument("--variant", default="F1")
+    ap.add_argument("--shape", default="grid", choices=["grid", "rand"],
+                    help="grid: nug-shaped (default); rand: tai-a-shaped generate_instance(n,1,99)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent engines instead of one z-sharded engine")
