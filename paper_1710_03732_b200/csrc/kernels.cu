@@ -1161,7 +1161,12 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
   }
 }
 
-template <int C, bool RI, bool DSM>
+// PH2: the same pipeline runs phase 2 (rlt2.cpp:344-381) on the RI layout:
+// V1/V2 stage the solve costs' X1/X2 blocks (P.costs), V3 the X3 D' block
+// when the costs are D' (P.costs_are_d; else the X3 cost is updated in
+// place in the tile layout), and each cell's cost gets its family's
+// add[s] + share (redistribute_family + the mirror shares).
+template <int C, bool RI, bool DSM, bool PH2 = false>
 __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, int K, int S,
                                                                  int rows_async, int R,
                                                                  int skip_x3w) {
@@ -1255,9 +1260,10 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       }
       if (lane == 31)
         bulk_g2s(B + oU3, P.push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &full[s]);
-      if constexpr (DSM) {  // D' of the unit: X1 / X2 row blocks and its d3 block
-        if (lane == 29) bulk_g2s(B + oV1, P.d + tb1, (unsigned)c12 * 8u, &full[s]);
-        if (lane == 28) bulk_g2s(B + oV2, P.d + tb2, (unsigned)c12 * 8u, &full[s]);
+      if constexpr (DSM) {  // D' (costs) of the unit: X1 / X2 row blocks and its d3 block
+        const double* src = PH2 ? P.costs : P.d;
+        if (lane == 29) bulk_g2s(B + oV1, src + tb1, (unsigned)c12 * 8u, &full[s]);
+        if (lane == 28) bulk_g2s(B + oV2, src + tb2, (unsigned)c12 * 8u, &full[s]);
         if (lane == 27)
           bulk_g2s(B + oV3, P.d3 + ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C,
                    (unsigned)c3 * 8u, &full[s]);
@@ -1344,6 +1350,51 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     const double* V1 = B + oV1;
     const double* V2 = B + oV2;
     const double* V3 = B + oV3;
+    if constexpr (PH2) {  // phase 2: cost += add[own] + share of the family (X1, X2, X3)
+      const double tol = 1e-9;
+      auto delta = [&](double p1, double p2, double p3, int own) {
+        double total = 0.0;
+        int nb = 3;
+        if (p1 > tol) total = dadd(total, p1); else ++nb;
+        if (p2 > tol) total = dadd(total, p2); else ++nb;
+        if (p3 > tol) total = dadd(total, p3); else ++nb;
+        const double share = __ddiv_rn(total, (double)nb);
+        const double po = own == 0 ? p1 : (own == 1 ? p2 : p3);
+        const double add = (total <= 0.0) ? 0.0 : ((po > tol) ? -po : share);
+        return dadd(add, share);
+      };
+      double* __restrict__ costs = P.costs;
+#pragma unroll
+      for (int k = 0; k < kPipeSlots; ++k) {
+        if (cells.rel[k] == 0xffffffffu) continue;
+        const uint32_t r = cells.rel[k] & 0x3fffffu;
+        const uint32_t so = cells.sm[k] & 0xffffu, sp = cells.sm[k] >> 16;
+        const uint32_t l1 = cells.l12[k] & 0xffffu, l2 = cells.l12[k] >> 16;
+        costs[tb1 + r] = dadd(V1[r], delta(P1[so], P2[sp], P3[l1], 0));  // X1
+        costs[tb2 + r] = dadd(V2[r], delta(P1[sp], P2[so], P3[l2], 1));  // X2
+      }
+#pragma unroll
+      for (int k = 0; k < kPipeSlots; ++k) {
+        if (cells.x3b[k] == 0xffffffffu) continue;
+        const int e = tid + k * kWsCT;
+        const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
+        const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
+        const uint32_t o = tb3 + pair * pstride + col;
+        const double dl = delta(P1[i1], P2[i2], P3[e], 2);
+        if (P.costs_are_d) {  // X3 D': d3 authoritative, the tile copy follows
+          const double v = dadd(V3[e], dl);
+          d3[ub + e] = v;
+          costs[o] = v;
+        } else {
+          costs[o] = dadd(costs[o], dl);
+        }
+      }
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
+                     : "memory");
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < kPipeSlots; ++k) {  // X1 and X2 cells (rlt2.cpp:280-293)
       if (cells.rel[k] == 0xffffffffu) continue;
@@ -1417,7 +1468,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   load_d(T, ch, DA);
   while (step(DA, DB) && step(DB, DA)) {
   }
-  if (blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
+  if (!PH2 && blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
     P.sa_fac[tid] = 0.0;
     P.sa_loc[tid] = 0.0;
   }
@@ -2610,6 +2661,27 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
 cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t st) {
   if (p.ntriples <= 0) return cudaSuccess;
   const int n = p.m, C = p.chunk;
+  if (env_int("QAPB_PHASE2_WS", 1)) {  // the warp-specialised pipeline in PH2 mode
+    FoldParams q = p;
+    q.costs_are_d = costs_are_d ? 1 : 0;
+    const int R = n, nrows = C * (n - 1), lp = n * (n - 1);
+    const int c12p = (C * (n - 1) * (n - 2) + 15) & ~15;
+    const size_t stage =
+        (size_t)((((2 * nrows * R + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) +
+                  2 * c12p + lp * C + 15) & ~15) * sizeof(double);
+    const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
+    const int nwork = (q.ntriples + K - 1) / K * q.nchunks;
+    const int grid = std::min(num_sms(), nwork);
+    auto go = [&](auto kern) {
+      allow_max_smem(kern);
+      kern<<<grid, kWsCT + 32, 2 * stage, st>>>(q, K, 2, 1, R, 0);
+    };
+    if (C == 2)
+      go(zfold_ws_kernel<2, true, true, true>);
+    else
+      go(zfold_ws_kernel<1, true, true, true>);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)(2 * C * (n - 1) * n + n * (n - 1) * C) * sizeof(double);
   const int units = p.ntriples * p.nchunks;
   if (C == 2) {

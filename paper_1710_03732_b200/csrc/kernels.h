@@ -172,6 +172,7 @@ struct FoldParams {
   int ri;
   // element counts of d / x3buf / d3 (bounds checks of a -DQAPB_BOUNDS build)
   size_t nz, nx3, nd3;
+  int costs_are_d;  // phase 2: the solve costs are D' (X3 members also in d3)
 };
 
 // Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
