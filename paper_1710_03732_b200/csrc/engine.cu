@@ -279,8 +279,9 @@ void Engine::alloc() {
   }
   // RI layout for the single-GPU 1-phase split engine (the warp-specialised
   // fold + tensor-map Z-LAPs); QAPB_ZLAYOUT=0 keeps the reference tile layout
-  ri_ = world_ == 1 && split_ && split_mode_ == 2 && stage_ev_.size() == 1 &&
-        env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3_group_);
+  ri_ = split_ && split_mode_ == 2 && stage_ev_.size() == 1 &&
+        env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3_group_) &&
+        (world_ == 1 || env_int("QAPB_ZLAYOUT_SHARDED", 1) != 0);
   if (ri_) {
     unsigned char h[3 * 128];
     encode_z_tmap(h, d_, m);
@@ -494,7 +495,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   std::memcpy(&id, nccl_id, sizeof id);
   comm_ = cached_comm(id, world_, rank_, dev_);
   shard_.chunk = chunk_;
-  cost_scatter_ = env_int("QAPB_COST_SCATTER", 0) != 0;
+  cost_scatter_ = env_int("QAPB_COST_SCATTER", 0) != 0 && !ri_;  // the scatter writes the tile layout
   // Receive buffers live here; peers write them directly over NVLink through
   // CUDA IPC mappings (pi from X3 owners, costs from fold owners).
   std::vector<long long> send, recv;
@@ -616,6 +617,10 @@ void Engine::enqueue_sharded_z(int it) {
       p.x3buf = x3buf_;
       p.x3_group = x3_group_;
       p.x3_ngroups = x3_ngroups_;
+    }
+    if (ri_) {  // RI layout: tiles by global index through the tensor maps
+      p.tmap_cost = tmaps_ + (costs == d_ ? 0 : 128);
+      p.tmap_pi = tmaps_ + 256;
     }
     kbegin(QAPB_K_ZLAP, st_);
     kcheck(launch_lap_batch(p, st_), "z-stage");
@@ -1142,11 +1147,18 @@ void Engine::assemble_sharded(int which, double* dst) const {
   const DeviceGuard dg(dev_);
   cuda_check(cudaStreamSynchronize(st_), "assemble");
   double* src = which == QAPB_ARR_PI_Z ? piz_ : (which == QAPB_ARR_INCZ ? incz_ : d_);
+  if (which == QAPB_ARR_STORE_D) split_scatter();  // local split D' -> tiles
+  double* ref = nullptr;  // RI: this rank's array in the reference layout
+  if (ri_) {
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&ref), nd_ * sizeof(double), st_),
+               "cudaMallocAsync");
+    kcheck(launch_z_relayout(m_, src, ref, 0, st_), "relayout");
+    src = ref;
+  }
   if (which == QAPB_ARR_STORE_D) {
-    split_scatter();  // local split D' -> tiles
-    kcheck(launch_shard_state_scatter(m_, shard_, triples_, d_, 0, st_), "d3 scatter");
+    kcheck(launch_shard_state_scatter(m_, shard_, triples_, src, 0, st_), "d3 scatter");
   } else if (which == QAPB_ARR_INCZ && hS_.iter >= 2) {  // a fold has stored costs
-    kcheck(launch_shard_state_scatter(m_, shard_, triples_, incz_, 1, st_), "cost scatter");
+    kcheck(launch_shard_state_scatter(m_, shard_, triples_, src, 1, st_), "cost scatter");
   }
   unsigned long long* buf = nullptr;
   cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), nd_ * sizeof(double), st_),
@@ -1156,6 +1168,7 @@ void Engine::assemble_sharded(int which, double* dst) const {
   nccl_check(nccl().AllReduce(buf, buf, nd_, ncclUint64, ncclSum, comm_, st_), "assemble");
   cuda_check(cudaMemcpyAsync(dst, buf, nd_ * sizeof(double), cudaMemcpyDefault, st_), "D2H");
   cuda_check(cudaFreeAsync(buf, st_), "cudaFreeAsync");
+  if (ref) cuda_check(cudaFreeAsync(ref, st_), "cudaFreeAsync");
   cuda_check(cudaStreamSynchronize(st_), "assemble");
 }
 

@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(256) zfold_kernel(FoldParams P) {
 // (TPC=0) lose the inter-CTA stage/update overlap: 3.25 vs 2.60 ms at n=30.
 constexpr int kFoldSlots = 7;  // cells per thread per member group (<= 7 * 256)
 
-template <bool SH>
+template <bool SH, bool RI = false>
 __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
   if (P.stop && *P.stop) return;
   extern __shared__ double sm[];
@@ -494,6 +494,8 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
   const int n = P.m, nm1 = n - 1, nm2 = n - 2, np = n + 1, C = P.chunk;
   const int lpairs = n * nm1;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
+  // RI layout (kernels.h z_ri_offset): a tile's rows are nm2 apart along lp
+  const uint32_t pstride = RI ? (uint32_t)nm2 : esz;
   const int nch = P.nchunks, ch = blockIdx.x % nch, r0 = blockIdx.x / nch, R = gridDim.x / nch;
   const int pa0 = p_lo + ch * C, Pe = min(C, p_hi - pa0);
   const FoldSmem L(n, C);
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       const int qi = rem / nm2, r = rem - qi * nm2;
       const int pa = pa0 + pa_l, q = qi + (qi >= pa);
       const int other = skip2(r, min(pa, q), max(pa, q));
-      rel12[k] = (uint32_t)lpair(pa, q) * esz + r;
+      rel12[k] = (uint32_t)lpair(pa, q) * pstride + r;
       fi12[k] = (uint32_t)L.fi(pa_l, q, other) | ((uint32_t)L.fi(pa_l, other, q) << 16);
       ju12[k] = (uint32_t)(pa_l * nm1 + qi) | ((uint32_t)(pa_l * nm1 + other - (other > pa)) << 16);
       lu12[k] = (uint32_t)lpair(q, other) | ((uint32_t)lpair(other, q) << 16);
@@ -564,9 +566,12 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
   for (int T = r0; T < P.ntriples; T += R) {
     const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
     const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
-    const uint32_t tb1 = (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
-    const uint32_t tb2 = (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
-    const uint32_t tb3 = (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
+    const uint32_t tb1 = RI ? (uint32_t)(fab * nm2 + c - 2) * lpairs * nm2
+                            : (uint32_t)fab * lpairs * esz + (uint32_t)(c - 2) * nm2;
+    const uint32_t tb2 = RI ? (uint32_t)(fac * nm2 + b - 1) * lpairs * nm2
+                            : (uint32_t)fac * lpairs * esz + (uint32_t)(b - 1) * nm2;
+    const uint32_t tb3 = RI ? (uint32_t)(fbc * nm2 + a) * lpairs * nm2
+                            : (uint32_t)fbc * lpairs * esz + (uint32_t)a * nm2;
     const size_t ub = ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;  // d3 base of the unit
     size_t unit = 0, rbT = 0;  // sharded: unit index and rows_before[fbc]
     if constexpr (SH) {
@@ -669,7 +674,7 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
         }
       }
       d3[ub + pair * C + pl] = dn;
-      const uint32_t o = tb3 + pair * esz + ((x3a[k] >> 12) & 63u);
+      const uint32_t o = tb3 + pair * pstride + ((x3a[k] >> 12) & 63u);
       QAPB_CHECK(o < P.nz, "lean x3 store", o, P.nz);
       if (fast)
         incz[o] = dadd(dmul(omk, p3), gain);
@@ -2608,7 +2613,8 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
     const int C = p.chunk;
     const size_t psmem = (size_t)(4 * C * (n - 1) * (n - 2) + 2 * C * n * (n - 1) +
                                   2 * C * (n - 1) + n * (n - 1)) * sizeof(double);
-    if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_PIPE", 1) && n % 2 == 0 &&
+    if (p.x3buf && p.x3mode == 2 && !p.shard && !p.ri && env_int("QAPB_FOLD_PIPE", 1) &&
+        n % 2 == 0 &&
         (C == 1 || (C == 2 && p.x3_group % 2 == 0)) && nz < 4294967295.0 &&
         C * (n - 1) * (n - 2) <= kPipeSlots * 512 && C * n * (n - 1) <= kPipeSlots * 512 &&
         n < 64 && 2 * psmem <= 220 * 1024) {
@@ -2625,7 +2631,8 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
       return cudaGetLastError();
     }
   }
-  if (p.x3buf && p.x3mode == 2 && !p.shard && env_int("QAPB_FOLD_BULK", 1) && n % 2 == 0 &&
+  if (p.x3buf && p.x3mode == 2 && !p.shard && !p.ri && env_int("QAPB_FOLD_BULK", 1) &&
+      n % 2 == 0 &&
       p.chunk == 2 && p.x3_group % 2 == 0 && nz < 4294967295.0 &&
       2 * (n - 1) * (n - 2) <= kFoldSlots * 256 && 2 * n * (n - 1) <= kFoldSlots * 256 &&
       n * (n - 1) < 16384 && n < 64) {
@@ -2642,7 +2649,8 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
       nz < 4294967295.0 && p.chunk * (n - 1) * (n - 2) <= kFoldSlots * 256 &&
       p.chunk * n * (n - 1) <= kFoldSlots * 256 && FoldSmem(n, p.chunk).cube < 4096 && n < 64 &&
       p.chunk * (n - 1) < 256 && n * (n - 1) < 16384) {
-    auto kern = p.shard ? zfold_lean_kernel<true> : zfold_lean_kernel<false>;
+    auto kern = p.shard ? (p.ri ? zfold_lean_kernel<true, true> : zfold_lean_kernel<true, false>)
+                        : (p.ri ? zfold_lean_kernel<false, true> : zfold_lean_kernel<false, false>);
     allow_max_smem(kern);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
@@ -2653,6 +2661,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
     kern<<<R * p.nchunks, 256, smem, st>>>(p);
     return cudaGetLastError();
   }
+  if (p.ri) return cudaErrorInvalidValue;  // the general fold reads the tile layout
   allow_max_smem(zfold_kernel);
   zfold_kernel<<<p.ntriples * p.nchunks, 256, smem, st>>>(p);
   return cudaGetLastError();
@@ -2712,8 +2721,8 @@ cudaError_t launch_lap_batch_t(const BatchLapParams& p, cudaStream_t st) {
   const bool aligned = (((uintptr_t)p.costs) & 15) == 0;
   const bool use_bulk = (tile_bytes % 16 == 0) && aligned;
   const bool store_bulk = use_bulk && p.pi && (((uintptr_t)p.pi) & 15) == 0;
-  if ((p.tmap_cost || p.tmap_pi) && (!use_bulk || !store_bulk || p.sh || !p.x3buf || p.patch))
-    return cudaErrorInvalidValue;  // the RI path is the single-GPU split Z stage only
+  if ((p.tmap_cost || p.tmap_pi) && (!use_bulk || !store_bulk || (!p.sh && (!p.x3buf || p.patch))))
+    return cudaErrorInvalidValue;  // the RI path: the split Z stage (single GPU) or sharded
   const size_t buf_elems = align_up(esz, 16);  // 128-byte aligned buffers
   // tile buffers per warp: 1 (more resident warps) unless QAPB_LAP_NBUF=2
   int nbuf = use_bulk ? std::max(1, std::min(2, env_int("QAPB_LAP_NBUF", 1))) : 1;
