@@ -51,6 +51,16 @@ struct DIdx {
   }
 };
 
+// x / d for 0 <= x < 2^22 and 0 < d < 2^12 through a float reciprocal and one
+// correction step (the compiler's 32-bit division by a runtime divisor is ~20
+// instructions)
+__device__ __forceinline__ int small_udiv(int x, int d) {
+  int q = __float2int_rz(__fmul_rz((float)x, __frcp_rn((float)d)));
+  const int r = x - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
 // r-th free index of {0..n-1} \ {lo, hi} (lo < hi): uncell's column rule.
 __device__ __forceinline__ int skip2(int r, int lo, int hi) {
   if (r >= lo) ++r;

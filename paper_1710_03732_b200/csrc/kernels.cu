@@ -1658,11 +1658,11 @@ template <int CPL>
 __device__ __forceinline__ void x3_split_lanes(const BatchLapParams& P, int n, int tg, int lane,
                                                X3Lane (&X)[CPL], int& b, int& tb) {
   const int nm1 = n - 1, m = n - 2, lpairs = n * nm1;
-  const int f = tg / lpairs, lp = tg - f * lpairs;
+  const int f = small_udiv(tg, lpairs), lp = tg - f * lpairs;
   const int ij = P.fpair_ij[f];
   b = ij & 0xffff;
   const int c = ij >> 16;
-  const int pb = lp / nm1, qq = lp - pb * nm1, pc = qq + (qq >= pb);
+  const int pb = small_udiv(lp, nm1), qq = lp - pb * nm1, pc = qq + (qq >= pb);
   const int lo = min(pb, pc), hi = max(pb, pc);
   tb = c3u(n) - (n - b) * (n - b - 1) / 2 + (c - b - 1);
   const int G = P.x3_group;

@@ -519,21 +519,21 @@ __device__ __forceinline__ void warp_lap_slack_inplace(double* __restrict__ cost
   }
   __syncwarp();
   const int esz = m * m;
-  if ((m & 1) == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0) {
-    int a = (2 * lane) / m, b = 2 * lane - a * m;  // element 2*lane + 64k
-    const int da = 64 / m, db = 64 - da * m;
-    for (int e = 2 * lane; e < esz; e += 64) {
-      double2 c = *reinterpret_cast<double2*>(cost + e);
-      const double ua = urow[a];
-      const double2 vb = *reinterpret_cast<const double2*>(vrow + b);
-      c.x = dsub(dsub(c.x, ua), vb.x);
-      c.y = dsub(dsub(c.y, ua), vb.y);
-      *reinterpret_cast<double2*>(cost + e) = c;
-      a += da;
-      b += db;
-      if (b >= m) {
-        b -= m;
-        ++a;
+  if ((m & 1) == 0 && m <= 64 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0) {
+    // lane -> (column pair cp, row phase g): it walks rows g, g + G, ... of
+    // columns 2cp, 2cp+1, so the two column duals stay in registers
+    const int pairs = m >> 1, G = small_udiv(32, pairs), g = small_udiv(lane, pairs),
+              cp = lane - g * pairs;
+    if (g < G) {
+      const double2 vb = *reinterpret_cast<const double2*>(vrow + 2 * cp);
+      double* c2 = cost + (size_t)g * m + 2 * cp;
+      const double* ur = urow + g;
+      for (int a = g; a < m; a += G, c2 += G * m, ur += G) {
+        double2 c = *reinterpret_cast<double2*>(c2);
+        const double ua = *ur;
+        c.x = dsub(dsub(c.x, ua), vb.x);
+        c.y = dsub(dsub(c.y, ua), vb.y);
+        *reinterpret_cast<double2*>(c2) = c;
       }
     }
   } else {
