@@ -329,6 +329,18 @@ QAPB_API qapb_status qapb_store_collapse_offset(const qapb_store* s, double offs
                                                 int loc, qapb_store** out);
 /* free / total bytes of a device (cudaMemGetInfo) */
 QAPB_API qapb_status qapb_device_memory(int device, size_t* free_bytes, size_t* total_bytes);
+
+/* ---- the SA acceptance exp (rlt2.cpp:494 std::exp) -------------------- */
+/* The device SA step evaluates glibc's double exp op for op (csrc/glibc_exp.cuh).
+ * qapb_exp_variant: which glibc build the host libm resolves exp to
+ * (1 = FMA, 0 = SSE2/AVX, -1 = neither; QAPB_EXP_VARIANT overrides).
+ * qapb_exp_glibc: the host restatement of that build (no GPU needed).
+ * qapb_exp_batch_device: y[i] = exp(x[i]) on the device, device pointers,
+ * enqueued on `stream` -- the function the SA kernel inlines. */
+QAPB_API int qapb_exp_variant(void);
+QAPB_API double qapb_exp_glibc(double x, int fma);
+QAPB_API qapb_status qapb_exp_batch_device(const double* x, double* y, size_t n, int fma,
+                                           void* stream);
 /* the CUDA device a store lives on */
 QAPB_API qapb_status qapb_store_device(const qapb_store* s, int* device);
 /* init_coefficients(inst), rlt2.cpp:66-89, built in HBM (D' = 0). */

@@ -672,6 +672,18 @@ QAPB_API qapb_status qapb_store_collapse_offset(const qapb_store* s, double offs
   });
 }
 
+QAPB_API int qapb_exp_variant(void) { return qapb::exp_variant_host(); }
+
+QAPB_API double qapb_exp_glibc(double x, int fma) { return qapb::exp_glibc_host(x, fma); }
+
+QAPB_API qapb_status qapb_exp_batch_device(const double* x, double* y, size_t n, int fma,
+                                           void* stream) {
+  return guard([&] {
+    qapb::cuda_check(qapb::launch_exp_batch(x, y, n, fma, static_cast<cudaStream_t>(stream)),
+                     "exp batch");
+  });
+}
+
 QAPB_API qapb_status qapb_device_memory(int device, size_t* free_bytes, size_t* total_bytes) {
   return guard([&] {
     qapb::DeviceGuard dg(device);

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <cstdio>
 #include <mutex>
 #include <set>
 #include <string>
@@ -301,6 +302,15 @@ void Engine::alloc() {
     sa_seed(&h, cfg_.seed);
     cuda_check(cudaMemcpyAsync(sa_state_, &h, sizeof h, cudaMemcpyHostToDevice, st_), "H2D sa");
     cuda_check(cudaStreamSynchronize(st_), "sa seed");
+    exp_fma_ = exp_variant_host();
+    if (exp_fma_ < 0) {  // not glibc >= 2.28: the accept test may differ from std::exp
+      static std::once_flag warned;
+      std::call_once(warned, [] {
+        std::fprintf(stderr, "qapb: host libm exp matches neither glibc build; device SA "
+                             "uses the FMA build (set QAPB_EXP_VARIANT=fma|nofma)\n");
+      });
+      exp_fma_ = 1;
+    }
   }
   salloc(st_, &counter_, stage_ev_.size() + 2);
   salloc(st_, &S_, 1);
@@ -910,6 +920,7 @@ void Engine::enqueue_iteration(int it) {  // rlt2.cpp:515-530
     sp.m = m_;
     sp.cool_period = cfg_.sa_cool_period;
     sp.fast = is_fast() ? 1 : 0;
+    sp.exp_fma = exp_fma_;
     sp.t0_fraction = cfg_.sa_t0_fraction;
     sp.kappa_cap = cfg_.sa_kappa_lb_cap;
     sp.cool_factor = cfg_.sa_cool_factor;

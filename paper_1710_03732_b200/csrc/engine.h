@@ -190,6 +190,7 @@ class Engine {
   DevScalars hS_{};
   std::mt19937_64 rng_;  // host SA (QAPB_HOST_SA=1); the device SA keeps its own state
   bool sa_dev_ = false;
+  int exp_fma_ = 1;  // glibc exp build the device SA restates (kernels.h)
   SaState* sa_state_ = nullptr;
   double temp_ = 0;
   qapb_record last_rec_{};

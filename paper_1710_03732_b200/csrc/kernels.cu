@@ -9,7 +9,9 @@
 //
 // Layouts are the reference's (StoreIndex); every Z tile and Y block is
 // contiguous.  See DESIGN.md for the roofline of each kernel.
+#include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -23,6 +25,7 @@
 #include <utility>
 
 #include "../../include/qapb200.h"
+#include "glibc_exp.cuh"
 #include "common.cuh"
 #include "kernels.h"
 #include "lap_warp.cuh"
@@ -2368,8 +2371,11 @@ __global__ void sa_apply_kernel(int m, double* b, const double* sa_fac, const do
 // std::uniform_real_distribution<double>(0,1) over std::mt19937_64 in
 // libstdc++ (generate_canonical: one 64-bit draw, (double)x / 2^64, clamped
 // below 1), so the state advances exactly as the reference's.  The accept
-// test U < exp(-kap/T) uses CUDA's exp (<= 1 ulp): it can differ from glibc's
-// only when U equals one of two adjacent doubles, p ~ 2^-52 per draw.
+// test U < exp(-kap/T) evaluates glibc's exp op for op (glibc_exp.cuh), in the
+// build (FMA or not) the host's libm resolves to, so it is bitwise the
+// reference's std::exp.
+__device__ const uint64_t g_exp_tab[256] = QAPB_EXP_TAB;
+
 __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
   y ^= (y >> 29) & 0x5555555555555555ULL;
   y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
@@ -2458,7 +2464,9 @@ __global__ void __launch_bounds__(32) sa_device_kernel(SaParams p, double* __res
   }
   for (int s = lane; s < 2 * m; s += 32) {
     const double kap = dmul(u[2 * s], cap);
-    acc[s] = u[2 * s + 1] < exp(ddiv(-kap, temp));
+    const double ex = ddiv(-kap, temp);
+    acc[s] = u[2 * s + 1] < (p.exp_fma ? qapb_exp::exp<true>(ex, g_exp_tab)
+                                       : qapb_exp::exp<false>(ex, g_exp_tab));
     amt[s] = kap;
   }
   __syncwarp();
@@ -2821,6 +2829,45 @@ cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, in
   x3_sync_kernel<<<4 * num_sms(), 256, 0, st>>>(n, chunk, nchunks, triples, p_lo, p_hi, d, d3,
                                                 total, to_d3, ri);
   return cudaGetLastError();
+}
+
+__global__ void exp_batch_kernel(const double* __restrict__ x, double* __restrict__ y, size_t n,
+                                 int fma) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = fma ? qapb_exp::exp<true>(x[i], g_exp_tab) : qapb_exp::exp<false>(x[i], g_exp_tab);
+}
+
+cudaError_t launch_exp_batch(const double* x, double* y, size_t n, int fma, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const size_t blocks = std::min<size_t>((n + 255) / 256, 148 * 16);
+  exp_batch_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, y, n, fma);
+  return cudaGetLastError();
+}
+
+static const uint64_t h_exp_tab[256] = QAPB_EXP_TAB;
+
+double exp_glibc_host(double x, int fma) {
+  return fma ? qapb_exp::exp<true>(x, h_exp_tab) : qapb_exp::exp<false>(x, h_exp_tab);
+}
+
+int exp_variant_host() {
+  if (const char* e = std::getenv("QAPB_EXP_VARIANT")) {
+    if (!std::strcmp(e, "fma")) return 1;
+    if (!std::strcmp(e, "nofma")) return 0;
+  }
+  // Ask the libm itself: at these arguments the two builds round differently
+  // (found by tests/test_exp_glibc.py's search), so the IFUNC's choice shows.
+  static const double probes[3] = {-0x1.bafef5135235bp+0, -0x1.6063d1ae7a948p+3,
+                                   -0x1.84fd45030fefdp+4};
+  int fma = 0, nofma = 0;
+  for (double p : probes) {
+    volatile double xv = p;  // keep the call at run time
+    const double y = std::exp(xv);
+    fma += y == exp_glibc_host(p, 1);
+    nofma += y == exp_glibc_host(p, 0);
+  }
+  return fma == 3 ? 1 : nofma == 3 ? 0 : -1;
 }
 
 cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,

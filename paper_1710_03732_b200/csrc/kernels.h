@@ -32,8 +32,15 @@ struct SaState {
 };
 struct SaParams {
   int m, cool_period, fast;
+  int exp_fma;  // which glibc exp build to restate (exp_variant_host())
   double t0_fraction, kappa_cap, cool_factor, upper_bound;
 };
+// glibc's double exp, restated bitwise (glibc_exp.cuh).  fma: 1 = the FMA
+// build, 0 = SSE2/AVX.  exp_variant_host(): the build the host libm uses
+// (-1: neither, i.e. not glibc >= 2.28).
+int exp_variant_host();
+double exp_glibc_host(double x, int fma);
+cudaError_t launch_exp_batch(const double* x, double* y, size_t n, int fma, cudaStream_t stream);
 // mt19937_64 seeding (std::mersenne_twister_engine::seed)
 void sa_seed(SaState* host_state, unsigned long long seed);
 
