@@ -284,10 +284,11 @@ void Engine::alloc() {
         env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3_group_) &&
         (world_ == 1 || env_int("QAPB_ZLAYOUT_SHARDED", 1) != 0);
   if (ri_) {
-    unsigned char h[3 * 128];
+    unsigned char h[4 * 128];
     encode_z_tmap(h, d_, m);
     if (incz_) encode_z_tmap(h + 128, incz_, m);
     encode_z_tmap(h + 256, piz_, m);
+    encode_rows_tmap(h + 384, piz_, m, chunk_);
     dalloc(&tmaps_, sizeof h);  // cudaMalloc: 256-byte aligned
     cuda_check(cudaMemcpyAsync(tmaps_, h, sizeof h, cudaMemcpyHostToDevice, st_),
                "H2D tensor maps");
@@ -779,6 +780,7 @@ FoldParams Engine::fold_params(int stage) const {
   }
   if (f.tri0 == 0 && f.ntriples == ntriples_) f.order = order_;
   f.ri = ri_ ? 1 : 0;
+  f.tmap_rows = (ri_ && tmaps_) ? tmaps_ + 384 : nullptr;
   f.nz = nd_;
   if (split_) {
     const int nch = world_ > 1 ? chunks_me_ : nchunks_;

@@ -145,7 +145,7 @@ class Engine {
   bool split_ = false;
   int split_mode_ = 0;
   // z arrays in the row-interleaved layout (kernels.h z_ri_offset); Z-LAP
-  // tiles move by 3-D TMA tensor copies: tmaps_ = {d, incz, pi(z)} maps
+  // tiles move by 3-D TMA tensor copies: tmaps_ = {d, incz, pi(z)} maps + the fold's 2-D pi(z) row map
   bool ri_ = false;
   unsigned char* tmaps_ = nullptr;
   bool cost_scatter_ = false;  // sharded: scatter remote X3 costs before the Z-LAPs

@@ -1128,8 +1128,11 @@ struct WsCells {
   uint32_t x3a[kPipeSlots], x3b[kPipeSlots];
 };
 
+// sh/off: the stage's X3 pi block holds 2^sh locations per pair, this
+// unit's first at `off` (C itself and 0 unless the whole x3buf group is staged)
 template <int C, bool RI>
-__device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, int R) {
+__device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, int R,
+                                         int sh = C == 2 ? 1 : 0, int off = 0) {
   const int nm1 = n - 1, nm2 = n - 2;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
   auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
@@ -1150,8 +1153,8 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
       w.rel[k] = (RI ? (uint32_t)e : ((uint32_t)lpair(pa, q) * esz + r)) | ((uint32_t)jo << 22);
       w.sm[k] = (uint32_t)((pa_l * nm1 + qi) * R + r) |
                 ((uint32_t)(jo * R + colskip(q, pa, other)) << 16);
-      w.l12[k] = (uint32_t)(lpair(q, other) * C + pa_l) |
-                 ((uint32_t)(lpair(other, q) * C + pa_l) << 16);
+      w.l12[k] = (uint32_t)((lpair(q, other) << sh) + off + pa_l) |
+                 ((uint32_t)((lpair(other, q) << sh) + off + pa_l) << 16);
     }
     w.x3b[k] = 0xffffffffu;
     if (e < c3) {
@@ -1174,10 +1177,22 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
 // when the costs are D' (P.costs_are_d; else the X3 cost is updated in
 // place in the tile layout), and each cell's cost gets its family's
 // add[s] + share (redistribute_family + the mirror shares).
+// rows_async: how the X1 / X2 pi rows arrive -- 0 one bulk copy per row,
+// 1 16-byte cp.async pieces, 2 one 2-D TMA tensor box per array (P.tmap_rows:
+// box {R, nrows} over rows of n-2, the two pad columns zero-filled out of
+// bounds).  x3w: stage the unit's whole x3buf group (one bulk copy) instead
+// of its C locations in 16/8-byte pieces.
 template <int C, bool RI, bool DSM, bool PH2 = false>
 __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, int K, int S,
                                                                  int rows_async, int R,
-                                                                 int skip_x3w) {
+                                                                 int x3w, int dbg) {
+  // dbg (timing experiments only; wrong results): 1 skip the X3 tile stores,
+  // 2 consumers only wait and release, 4 compute without global stores.
+  // dbg >> 8: L2 hints -- 1 X3 tile stores evict_last (their 16-byte pieces
+  // merge into whole sectors before eviction), 2 other stores evict_first,
+  // 4 staged loads evict_first
+  const int hints = dbg >> 8;
+  dbg &= 0xff;
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
@@ -1190,8 +1205,13 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   const int nrows = C * nm1, nrows_p = (nrows + 1) & ~1;
   const uint32_t pstride = RI ? (uint32_t)nm2 : esz;  // tile -> tile along lp, same row
   const int c3 = lpairs * C;
+  const int Gx = P.x3_group;
+  const bool pieces = Gx != C && !x3w;  // X3 pi gathered in 16/8-byte cp.async pieces
+  const int p3n = (Gx != C && x3w) ? lpairs * Gx : c3;  // X3 pi doubles staged per unit
   // stage: P1 rows | P2 rows | P3 (fold order) | U1 | U2 | U3 (all 16-byte aligned)
-  const int oP2 = nrows * R, oP3 = 2 * nrows * R, oU1 = oP3 + c3, oU2 = oU1 + nrows_p,
+  // (P1 / P2 start 128-byte aligned: TMA tensor boxes land there)
+  const int prow = (nrows * R + 15) & ~15;
+  const int oP2 = prow, oP3 = 2 * prow, oU1 = oP3 + p3n, oU2 = oU1 + nrows_p,
             oU3 = oU2 + nrows_p;
   // DSM (RI only): the unit's D' blocks (X1 / X2 rows, d3) staged too, dense
   const int c12 = C * nm1 * nm2;
@@ -1201,8 +1221,6 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = (P.ntriples + K - 1) / K, nwork = nblk * nch, G = gridDim.x;
   if ((int)blockIdx.x >= nwork) return;
-  const int Gx = P.x3_group;
-  const bool pieces = Gx != C;  // X3 pi not contiguous per unit: 16/8-byte cp.async pieces
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 32);  // one arrival per producer lane (after its cp.async pieces)
@@ -1226,8 +1244,9 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
 
   if (warp == kWsCW) {  // ---------------- producer warp ----------------
     const unsigned row_bytes = (unsigned)nm2 * 8u;
-    const unsigned tx = (rows_async ? 0u : 2u * nrows * row_bytes) + (unsigned)lpairs * 8u +
-                        (pieces ? 0u : (unsigned)c3 * 8u) +
+    const unsigned tx = (rows_async == 0 ? 2u * nrows * row_bytes
+                         : rows_async == 2 ? 2u * nrows * R * 8u : 0u) +
+                        (unsigned)lpairs * 8u + (pieces ? 0u : (unsigned)p3n * 8u) +
                         (DSM ? (unsigned)(2 * c12 + c3) * 8u : 0u);
     int w = blockIdx.x, pos = (w / nch) * K;
     for (int u = 0; w < nwork; ++u, advance(w, pos)) {
@@ -1248,7 +1267,17 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       __syncwarp();
       // X1 / X2 pi rows: row `row` (= (pa_l, qi) = location pair lpair(pa0,..) + row)
       // sits at tb + row * pstride
-      if (RI && R == nm2) {  // one copy per array: the unit's rows are contiguous
+      if (rows_async == 2) {  // one 2-D box per array, rows padded to R in smem
+        if (hints & 4) {
+          const uint64_t pol = policy_evict_first();
+          if (lane == 0) tma_load_2d_hint(B, P.tmap_rows, 0, (int)(tb1 / (uint32_t)nm2), &full[s], pol);
+          if (lane == 1)
+            tma_load_2d_hint(B + oP2, P.tmap_rows, 0, (int)(tb2 / (uint32_t)nm2), &full[s], pol);
+        } else {
+          if (lane == 0) tma_load_2d(B, P.tmap_rows, 0, (int)(tb1 / (uint32_t)nm2), &full[s]);
+          if (lane == 1) tma_load_2d(B + oP2, P.tmap_rows, 0, (int)(tb2 / (uint32_t)nm2), &full[s]);
+        }
+      } else if (RI && R == nm2) {  // one copy per array: the unit's rows are contiguous
         if (lane == 0) bulk_g2s(B, P.piz + tb1, (unsigned)nrows * row_bytes, &full[s]);
         if (lane == 1) bulk_g2s(B + oP2, P.piz + tb2, (unsigned)nrows * row_bytes, &full[s]);
       } else if (rows_async) {  // 16-byte cp.async pieces
@@ -1270,16 +1299,24 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         bulk_g2s(B + oU3, P.push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &full[s]);
       if constexpr (DSM) {  // D' (costs) of the unit: X1 / X2 row blocks and its d3 block
         const double* src = PH2 ? P.costs : P.d;
-        if (lane == 29) bulk_g2s(B + oV1, src + tb1, (unsigned)c12 * 8u, &full[s]);
-        if (lane == 28) bulk_g2s(B + oV2, src + tb2, (unsigned)c12 * 8u, &full[s]);
-        if (lane == 27)
-          bulk_g2s(B + oV3, P.d3 + ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C,
-                   (unsigned)c3 * 8u, &full[s]);
+        const double* s3 = P.d3 + ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;
+        if (hints & 4) {
+          const uint64_t pol = policy_evict_first();
+          if (lane == 29) bulk_g2s_hint(B + oV1, src + tb1, (unsigned)c12 * 8u, &full[s], pol);
+          if (lane == 28) bulk_g2s_hint(B + oV2, src + tb2, (unsigned)c12 * 8u, &full[s], pol);
+          if (lane == 27) bulk_g2s_hint(B + oV3, s3, (unsigned)c3 * 8u, &full[s], pol);
+        } else {
+          if (lane == 29) bulk_g2s(B + oV1, src + tb1, (unsigned)c12 * 8u, &full[s]);
+          if (lane == 28) bulk_g2s(B + oV2, src + tb2, (unsigned)c12 * 8u, &full[s]);
+          if (lane == 27) bulk_g2s(B + oV3, s3, (unsigned)c3 * 8u, &full[s]);
+        }
       }
       const int g0 = pa0 / Gx;
-      const size_t upi = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx + (pa0 - g0 * Gx);
-      if (!pieces) {
-        if (lane == 30) bulk_g2s(B + oP3, P.x3buf + upi, (unsigned)c3 * 8u, &full[s]);
+      const size_t ugr = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx;
+      const size_t upi = ugr + (pa0 - g0 * Gx);
+      if (!pieces) {  // contiguous: this unit's block (Gx == C) or its whole group
+        if (lane == 30)
+          bulk_g2s(B + oP3, P.x3buf + (Gx == C ? upi : ugr), (unsigned)p3n * 8u, &full[s]);
       } else {
         for (int e = lane; e < lpairs; e += 32) {
           if constexpr (C == 2)
@@ -1309,7 +1346,11 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   WsCells cells;
   int w = blockIdx.x, pos = (w / nch) * K;
   int T = tri(pos), ch = w % nch;
-  ws_cells<C, RI>(cells, n, ch * C, tid, R);
+  // X3 pi block in the stage: 2^sh locations per pair, this unit's at p3off
+  const int lc = C == 2 ? 1 : 0;
+  const int sh = p3n == c3 ? lc : (Gx == 4 ? 2 : Gx == 2 ? 1 : 3);
+  auto p3off = [&](int ch_) { return p3n == c3 ? 0 : (ch_ * C) % Gx; };
+  ws_cells<C, RI>(cells, n, ch * C, tid, R, sh, p3off(ch));
   // X1 / X2: base of the unit's rows (RI) or of its tiles' rows (cells add the
   // tile offset); X3: row a of the (b,c) tiles, + pair * pstride + col
   auto bases = [&](int T_, int ch_, uint32_t& tb1, uint32_t& tb2, uint32_t& tb3, size_t& ub) {
@@ -1348,6 +1389,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     size_t ub;
     bases(T, ch, tb1, tb2, tb3, ub);
     mbar_wait(&full[s], (u / S) & 1);
+    const int p3o = p3off(ch);
     const double* B = sm + (size_t)s * stage_sz;
     const double* P1 = B;
     const double* P2 = B + oP2;
@@ -1388,7 +1430,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
         const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
         const uint32_t o = tb3 + pair * pstride + col;
-        const double dl = delta(P1[i1], P2[i2], P3[e], 2);
+        const double dl = delta(P1[i1], P2[i2], P3[((e >> lc) << sh) + p3o + (e & (C - 1))], 2);
         if (P.costs_are_d) {  // X3 D': d3 authoritative, the tile copy follows
           const double v = dadd(V3[e], dl);
           d3[ub + e] = v;
@@ -1403,6 +1445,20 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
                      : "memory");
       return;
     }
+    double sink = 0.0;
+    const uint64_t pol_last = (hints & 1) ? policy_evict_last() : 0;
+    const uint64_t pol_first = (hints & 2) ? policy_evict_first() : 0;
+    auto st = [&](double* p, double v) {
+      if (dbg & 4) sink = dadd(sink, v);
+      else if (hints & 2) st_hint(p, v, pol_first);
+      else *p = v;
+    };
+    auto st3 = [&](double* p, double v) {  // the X3 tile stores
+      if (dbg & 4) sink = dadd(sink, v);
+      else if (hints & 1) st_hint(p, v, pol_last);
+      else *p = v;
+    };
+    if (dbg & 2) goto release;
 #pragma unroll
     for (int k = 0; k < kPipeSlots; ++k) {  // X1 and X2 cells (rlt2.cpp:280-293)
       if (cells.rel[k] == 0xffffffffu) continue;
@@ -1412,18 +1468,18 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       {  // X1: (pb, pc) = (q, other)
         const double p1 = P1[so], p2 = P2[sp], p3 = P3[l1];
         const double s2 = dadd(dmul(kz, p2), U2[jo]);
-        const double s3 = dadd(dmul(kz, p3), U3[l1 / C]);
+        const double s3 = dadd(dmul(kz, p3), U3[l1 >> sh]);
         const double gain = dadd(dmul(phi, s2), dmul(phi, s3));
-        d[tb1 + r] = dadd(DSM ? V1[r] : D[k], dsub(gain, dmul(kz, p1)));
-        if (fast) incz[tb1 + r] = dadd(dmul(omk, p1), gain);
+        st(&d[tb1 + r], dadd(DSM ? V1[r] : D[k], dsub(gain, dmul(kz, p1))));
+        if (fast) st(&incz[tb1 + r], dadd(dmul(omk, p1), gain));
       }
       {  // X2: (pb, pc) = (other, q)
         const double p2 = P2[so], p1 = P1[sp], p3 = P3[l2];
         const double s1 = dadd(dmul(kz, p1), U1[jo]);
-        const double s3 = dadd(dmul(kz, p3), U3[l2 / C]);
+        const double s3 = dadd(dmul(kz, p3), U3[l2 >> sh]);
         const double gain = dadd(dmul(phi, s1), dmul(phi, s3));
-        d[tb2 + r] = dadd(DSM ? V2[r] : D[kPipeSlots + k], dsub(gain, dmul(kz, p2)));
-        if (fast) incz[tb2 + r] = dadd(dmul(omk, p2), gain);
+        st(&d[tb2 + r], dadd(DSM ? V2[r] : D[kPipeSlots + k], dsub(gain, dmul(kz, p2))));
+        if (fast) st(&incz[tb2 + r], dadd(dmul(omk, p2), gain));
       }
     }
 #pragma unroll
@@ -1432,19 +1488,21 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       const int e = tid + k * kWsCT;
       const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
       const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
-      const double p3 = P3[e], p1 = P1[i1], p2 = P2[i2];
+      const double p3 = P3[((e >> lc) << sh) + p3o + (e & (C - 1))], p1 = P1[i1], p2 = P2[i2];
       const double s1 = dadd(dmul(kz, p1), U1[i1 / (uint32_t)R]);
       const double s2 = dadd(dmul(kz, p2), U2[i2 / (uint32_t)R]);
       const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
       const double dn = dadd(DSM ? V3[e] : D[2 * kPipeSlots + k], dsub(gain, dmul(kz, p3)));
-      d3[ub + e] = dn;
+      st(&d3[ub + e], dn);
       const uint32_t o = tb3 + pair * pstride + col;
-      if (skip_x3w) continue;  // timing experiment only (wrong results)
+      if (dbg & 1) continue;
       if (fast)
-        incz[o] = dadd(dmul(omk, p3), gain);
+        st3(&incz[o], dadd(dmul(omk, p3), gain));
       else
-        d[o] = dn;
+        st3(&d[o], dn);
     }
+    if ((dbg & 4) && sink == 1234.5) d[0] = sink;
+  release:
     __syncwarp();
     if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
@@ -1467,7 +1525,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     T = T2;
     if (!pre) {  // new chunk: new cell pattern, then its D'
       ch = ch2;
-      ws_cells<C, RI>(cells, n, ch * C, tid, R);
+      ws_cells<C, RI>(cells, n, ch * C, tid, R, sh, p3off(ch));
       load_d(T, ch, Dn);
     }
     return true;
@@ -2586,9 +2644,15 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
     const bool dsm = p.ri && env_int("QAPB_FOLD_WS_DSM", 1);
     const int R = dense ? n - 2 : n, nrows = C * (n - 1), lp = n * (n - 1);
     const int c12p = (C * (n - 1) * (n - 2) + 15) & ~15;
-    const size_t stage =
-        (size_t)((((2 * nrows * R + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) +
-                  (dsm ? 2 * c12p + lp * C : 0) + 15) & ~15) * sizeof(double);
+    // stage the whole x3buf group of a unit (one bulk copy; the neighbour
+    // chunk reads the other half from L2) instead of 16-byte pieces
+    auto stage_of = [&](int p3n) {
+      return (size_t)((((2 * ((nrows * R + 15) & ~15) + p3n + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) +
+                       (dsm ? 2 * c12p + lp * C : 0) + 15) & ~15) * sizeof(double);
+    };
+    const int x3w = (p.x3_group == 2 * C && env_int("QAPB_FOLD_X3_WHOLE", 1) &&
+                     stage_of(lp * p.x3_group) * 2 <= 210 * 1024) ? 1 : 0;
+    const size_t stage = stage_of(x3w ? lp * p.x3_group : lp * C);
     const int S = std::min(kWsMaxStages, (int)((210 * 1024) / stage));
     if (p.x3buf && p.x3mode == 2 && !p.shard &&
         (p.ri || (env_int("QAPB_FOLD_WS", 0) && env_int("QAPB_FOLD_PIPE", 1))) && n % 2 == 0 &&
@@ -2601,11 +2665,16 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
       // measured at n=30 (RI): two stages beat three and four; with D' staged,
       // 16-byte cp.async rows beat TMA bulk row copies (2.18 vs 2.41 ms)
       const int St = std::max(2, std::min(S, env_int("QAPB_FOLD_WS_STAGES", 2)));
-      const int ra = env_int("QAPB_FOLD_WS_ROWS", dsm ? 1 : 0);
+      // X1 / X2 pi rows: one padded 2-D TMA box per array (measured best),
+      // else 16-byte cp.async pieces; a dense stage (R = n-2) takes one bulk copy
+      const int ra = dense ? 0
+                     : env_int("QAPB_FOLD_WS_ROWS", (p.tmap_rows && R == n) ? 2 : (dsm ? 1 : 0));
+      if (ra == 2 && (!p.tmap_rows || R != n)) return cudaErrorInvalidValue;
       auto go = [&](auto kern) {
         allow_max_smem(kern);
-        kern<<<grid, kWsCT + 32, St * stage, st>>>(p, K, St, ra, R,
-                                                   env_int("QAPB_FOLD_SKIP_X3W", 0));
+        kern<<<grid, kWsCT + 32, St * stage, st>>>(
+            p, K, St, ra, R, x3w,
+            env_int("QAPB_FOLD_DBG", 0) | (env_int("QAPB_FOLD_HINTS", ra == 2 ? 3 : 0) << 8));
       };
       if (C == 2) {
         if (dsm) go(zfold_ws_kernel<2, true, true>);
@@ -2683,15 +2752,21 @@ cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t
     q.costs_are_d = costs_are_d ? 1 : 0;
     const int R = n, nrows = C * (n - 1), lp = n * (n - 1);
     const int c12p = (C * (n - 1) * (n - 2) + 15) & ~15;
-    const size_t stage =
-        (size_t)((((2 * nrows * R + lp * C + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) +
-                  2 * c12p + lp * C + 15) & ~15) * sizeof(double);
+    auto stage_of = [&](int p3n) {
+      return (size_t)((((2 * ((nrows * R + 15) & ~15) + p3n + 2 * ((nrows + 1) & ~1) + lp + 15) & ~15) +
+                       2 * c12p + lp * C + 15) & ~15) * sizeof(double);
+    };
+    const int x3w = (p.x3_group == 2 * C && env_int("QAPB_FOLD_X3_WHOLE", 1) &&
+                     stage_of(lp * p.x3_group) * 2 <= 210 * 1024) ? 1 : 0;
+    const size_t stage = stage_of(x3w ? lp * p.x3_group : lp * C);
     const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
     const int nwork = (q.ntriples + K - 1) / K * q.nchunks;
     const int grid = std::min(num_sms(), nwork);
+    const int ra = env_int("QAPB_FOLD_WS_ROWS", q.tmap_rows ? 2 : 1);
+    if (ra == 2 && !q.tmap_rows) return cudaErrorInvalidValue;
     auto go = [&](auto kern) {
       allow_max_smem(kern);
-      kern<<<grid, kWsCT + 32, 2 * stage, st>>>(q, K, 2, 1, R, 0);
+      kern<<<grid, kWsCT + 32, 2 * stage, st>>>(q, K, 2, ra, R, x3w, 0);
     };
     if (C == 2)
       go(zfold_ws_kernel<2, true, true, true>);
@@ -2913,6 +2988,25 @@ void encode_z_tmap(void* out128, const double* base, int n) {
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  std::memcpy(out128, &m, sizeof m);
+}
+
+void encode_rows_tmap(void* out128, const double* base, int n, int chunk) {
+  auto fn = tmap_encoder();
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled is not available");
+  const cuuint64_t nm2 = (cuuint64_t)(n - 2);
+  const cuuint64_t rows = (cuuint64_t)n * (n - 1) / 2 * n * (n - 1) * nm2;
+  const cuuint64_t dims[2] = {nm2, rows};
+  const cuuint64_t strides[1] = {nm2 * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)n, (cuuint32_t)(chunk * (n - 1))};
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (rows) failed: " + std::to_string((int)r));
   std::memcpy(out128, &m, sizeof m);
 }
 

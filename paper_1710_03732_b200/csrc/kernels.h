@@ -180,6 +180,9 @@ struct FoldParams {
   // element counts of d / x3buf / d3 (bounds checks of a -DQAPB_BOUNDS build)
   size_t nz, nx3, nd3;
   int costs_are_d;  // phase 2: the solve costs are D' (X3 members also in d3)
+  // RI: CUtensorMap (global, 64-byte aligned) of pi(z) as rows of n-2 with a
+  // box of {n, chunk*(n-1)} -- a unit's X1 / X2 rows, padded to n in smem
+  const void* tmap_rows;
 };
 
 // Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
@@ -273,6 +276,9 @@ cudaError_t launch_z_relayout(int n, const double* src, double* dst, int to_ri, 
 bool ri_supported(int n, int chunk, int x3_group);
 // CUtensorMap (128 bytes) of an RI z array for the Z-LAP tile copies
 void encode_z_tmap(void* out128, const double* base, int n);
+// pi(z) (RI) as a 2-D tensor of rows of n-2 doubles, box {n, chunk*(n-1)}:
+// a fold unit's X1 / X2 rows with two zero-filled pad columns (FoldParams::tmap_rows)
+void encode_rows_tmap(void* out128, const double* base, int n, int chunk);
 // theta of every rank's tile runs <-> one contiguous buffer (rank segments)
 // single-GPU X3 split: D' of the X3 members, tile layout <-> fold order
 cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, int ntriples,
