@@ -679,10 +679,12 @@ __global__ void __launch_bounds__(256, 2) zfold_lean_kernel(FoldParams P) {
       d3[ub + pair * C + pl] = dn;
       const uint32_t o = tb3 + pair * pstride + ((x3a[k] >> 12) & 63u);
       QAPB_CHECK(o < P.nz, "lean x3 store", o, P.nz);
-      if (fast)
-        incz[o] = dadd(dmul(omk, p3), gain);
-      else
-        d[o] = dn;
+      // scattered 8/16-byte pieces of tile rows: keep them in L2 until the
+      // other chunks' pieces complete the sectors (see zfold_ws_kernel)
+      double* dst = fast ? &incz[o] : &d[o];
+      const double v = fast ? dadd(dmul(omk, p3), gain) : dn;
+      if (P.l2_hints) st_hint(dst, v, policy_evict_last());
+      else *dst = v;
     }
     __syncthreads();  // the next triple's staging overwrites shared memory
   }
@@ -1431,12 +1433,16 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
         const uint32_t o = tb3 + pair * pstride + col;
         const double dl = delta(P1[i1], P2[i2], P3[((e >> lc) << sh) + p3o + (e & (C - 1))], 2);
+        const uint64_t pol = (hints & 1) ? policy_evict_last() : 0;
         if (P.costs_are_d) {  // X3 D': d3 authoritative, the tile copy follows
           const double v = dadd(V3[e], dl);
           d3[ub + e] = v;
-          costs[o] = v;
+          if (hints & 1) st_hint(&costs[o], v, pol);
+          else costs[o] = v;
         } else {
-          costs[o] = dadd(costs[o], dl);
+          const double v = dadd(costs[o], dl);
+          if (hints & 1) st_hint(&costs[o], v, pol);
+          else costs[o] = v;
         }
       }
       __syncwarp();
@@ -2735,7 +2741,9 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
     const int tpc = env_int("QAPB_FOLD_LEAN_TPC", 4);  // triples per CTA (0: persistent)
     const int R = tpc > 0 ? (p.ntriples + tpc - 1) / tpc
                           : std::max(1, std::min(p.ntriples, slots / p.nchunks));
-    kern<<<R * p.nchunks, 256, smem, st>>>(p);
+    FoldParams q = p;
+    q.l2_hints = env_int("QAPB_LEAN_HINTS", 1);
+    kern<<<R * p.nchunks, 256, smem, st>>>(q);
     return cudaGetLastError();
   }
   if (p.ri) return cudaErrorInvalidValue;  // the general fold reads the tile layout
@@ -2766,7 +2774,8 @@ cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t
     if (ra == 2 && !q.tmap_rows) return cudaErrorInvalidValue;
     auto go = [&](auto kern) {
       allow_max_smem(kern);
-      kern<<<grid, kWsCT + 32, 2 * stage, st>>>(q, K, 2, ra, R, x3w, 0);
+      kern<<<grid, kWsCT + 32, 2 * stage, st>>>(
+          q, K, 2, ra, R, x3w, env_int("QAPB_FOLD_HINTS", ra == 2 ? 1 : 0) << 8);
     };
     if (C == 2)
       go(zfold_ws_kernel<2, true, true, true>);

@@ -183,6 +183,7 @@ struct FoldParams {
   // RI: CUtensorMap (global, 64-byte aligned) of pi(z) as rows of n-2 with a
   // box of {n, chunk*(n-1)} -- a unit's X1 / X2 rows, padded to n in smem
   const void* tmap_rows;
+  int l2_hints;  // zfold_lean_kernel: X3 tile stores evict_last (QAPB_LEAN_HINTS)
 };
 
 // Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
