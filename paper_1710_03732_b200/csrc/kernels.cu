@@ -1132,9 +1132,12 @@ struct WsCells {
 
 // sh/off: the stage's X3 pi block holds 2^sh locations per pair, this
 // unit's first at `off` (C itself and 0 unless the whole x3buf group is staged)
+// Pe: valid locations of the chunk (a rank's last chunk may be partial); sl
+// (sharded): owner of each X3 cell's tile, kept as xr+1 in x3a bits 24..27
 template <int C, bool RI>
 __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, int R,
-                                         int sh = C == 2 ? 1 : 0, int off = 0) {
+                                         int sh = C == 2 ? 1 : 0, int off = 0, int Pe = C,
+                                         const ShardLocal* sl = nullptr) {
   const int nm1 = n - 1, nm2 = n - 2;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
   auto lpair = [&](int p, int q) { return p * nm1 + q - (q > p); };
@@ -1144,7 +1147,7 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
   for (int k = 0; k < kPipeSlots; ++k) {
     const int e = tid + k * kWsCT;
     w.rel[k] = 0xffffffffu;
-    if (e < c12) {
+    if (e < Pe * nm1 * nm2) {
       const int pa_l = e / (nm1 * nm2), rem = e - pa_l * nm1 * nm2;
       const int qi = rem / nm2, r = rem - qi * nm2;
       const int pa = pa0 + pa_l, q = qi + (qi >= pa);
@@ -1163,10 +1166,11 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
       const int pair = e / C, pa_l = e - pair * C;
       const int pb = pair / nm1, pci = pair - pb * nm1, pc = pci + (pci >= pb);
       const int pa = pa0 + pa_l;
-      if (pa != pb && pa != pc) {
+      if (pa_l < Pe && pa != pb && pa != pc) {
         const int j1 = pa_l * nm1 + pb - (pb > pa), j2 = pa_l * nm1 + pc - (pc > pa);
         // smem index of the X1 / X2 partner; its push row is that index / R
         w.x3a[k] = (uint32_t)colskip(pa, pb, pc) | ((uint32_t)pair << 8);
+        if (sl && sl->owner[pb] != sl->rank) w.x3a[k] |= (uint32_t)(sl->owner[pb] + 1) << 24;
         w.x3b[k] = (uint32_t)(j1 * R + colskip(pc, pa, pb)) |
                    ((uint32_t)(j2 * R + colskip(pb, pa, pc)) << 16);
       }
@@ -1184,7 +1188,13 @@ __device__ __forceinline__ void ws_cells(WsCells& w, int n, int pa0, int tid, in
 // box {R, nrows} over rows of n-2, the two pad columns zero-filled out of
 // bounds).  x3w: stage the unit's whole x3buf group (one bulk copy) instead
 // of its C locations in 16/8-byte pieces.
-template <int C, bool RI, bool DSM, bool PH2 = false>
+// SH (sharded, RI + DSM, C = 2): the CTA folds this rank's locations
+// [p_lo, p_hi) (the last chunk may be partial); X3 cells whose tile another
+// rank owns stage their D' from and store it to this rank's per-owner buffer
+// (ShardLocal::d3) and their new cost to the owner's cost buffer over NVLink
+// (ShardLocal::cost_send); their pi is in x3buf, gathered from the owners'
+// pushes by x3_gather_kernel before the fold.
+template <int C, bool RI, bool DSM, bool PH2 = false, bool SH = false>
 __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, int K, int S,
                                                                  int rows_async, int R,
                                                                  int x3w, int dbg) {
@@ -1198,6 +1208,13 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   if (P.stop && *P.stop) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
+  __shared__ ShardLocal sl;
+  int p_lo = 0, p_hi = P.m;
+  if constexpr (SH) {
+    shard_local_load(P.shard, P.m, &sl);
+    p_lo = sl.pbound[sl.rank];
+    p_hi = sl.pbound[sl.rank + 1];
+  }
   const int n = P.m, nm1 = n - 1, nm2 = n - 2;
   const int lpairs = n * nm1;
   const uint32_t esz = (uint32_t)(nm2 * nm2);
@@ -1246,15 +1263,18 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
 
   if (warp == kWsCW) {  // ---------------- producer warp ----------------
     const unsigned row_bytes = (unsigned)nm2 * 8u;
-    const unsigned tx = (rows_async == 0 ? 2u * nrows * row_bytes
-                         : rows_async == 2 ? 2u * nrows * R * 8u : 0u) +
-                        (unsigned)lpairs * 8u + (pieces ? 0u : (unsigned)p3n * 8u) +
-                        (DSM ? (unsigned)(2 * c12 + c3) * 8u : 0u);
+    const unsigned tx0 = (rows_async == 0 ? 2u * nrows * row_bytes
+                          : rows_async == 2 ? 2u * nrows * R * 8u : 0u) +
+                         (unsigned)lpairs * 8u + (pieces ? 0u : (unsigned)p3n * 8u) +
+                         (DSM ? (unsigned)c3 * 8u : 0u);
     int w = blockIdx.x, pos = (w / nch) * K;
     for (int u = 0; w < nwork; ++u, advance(w, pos)) {
       const int s = u % S;
       if (u >= S) mbar_wait(&empty[s], ((u / S) - 1) & 1);
-      const int T = tri(pos), ch = w % nch, pa0 = ch * C;
+      const int T = tri(pos), ch = w % nch, pr0 = ch * C, pa0 = p_lo + pr0;
+      const int Pe = min(C, p_hi - pa0);
+      const int c12e = Pe * nm1 * nm2;  // D' doubles of the unit's valid X1 / X2 rows
+      const unsigned tx = tx0 + (DSM ? 2u * (unsigned)c12e * 8u : 0u);
       const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
       const int fab = ix.fpair(a, b), fac = ix.fpair(a, c), fbc = ix.fpair(b, c);
       // the unit's first X1 / X2 row (location pair (pa0, ...))
@@ -1301,8 +1321,18 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         bulk_g2s(B + oU3, P.push + (size_t)fbc * lpairs, (unsigned)lpairs * 8u, &full[s]);
       if constexpr (DSM) {  // D' (costs) of the unit: X1 / X2 row blocks and its d3 block
         const double* src = PH2 ? P.costs : P.d;
-        const double* s3 = P.d3 + ((size_t)(P.tri0 + T) * nch + ch) * lpairs * C;
-        if (hints & 4) {
+        const size_t unit = (size_t)(P.tri0 + T) * nch + ch;
+        const double* s3 = P.d3 + unit * lpairs * C;
+        if constexpr (SH) {  // d3 of local pairs here, of each owner's pairs in sl.d3[xr]
+          if (lane < sl.world) {
+            const int x0 = sl.pbound[lane], nx = sl.pbound[lane + 1] - x0;
+            const double* s3x = lane == sl.rank ? s3 + (size_t)x0 * nm1 * C
+                                                : sl.d3[lane] + unit * nx * nm1 * C;
+            bulk_g2s(B + oV3 + x0 * nm1 * C, s3x, (unsigned)(nx * nm1 * C) * 8u, &full[s]);
+          }
+          if (lane == 29) bulk_g2s(B + oV1, src + tb1, (unsigned)c12e * 8u, &full[s]);
+          if (lane == 28) bulk_g2s(B + oV2, src + tb2, (unsigned)c12e * 8u, &full[s]);
+        } else if (hints & 4) {
           const uint64_t pol = policy_evict_first();
           if (lane == 29) bulk_g2s_hint(B + oV1, src + tb1, (unsigned)c12 * 8u, &full[s], pol);
           if (lane == 28) bulk_g2s_hint(B + oV2, src + tb2, (unsigned)c12 * 8u, &full[s], pol);
@@ -1313,9 +1343,9 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
           if (lane == 27) bulk_g2s(B + oV3, s3, (unsigned)c3 * 8u, &full[s]);
         }
       }
-      const int g0 = pa0 / Gx;
+      const int g0 = pr0 / Gx;  // x3buf groups count this rank's locations
       const size_t ugr = ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * Gx;
-      const size_t upi = ugr + (pa0 - g0 * Gx);
+      const size_t upi = ugr + (pr0 - g0 * Gx);
       if (!pieces) {  // contiguous: this unit's block (Gx == C) or its whole group
         if (lane == 30)
           bulk_g2s(B + oP3, P.x3buf + (Gx == C ? upi : ugr), (unsigned)p3n * 8u, &full[s]);
@@ -1327,7 +1357,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
             cp_async8(B + oP3 + e, P.x3buf + upi + (size_t)e * Gx);
         }
       }
-      for (int e = lane; e < nrows; e += 32) {  // push rows of the (a,b) / (a,c) tiles
+      for (int e = lane; e < Pe * nm1; e += 32) {  // push rows of the (a,b) / (a,c) tiles
         cp_async8(B + oU1 + e, P.push + (size_t)fab * lpairs + pa0 * nm1 + e);
         cp_async8(B + oU2 + e, P.push + (size_t)fac * lpairs + pa0 * nm1 + e);
       }
@@ -1352,12 +1382,14 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   const int lc = C == 2 ? 1 : 0;
   const int sh = p3n == c3 ? lc : (Gx == 4 ? 2 : Gx == 2 ? 1 : 3);
   auto p3off = [&](int ch_) { return p3n == c3 ? 0 : (ch_ * C) % Gx; };
-  ws_cells<C, RI>(cells, n, ch * C, tid, R, sh, p3off(ch));
+  auto pe_of = [&](int ch_) { return min(C, p_hi - (p_lo + ch_ * C)); };
+  const ShardLocal* slp = SH ? &sl : nullptr;
+  ws_cells<C, RI>(cells, n, p_lo + ch * C, tid, R, sh, p3off(ch), pe_of(ch), slp);
   // X1 / X2: base of the unit's rows (RI) or of its tiles' rows (cells add the
   // tile offset); X3: row a of the (b,c) tiles, + pair * pstride + col
   auto bases = [&](int T_, int ch_, uint32_t& tb1, uint32_t& tb2, uint32_t& tb3, size_t& ub) {
     const int a = P.triples[3 * T_], b = P.triples[3 * T_ + 1], c = P.triples[3 * T_ + 2];
-    const int pa0 = ch_ * C;
+    const int pa0 = p_lo + ch_ * C;
     if (RI) {
       tb1 = ((uint32_t)(ix.fpair(a, b) * nm2 + c - 2) * lpairs + pa0 * nm1) * nm2;
       tb2 = ((uint32_t)(ix.fpair(a, c) * nm2 + b - 1) * lpairs + pa0 * nm1) * nm2;
@@ -1493,12 +1525,23 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
       if (cells.x3b[k] == 0xffffffffu) continue;
       const int e = tid + k * kWsCT;
       const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
-      const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
+      const uint32_t pair = (cells.x3a[k] >> 8) & 0xffffu, col = cells.x3a[k] & 0xffu;
       const double p3 = P3[((e >> lc) << sh) + p3o + (e & (C - 1))], p1 = P1[i1], p2 = P2[i2];
       const double s1 = dadd(dmul(kz, p1), U1[i1 / (uint32_t)R]);
       const double s2 = dadd(dmul(kz, p2), U2[i2 / (uint32_t)R]);
       const double gain = dadd(dmul(phi, s1), dmul(phi, s2));
       const double dn = dadd(DSM ? V3[e] : D[2 * kPipeSlots + k], dsub(gain, dmul(kz, p3)));
+      if constexpr (SH) {
+        const int xr = (int)(cells.x3a[k] >> 24) - 1;
+        if (xr >= 0) {  // the tile is xr's: D' stays here, the new cost goes there (NVLink)
+          const int x0 = sl.pbound[xr], nx = sl.pbound[xr + 1] - x0;
+          const size_t gi = (((size_t)(P.tri0 + T) * nch + ch) * nx * nm1 +
+                             pair - (uint32_t)(x0 * nm1)) * C + (e & (C - 1));
+          sl.d3[xr][gi] = dn;
+          sl.cost_send[xr][gi] = fast ? dadd(dmul(omk, p3), gain) : dn;
+          continue;
+        }
+      }
       st(&d3[ub + e], dn);
       const uint32_t o = tb3 + pair * pstride + col;
       if (dbg & 1) continue;
@@ -1531,7 +1574,7 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
     T = T2;
     if (!pre) {  // new chunk: new cell pattern, then its D'
       ch = ch2;
-      ws_cells<C, RI>(cells, n, ch * C, tid, R, sh, p3off(ch));
+      ws_cells<C, RI>(cells, n, p_lo + ch * C, tid, R, sh, p3off(ch), pe_of(ch), slp);
       load_d(T, ch, Dn);
     }
     return true;
@@ -1543,6 +1586,37 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
   if (!PH2 && blockIdx.x == 0 && tid < n) {  // rlt2.cpp:297-298
     P.sa_fac[tid] = 0.0;
     P.sa_loc[tid] = 0.0;
+  }
+}
+
+// Sharded warp-specialised fold: the pi of this rank's families' X3 cells
+// whose tiles other ranks own arrives in pi_recv, pushed there by the owners'
+// Z-LAPs (the layout zfold_lean_kernel reads); copy it into those cells'
+// x3buf slots, so that the fold stages every pair's pi with one bulk copy.
+// One CTA per unit (triple, chunk of this rank's locations).
+__global__ void __launch_bounds__(256) x3_gather_kernel(FoldParams P) {
+  if (P.stop && *P.stop) return;
+  __shared__ ShardLocal sl;
+  shard_local_load(P.shard, P.m, &sl);
+  __syncthreads();
+  const int n = P.m, nm1 = n - 1, lpairs = n * nm1, C = P.chunk, nch = P.nchunks;
+  const int G = P.x3_group;
+  const int p_lo = sl.pbound[sl.rank], p_hi = sl.pbound[sl.rank + 1], W = p_hi - p_lo;
+  const int T = blockIdx.x / nch, ch = blockIdx.x - T * nch;
+  const int pr0 = ch * C, Pe = min(C, W - pr0);
+  const int a = P.triples[3 * T], b = P.triples[3 * T + 1], c = P.triples[3 * T + 2];
+  const DIdx ix(n);
+  const size_t rbT = (size_t)P.shard->rows_before[ix.fpair(b, c)];
+  const int g0 = pr0 / G;
+  const size_t upi =
+      ((size_t)(P.tri0 + T) * P.x3_ngroups + g0) * lpairs * G + (pr0 - g0 * G);
+  for (int e = threadIdx.x; e < lpairs * Pe; e += blockDim.x) {
+    const int pair = e / Pe, pl = e - pair * Pe;
+    const int xr = sl.owner[pair / nm1];
+    if (xr == sl.rank) continue;  // written by this rank's own Z-LAPs
+    const int x0 = sl.pbound[xr], nx = sl.pbound[xr + 1] - x0, lpl = pair - x0 * nm1;
+    const size_t xi = ((size_t)nx * nm1 * rbT + (size_t)lpl * b + a) * W + pr0 + pl;
+    P.x3buf[upi + (size_t)pair * G + pl] = sl.pi_recv[xr][xi];
   }
 }
 
@@ -2660,7 +2734,9 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
                      stage_of(lp * p.x3_group) * 2 <= 210 * 1024) ? 1 : 0;
     const size_t stage = stage_of(x3w ? lp * p.x3_group : lp * C);
     const int S = std::min(kWsMaxStages, (int)((210 * 1024) / stage));
-    if (p.x3buf && p.x3mode == 2 && !p.shard &&
+    // sharded engines (RI, chunk 2) run it too, with the X3 exchange (SH)
+    const bool ws_shard = p.shard && p.ri && dsm && C == 2 && env_int("QAPB_FOLD_WS_SHARDED", 1);
+    if (p.x3buf && p.x3mode == 2 && (!p.shard || ws_shard) &&
         (p.ri || (env_int("QAPB_FOLD_WS", 0) && env_int("QAPB_FOLD_PIPE", 1))) && n % 2 == 0 &&
         (C == 1 || (C == 2 && p.x3_group % 2 == 0)) && nz < 4294967295.0 &&
         C * (n - 1) * (n - 2) <= kPipeSlots * kWsCT && C * n * (n - 1) <= kPipeSlots * kWsCT &&
@@ -2682,7 +2758,10 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
             p, K, St, ra, R, x3w,
             env_int("QAPB_FOLD_DBG", 0) | (env_int("QAPB_FOLD_HINTS", ra == 2 ? 3 : 0) << 8));
       };
-      if (C == 2) {
+      if (ws_shard) {
+        x3_gather_kernel<<<p.ntriples * p.nchunks, 256, 0, st>>>(p);
+        go(zfold_ws_kernel<2, true, true, false, true>);
+      } else if (C == 2) {
         if (dsm) go(zfold_ws_kernel<2, true, true>);
         else p.ri ? go(zfold_ws_kernel<2, true, false>) : go(zfold_ws_kernel<2, false, false>);
       } else {
