@@ -234,6 +234,10 @@ void Engine::alloc() {
   nd_ = (size_t)tiles_ * esz_;
   ntriples_ = m * (m - 1) * (m - 2) / 6;
   chunk_ = fold_chunk(m);
+  // even n >= 20: two locations per fold unit, so that the row-interleaved
+  // layout and the warp-specialised fold apply (measured: n=20 fold 0.246 ->
+  // 0.210 ms, n=22 0.433 -> 0.317; below 20 the family-cube folds are faster)
+  if (m % 2 == 0 && m >= 20 && chunk_ > 2 && !std::getenv("QAPB_FOLD_CHUNK")) chunk_ = 2;
   nchunks_ = (m + chunk_ - 1) / chunk_;
   salloc(st_, &b_, nb_);
   salloc(st_, &c_, nc_);
@@ -624,6 +628,7 @@ void Engine::enqueue_sharded_z(int it) {
     p.sh = shard_dev_;
     p.fpair_ij = fpair_ij_;
     p.patch = (it > 0 && !cost_scatter_) ? 1 : 0;
+    if (env_int("QAPB_LAP_NOPATCH", 0)) p.patch = 0;  // timing experiment only (wrong results)
     if (split_) {  // local X3 members: slack into the fold-order split buffer
       p.x3buf = x3buf_;
       p.x3_group = x3_group_;

@@ -6,6 +6,7 @@
 // exception types again.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cstdint>
 #include <cstdio>
@@ -25,6 +26,41 @@
 #define QAP_API __attribute__((visibility("default")))
 
 namespace qap {
+// QAPB_FACADE_STATS=1: wall time spent per facade call kind, summed over
+// all threads, printed to stderr at exit (where a branch-and-bound spends its
+// node time).  Off: one getenv per process.
+namespace {
+enum StatKind { kStCollapse, kStEngine, kStRun, kStSnapshot, kStInit, kStKinds };
+struct FacadeStats {
+  std::atomic<long long> ns[kStKinds]{};
+  std::atomic<long long> calls[kStKinds]{};
+  std::atomic<long long> iterations{0};
+  bool on = std::getenv("QAPB_FACADE_STATS") != nullptr;
+  ~FacadeStats() {
+    if (!on) return;
+    static const char* names[kStKinds] = {"collapse_store", "AscentEngine()", "run()",
+                                          "snapshot()", "init_coefficients"};
+    for (int k = 0; k < kStKinds; ++k)
+      std::fprintf(stderr, "qapb facade: %-18s calls %8lld  total %9.3f s  mean %8.3f ms\n",
+                   names[k], calls[k].load(), ns[k].load() * 1e-9,
+                   calls[k] ? ns[k].load() * 1e-6 / calls[k].load() : 0.0);
+    std::fprintf(stderr, "qapb facade: iterations %lld\n", iterations.load());
+  }
+};
+FacadeStats g_stats;
+struct StatTimer {
+  StatKind k;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit StatTimer(StatKind kind) : k(kind) {}
+  ~StatTimer() {
+    if (!g_stats.on) return;
+    g_stats.ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                         std::chrono::steady_clock::now() - t0).count();
+    ++g_stats.calls[k];
+  }
+};
+}  // namespace
+
 namespace {
 
 void check(qapb_status rc) {
@@ -235,6 +271,7 @@ std::shared_ptr<qapb_store> on_device(const CoefficientStore& st, int device) {
 
 // rlt2.cpp:66-89: built in HBM by the init kernel (D' = 0), kept there
 QAP_API CoefficientStore init_coefficients(const QapInstance& inst) {
+  StatTimer timer(kStInit);
   if (inst.n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
   const double* lin = inst.linear.empty() ? nullptr : inst.linear.data();
   qapb_store* p = nullptr;
@@ -266,6 +303,7 @@ QAP_API double store_evaluate(const CoefficientStore& st, const std::vector<int>
 
 // rlt2.cpp:109-182, device to device; the child stays in HBM
 QAP_API CoefficientStore collapse_store(const CoefficientStore& st, int fac, int loc) {
+  StatTimer timer(kStCollapse);
   const int mc = st.m - 1;
   if (mc < 2) throw std::invalid_argument("collapse_store: store too small");
   std::shared_ptr<qapb_store> src = on_device(st, bank_device(0));
@@ -311,6 +349,7 @@ int bank_device(int requested) {
 
 QAP_API AscentEngine::AscentEngine(CoefficientStore store, const AscentConfig& cfg)
     : cfg_(cfg), m_(store.m) {
+  StatTimer timer(kStEngine);
   if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");
   cfg_.device = bank_device(cfg.device);
   const qapb_config c = to_c(cfg_);
@@ -360,11 +399,13 @@ QAP_API double AscentEngine::iterate() {
 }
 
 QAP_API BoundReport AscentEngine::run() {
+  StatTimer timer(kStRun);
   invalidate();
   std::vector<qapb_record> recs(std::max(1, cfg_.iter_limit));
   std::vector<int> cert(m_, -1);
   qapb_report r{};
   check(qapb_engine_run(h_, &r, recs.data(), (int)recs.size(), cert.data()));
+  if (g_stats.on) g_stats.iterations += r.iterations;
   return report_from(r, recs, cert, cfg_);
 }
 
@@ -408,6 +449,7 @@ QAP_API const CoefficientStore& AscentEngine::store() const {
 // device has less than a quarter of its memory free, the snapshot goes to the
 // host instead (host-resident store; collapse_store uploads it again).
 QAP_API CoefficientStore AscentEngine::snapshot() const {
+  StatTimer timer(kStSnapshot);
   size_t free_b = 0, total_b = 0;
   check(qapb_device_memory(cfg_.device, &free_b, &total_b));
   const size_t need = (nc_of(m_) + nd_of(m_) + (size_t)m_ * m_) * sizeof(double);
