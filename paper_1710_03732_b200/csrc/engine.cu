@@ -131,6 +131,40 @@ void sfree(cudaStream_t st, T*& p) {
   p = nullptr;
 }
 
+// Pinned host blocks for the engines' scalar mirrors, recycled for the life of
+// the process: cudaFreeHost synchronises the device, which would make every
+// branch-and-bound node's engine teardown wait for all other banks' work.
+constexpr size_t kPinnedBlock = 512;
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<void*> free_list;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* pool = new PinnedPool;  // never destroyed: engines may outlive statics
+  return *pool;
+}
+void* pinned_get() {
+  static_assert(sizeof(DevScalars) <= kPinnedBlock, "DevScalars");
+  PinnedPool& pp = pinned_pool();
+  std::lock_guard<std::mutex> lk(pp.mu);
+  std::vector<void*>& free_list = pp.free_list;
+  if (free_list.empty()) {
+    constexpr int kPer = 64;
+    char* slab = nullptr;
+    cuda_check(cudaMallocHost(reinterpret_cast<void**>(&slab), kPer * kPinnedBlock),
+               "cudaMallocHost");
+    for (int k = 0; k < kPer; ++k) free_list.push_back(slab + k * kPinnedBlock);
+  }
+  void* p = free_list.back();
+  free_list.pop_back();
+  return p;
+}
+void pinned_put(void* p) {
+  PinnedPool& pp = pinned_pool();
+  std::lock_guard<std::mutex> lk(pp.mu);
+  pp.free_list.push_back(p);
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : dflt;
@@ -200,9 +234,9 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
   init_state();
   double *df = nullptr, *dd = nullptr, *dl = nullptr;
   const size_t nn = (size_t)n * n;
-  dalloc(&df, nn);
-  dalloc(&dd, nn);
-  if (linear) dalloc(&dl, nn);
+  salloc(st_, &df, nn);
+  salloc(st_, &dd, nn);
+  if (linear) salloc(st_, &dl, nn);
   cuda_check(cudaMemcpyAsync(df, flow, nn * 8, cudaMemcpyHostToDevice, st_), "H2D flow");
   cuda_check(cudaMemcpyAsync(dd, dist, nn * 8, cudaMemcpyHostToDevice, st_), "H2D dist");
   if (linear)
@@ -213,10 +247,10 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
   split_gather();
   hS_.offset = 0.0;
   push_scalars();
+  sfree(st_, df);
+  sfree(st_, dd);
+  sfree(st_, dl);
   cuda_check(cudaStreamSynchronize(st_), "engine create");
-  cudaFree(df);
-  cudaFree(dd);
-  if (dl) cudaFree(dl);
 }
 
 void Engine::alloc() {
@@ -293,7 +327,7 @@ void Engine::alloc() {
     if (incz_) encode_z_tmap(h + 128, incz_, m);
     encode_z_tmap(h + 256, piz_, m);
     encode_rows_tmap(h + 384, piz_, m, chunk_);
-    dalloc(&tmaps_, sizeof h);  // cudaMalloc: 256-byte aligned
+    salloc(st_, &tmaps_, sizeof h);  // pool blocks are 256-byte aligned (CUtensorMap: 64)
     cuda_check(cudaMemcpyAsync(tmaps_, h, sizeof h, cudaMemcpyHostToDevice, st_),
                "H2D tensor maps");
     cuda_check(cudaStreamSynchronize(st_), "H2D tensor maps");
@@ -319,8 +353,7 @@ void Engine::alloc() {
   }
   salloc(st_, &counter_, stage_ev_.size() + 2);
   salloc(st_, &S_, 1);
-  cuda_check(cudaMallocHost(reinterpret_cast<void**>(&hSpin_), sizeof(DevScalars)),
-             "cudaMallocHost");
+  hSpin_ = static_cast<DevScalars*>(pinned_get());
   std::vector<int> tr;
   tr.reserve(3 * (size_t)ntriples_);
   for (int a = 0; a < m; ++a)
@@ -412,18 +445,22 @@ Engine::~Engine() {
     sfree(st_, *p);
   sfree(st_, S_);
   sfree(st_, sa_state_);
-  dfree(hist_bound_); dfree(hist_best_);
-  if (hist_t_) cudaFree(hist_t_);
-  if (hSpin_) cudaFreeHost(hSpin_);
+  sfree(st_, hist_bound_);
+  sfree(st_, hist_best_);
+  sfree(st_, hist_t_);
+  if (hSpin_) {
+    cudaStreamSynchronize(st_);  // no copy may still target the block
+    pinned_put(hSpin_);
+  }
   for (void* p : peer_maps_) cudaIpcCloseMemHandle(p);
   if (comm_ && barrier_) {  // no peer may still map my receive buffers
     barrier();
     cudaStreamSynchronize(st_);
   }
   for (auto* p : xbufs_) cudaFree(p);
-  if (tmaps_) cudaFree(tmaps_);
+  sfree(st_, tmaps_);
   if (shard_dev_) cudaFree(shard_dev_);
-  if (feas_bad_) cudaFree(feas_bad_);
+  sfree(st_, feas_bad_);
   if (rows_before_) cudaFree(rows_before_);
   if (barrier_) cudaFree(barrier_);
   if (theta_buf_) cudaFree(theta_buf_);
@@ -439,9 +476,9 @@ void Engine::ensure_hist(int need) {
   int cap = std::max(need, 2 * hist_cap_);
   double *nb = nullptr, *nbest = nullptr;
   unsigned long long* nt = nullptr;
-  dalloc(&nb, cap);
-  dalloc(&nbest, cap);
-  dalloc(&nt, 4 * (size_t)cap);
+  salloc(st_, &nb, cap);
+  salloc(st_, &nbest, cap);
+  salloc(st_, &nt, 4 * (size_t)cap);
   cuda_check(cudaMemsetAsync(nt, 0, 4 * (size_t)cap * sizeof(unsigned long long), st_),
              "memset");
   if (hist_cap_) {
@@ -454,9 +491,9 @@ void Engine::ensure_hist(int need) {
                "hist");
     cuda_check(cudaStreamSynchronize(st_), "hist");
   }
-  dfree(hist_bound_);
-  dfree(hist_best_);
-  if (hist_t_) cudaFree(hist_t_);
+  sfree(st_, hist_bound_);
+  sfree(st_, hist_best_);
+  sfree(st_, hist_t_);
   hist_bound_ = nb;
   hist_best_ = nbest;
   hist_t_ = nt;
@@ -494,7 +531,7 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
   for (int r = 0; r <= world_; ++r) shard_.pbound[r] = pb[r];
   p_lo_ = pb[rank_];
   p_hi_ = pb[rank_ + 1];
-  dalloc(&feas_bad_, 1);
+  salloc(st_, &feas_bad_, 1);
   if (world_ == 1) return;
   // fold chunks of my locations
   chunks_me_ = (p_hi_ - p_lo_ + chunk_ - 1) / chunk_;
@@ -1029,7 +1066,9 @@ void Engine::stage_times(int k, double* z, double* y, double* x) const {
   }
   if (!hist_t_ || k >= hist_cap_) return;
   unsigned long long t[4] = {0, 0, 0, 0};
-  cuda_check(cudaMemcpy(t, hist_t_ + 4 * (size_t)k, sizeof t, cudaMemcpyDeviceToHost), "D2H t");
+  cuda_check(cudaMemcpyAsync(t, hist_t_ + 4 * (size_t)k, sizeof t, cudaMemcpyDeviceToHost, st_),
+             "D2H t");
+  cuda_check(cudaStreamSynchronize(st_), "D2H t");
   auto ms = [](unsigned long long a, unsigned long long b) {
     return (a && b && b >= a) ? (double)(b - a) * 1e-6 : 0.0;
   };
@@ -1041,17 +1080,20 @@ void Engine::stage_times(int k, double* z, double* y, double* x) const {
 void Engine::fill_records(int from, int to, std::vector<qapb_record>* recs) const {
   if (!recs || to <= from) return;
   std::vector<double> bnd(to - from), bst(to - from);
-  cuda_check(cudaMemcpy(bnd.data(), hist_bound_ + from, (to - from) * 8, cudaMemcpyDeviceToHost),
+  cuda_check(cudaMemcpyAsync(bnd.data(), hist_bound_ + from, (to - from) * 8,
+                             cudaMemcpyDeviceToHost, st_),
              "D2H hist");
-  cuda_check(cudaMemcpy(bst.data(), hist_best_ + from, (to - from) * 8, cudaMemcpyDeviceToHost),
+  cuda_check(cudaMemcpyAsync(bst.data(), hist_best_ + from, (to - from) * 8,
+                             cudaMemcpyDeviceToHost, st_),
              "D2H hist");
   std::vector<unsigned long long> ts;  // device stage timestamps of these iterations
   if (hist_t_ && to <= hist_cap_) {
     ts.resize(4 * (size_t)(to - from));
-    cuda_check(cudaMemcpy(ts.data(), hist_t_ + 4 * (size_t)from, ts.size() * 8,
-                          cudaMemcpyDeviceToHost),
+    cuda_check(cudaMemcpyAsync(ts.data(), hist_t_ + 4 * (size_t)from, ts.size() * 8,
+                               cudaMemcpyDeviceToHost, st_),
                "D2H stage times");
   }
+  cuda_check(cudaStreamSynchronize(st_), "D2H hist");
   for (int k = from; k < to; ++k) {
     qapb_record r{};
     r.iteration = k + 1;
@@ -1122,7 +1164,8 @@ void Engine::run(qapb_report* rep, std::vector<qapb_record>* recs, std::vector<i
   if (to > from) {
     const int k = to - 1;
     double bnd = 0;
-    cuda_check(cudaMemcpy(&bnd, hist_bound_ + k, 8, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpyAsync(&bnd, hist_bound_ + k, 8, cudaMemcpyDeviceToHost, st_), "D2H");
+    cuda_check(cudaStreamSynchronize(st_), "D2H");
     last_rec_ = qapb_record{to, bnd, gap(), 0, 0, 0};
   }
 }
@@ -1132,14 +1175,18 @@ std::vector<int> Engine::certificate() const {
   std::vector<int> out;
   if (!hS_.has_cert) return out;
   out.resize(m_);
-  cuda_check(cudaMemcpy(out.data(), cert_, m_ * sizeof(int), cudaMemcpyDeviceToHost), "D2H cert");
+  cuda_check(cudaMemcpyAsync(out.data(), cert_, m_ * sizeof(int), cudaMemcpyDeviceToHost, st_),
+             "D2H cert");
+  cuda_check(cudaStreamSynchronize(st_), "D2H cert");
   return out;
 }
 
 std::vector<int> Engine::x_assignment() const {
   const DeviceGuard dg(dev_);
   std::vector<int> out(m_);
-  cuda_check(cudaMemcpy(out.data(), xrow_, m_ * sizeof(int), cudaMemcpyDeviceToHost), "D2H xrow");
+  cuda_check(cudaMemcpyAsync(out.data(), xrow_, m_ * sizeof(int), cudaMemcpyDeviceToHost, st_),
+             "D2H xrow");
+  cuda_check(cudaStreamSynchronize(st_), "D2H xrow");
   return out;
 }
 
@@ -1307,9 +1354,13 @@ void Engine::history(int from, int count, double* bounds, double* best) const {
     throw std::invalid_argument("history: range outside completed iterations");
   if (!count) return;
   if (bounds)
-    cuda_check(cudaMemcpy(bounds, hist_bound_ + from, count * 8, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpyAsync(bounds, hist_bound_ + from, count * 8, cudaMemcpyDeviceToHost,
+                               st_),
+               "D2H");
   if (best)
-    cuda_check(cudaMemcpy(best, hist_best_ + from, count * 8, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpyAsync(best, hist_best_ + from, count * 8, cudaMemcpyDeviceToHost, st_),
+               "D2H");
+  cuda_check(cudaStreamSynchronize(st_), "D2H");
 }
 
 double Engine::time_kernel(int kind, int reps) {
