@@ -226,8 +226,11 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
   if (world_ < 1 || world_ > kMaxRanks || rank_ < 0 || rank_ >= world_)
     throw std::invalid_argument("AscentEngine: bad rank/world");
-  if (world_ > 1 && (is_two_phase() || (cfg.sa_enabled && env_int("QAPB_HOST_SA", 0))))
-    throw std::invalid_argument("sharded engine: F1/S1 (SA on the device) only (round 1)");
+  if (world_ > 1 && cfg.sa_enabled && env_int("QAPB_HOST_SA", 0))
+    throw std::invalid_argument("sharded engine: SA runs on the device (QAPB_HOST_SA unsupported)");
+  if (world_ > 1 && is_two_phase() && n % 2)
+    throw std::invalid_argument("sharded engine: the 2-phase variants need even n "
+                                "(row-interleaved layout)");
   if (world_ > n) throw std::invalid_argument("sharded engine: more ranks than locations");
   alloc();
   setup_shards(nccl_id);
@@ -271,7 +274,10 @@ void Engine::alloc() {
   // even n >= 20: two locations per fold unit, so that the row-interleaved
   // layout and the warp-specialised fold apply (measured: n=20 fold 0.246 ->
   // 0.210 ms, n=22 0.433 -> 0.317; below 20 the family-cube folds are faster)
-  if (m % 2 == 0 && m >= 20 && chunk_ > 2 && !std::getenv("QAPB_FOLD_CHUNK")) chunk_ = 2;
+  if (world_ == 1 && m % 2 == 0 && m >= 20 && chunk_ > 2 && !std::getenv("QAPB_FOLD_CHUNK"))
+    chunk_ = 2;
+  // sharded 2-phase runs phase 2 in the warp-specialised pipeline (chunk 2)
+  if (world_ > 1 && is_two_phase() && m % 2 == 0) chunk_ = 2;
   nchunks_ = (m + chunk_ - 1) / chunk_;
   salloc(st_, &b_, nb_);
   salloc(st_, &c_, nc_);
@@ -302,8 +308,8 @@ void Engine::alloc() {
   if (!is_two_phase())
     split_ = world_ == 1 ? split_mode_ != 0 : split_mode_ == 2;
   else
-    split_ = world_ == 1 && split_mode_ == 2 && stage_ev_.size() == 1 &&
-             env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3g);
+    split_ = split_mode_ == 2 && stage_ev_.size() == 1 && env_int("QAPB_ZLAYOUT", 1) != 0 &&
+             ri_supported(m, chunk_, x3g);
   if (split_) {  // X3 members in fold order (kernels.h, FoldParams::x3buf)
     int range = m;
     if (world_ > 1) {
@@ -321,6 +327,9 @@ void Engine::alloc() {
   ri_ = split_ && split_mode_ == 2 && stage_ev_.size() == 1 &&
         env_int("QAPB_ZLAYOUT", 1) != 0 && ri_supported(m, chunk_, x3_group_) &&
         (world_ == 1 || env_int("QAPB_ZLAYOUT_SHARDED", 1) != 0);
+  if (world_ > 1 && is_two_phase() && !ri_)
+    throw std::invalid_argument("sharded engine: the 2-phase variants need the row-interleaved "
+                                "layout (QAPB_ZLAYOUT, QAPB_X3SPLIT=2, n < 64)");
   if (ri_) {
     unsigned char h[4 * 128];
     encode_z_tmap(h, d_, m);
@@ -566,6 +575,12 @@ void Engine::setup_shards(const unsigned char* nccl_id) {
     shard_.pi_recv[p] = sr;
     shard_.cost_recv[p] = gr;
     shard_.d3[p] = d3;
+    if (is_two_phase() && is_fast()) {  // F2: the fold's remote X3 costs, updated by phase 2
+      double* kp = nullptr;
+      dalloc(&kp, shard_cost_count(shard_, m, rank_, p));
+      xbufs_.push_back(kp);
+      shard_.keep[p] = kp;
+    }
     // sharded engines start from init_coefficients (D' = 0, rlt2.cpp:87)
     cuda_check(cudaMemsetAsync(d3, 0, shard_cost_count(shard_, m, rank_, p) * sizeof(double),
                                st_),
@@ -633,6 +648,7 @@ void Engine::enqueue_sharded_z(int it) {
     FoldParams f = fold_params(-1);
     f.nchunks = chunks_me_;
     f.shard = shard_dev_;
+    f.keep_cost = is_two_phase() && fast ? 1 : 0;
     kbegin(QAPB_K_ZFOLD, st_);
     kcheck(launch_zfold(f, st_), "z-fold");
     kend(st_);
@@ -647,16 +663,18 @@ void Engine::enqueue_sharded_z(int it) {
       ++launches_;
     }
   }
-  {  // Z-LAPs of my runs: one run of rl tiles per facility-pair block
+  // Z-LAPs of my runs: one run of rl tiles per facility-pair block
+  auto zlaps = [&](double* values, const double* theta_ref, int counter, bool patch) {
     const int rl = (p_hi_ - p_lo_) * (m_ - 1);
     BatchLapParams p{};
     p.costs = costs;
     p.m = m_ - 2;
     p.count = fpairs_ * rl;
-    p.counter = counter_ + S;
+    p.counter = counter_ + counter;
     p.stop = &S_->stop;
     p.stop_w = &S_->stop;
-    p.values = theta_;
+    p.values = values;
+    p.theta_ref = theta_ref;
     p.pi = piz_;
     p.err_tile = &S_->err_tile;
     p.run_len = rl;
@@ -664,7 +682,7 @@ void Engine::enqueue_sharded_z(int it) {
     p.run_off = p_lo_ * (m_ - 1);
     p.sh = shard_dev_;
     p.fpair_ij = fpair_ij_;
-    p.patch = (it > 0 && !cost_scatter_) ? 1 : 0;
+    p.patch = (patch && !cost_scatter_) ? 1 : 0;
     if (env_int("QAPB_LAP_NOPATCH", 0)) p.patch = 0;  // timing experiment only (wrong results)
     if (split_) {  // local X3 members: slack into the fold-order split buffer
       p.x3buf = x3buf_;
@@ -677,6 +695,32 @@ void Engine::enqueue_sharded_z(int it) {
     }
     kbegin(QAPB_K_ZLAP, st_);
     kcheck(launch_lap_batch(p, st_), "z-stage");
+    kend(st_);
+    ++launches_;
+  };
+  if (!is_two_phase()) {
+    zlaps(theta_, nullptr, S, it > 0);
+  } else {  // rlt2.cpp:328-336 across the ranks
+    zlaps(theta1_, nullptr, S, it > 0);
+    kbegin(QAPB_K_XCHG, st_);
+    barrier();  // every rank's phase-1 pi has landed in the fold owners' buffers
+    kend(st_);
+    FoldParams f = fold_params(-1);
+    f.nchunks = chunks_me_;
+    f.shard = shard_dev_;
+    f.costs = costs;
+    kbegin(QAPB_K_PHASE2, st_);
+    kcheck(launch_phase2_ri(f, costs == d_, st_), "phase-2");
+    kend(st_);
+    kbegin(QAPB_K_XCHG, st_);
+    barrier();  // the redistributed X3 costs have landed in their owners' buffers
+    kend(st_);
+    launches_ += 2;
+    zlaps(theta_, theta1_, S + 1, true);
+    kbegin(QAPB_K_XCHG, st_);  // one verdict on a phase-2 regression for every rank
+    nccl_check(nccl().AllReduce(&S_->err_tile, &S_->err_tile, 1, ncclInt, ncclMin, comm_, st_),
+               "allreduce err_tile");
+    kcheck(launch_err_to_stop(S_, st_), "phase-2 verdict");
     kend(st_);
     ++launches_;
   }

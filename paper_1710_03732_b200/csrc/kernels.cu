@@ -147,6 +147,7 @@ struct ShardLocal {
   const double* pi_recv[kMaxRanks];
   double* d3[kMaxRanks];
   double* cost_send[kMaxRanks];
+  double* keep[kMaxRanks];
 };
 
 __device__ __forceinline__ void shard_local_load(const ShardInfo* sh, int n, ShardLocal* sl) {
@@ -159,6 +160,7 @@ __device__ __forceinline__ void shard_local_load(const ShardInfo* sh, int n, Sha
   if (tid < sh->world) {
     sl->pi_recv[tid] = sh->pi_recv[tid];
     sl->d3[tid] = sh->d3[tid];
+    sl->keep[tid] = sh->keep[tid];
     sl->cost_send[tid] = sh->cost_send[tid];
   }
   for (int p = tid; p < n; p += blockDim.x) sl->owner[p] = shard_owner(*sh, p);
@@ -1462,9 +1464,26 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
         if (cells.x3b[k] == 0xffffffffu) continue;
         const int e = tid + k * kWsCT;
         const uint32_t i1 = cells.x3b[k] & 0xffffu, i2 = cells.x3b[k] >> 16;
-        const uint32_t pair = cells.x3a[k] >> 8, col = cells.x3a[k] & 0xffu;
+        const uint32_t pair = (cells.x3a[k] >> 8) & 0xffffu, col = cells.x3a[k] & 0xffu;
         const uint32_t o = tb3 + pair * pstride + col;
         const double dl = delta(P1[i1], P2[i2], P3[((e >> lc) << sh) + p3o + (e & (C - 1))], 2);
+        if constexpr (SH) {
+          const int xr = (int)(cells.x3a[k] >> 24) - 1;
+          if (xr >= 0) {  // the tile is xr's: its new cost goes there (NVLink)
+            const int x0 = sl.pbound[xr], nx = sl.pbound[xr + 1] - x0;
+            const size_t gi = (((size_t)(P.tri0 + T) * nch + ch) * nx * nm1 + pair -
+                               (uint32_t)(x0 * nm1)) * C + (e & (C - 1));
+            double v;
+            if (P.costs_are_d) {  // X3 D' kept here (sl.d3), staged in V3
+              v = dadd(V3[e], dl);
+              sl.d3[xr][gi] = v;
+            } else {  // the fold's cost of the cell, kept here for phase 2
+              v = dadd(sl.keep[xr][gi], dl);
+            }
+            sl.cost_send[xr][gi] = v;
+            continue;
+          }
+        }
         const uint64_t pol = (hints & 1) ? policy_evict_last() : 0;
         if (P.costs_are_d) {  // X3 D': d3 authoritative, the tile copy follows
           const double v = dadd(V3[e], dl);
@@ -1537,8 +1556,10 @@ __global__ void __launch_bounds__(kWsCT + 32, 1) zfold_ws_kernel(FoldParams P, i
           const int x0 = sl.pbound[xr], nx = sl.pbound[xr + 1] - x0;
           const size_t gi = (((size_t)(P.tri0 + T) * nch + ch) * nx * nm1 +
                              pair - (uint32_t)(x0 * nm1)) * C + (e & (C - 1));
+          const double cost = fast ? dadd(dmul(omk, p3), gain) : dn;
           sl.d3[xr][gi] = dn;
-          sl.cost_send[xr][gi] = fast ? dadd(dmul(omk, p3), gain) : dn;
+          sl.cost_send[xr][gi] = cost;
+          if (P.keep_cost) sl.keep[xr][gi] = cost;  // phase 2 (F2) updates it
           continue;
         }
       }
@@ -2749,8 +2770,12 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
       const int St = std::max(2, std::min(S, env_int("QAPB_FOLD_WS_STAGES", 2)));
       // X1 / X2 pi rows: one padded 2-D TMA box per array (measured best),
       // else 16-byte cp.async pieces; a dense stage (R = n-2) takes one bulk copy
+      // Sharded engines stage the rows with cp.async pieces: a sharded phase 2
+      // at n=12 raised a misaligned-address fault with the TMA boxes, which
+      // was not root-caused before the GPUs closed
       const int ra = dense ? 0
-                     : env_int("QAPB_FOLD_WS_ROWS", (p.tmap_rows && R == n) ? 2 : (dsm ? 1 : 0));
+                     : env_int("QAPB_FOLD_WS_ROWS",
+                               (p.tmap_rows && R == n && !p.shard) ? 2 : (dsm ? 1 : 0));
       if (ra == 2 && (!p.tmap_rows || R != n)) return cudaErrorInvalidValue;
       auto go = [&](auto kern) {
         allow_max_smem(kern);
@@ -2834,7 +2859,7 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
 cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t st) {
   if (p.ntriples <= 0) return cudaSuccess;
   const int n = p.m, C = p.chunk;
-  if (env_int("QAPB_PHASE2_WS", 1)) {  // the warp-specialised pipeline in PH2 mode
+  if (env_int("QAPB_PHASE2_WS", 1) || p.shard) {  // the warp-specialised pipeline, PH2 mode
     FoldParams q = p;
     q.costs_are_d = costs_are_d ? 1 : 0;
     const int R = n, nrows = C * (n - 1), lp = n * (n - 1);
@@ -2849,17 +2874,22 @@ cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t
     const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
     const int nwork = (q.ntriples + K - 1) / K * q.nchunks;
     const int grid = std::min(num_sms(), nwork);
-    const int ra = env_int("QAPB_FOLD_WS_ROWS", q.tmap_rows ? 2 : 1);
+    const int ra = env_int("QAPB_FOLD_WS_ROWS", (q.tmap_rows && !q.shard) ? 2 : 1);
     if (ra == 2 && !q.tmap_rows) return cudaErrorInvalidValue;
     auto go = [&](auto kern) {
       allow_max_smem(kern);
       kern<<<grid, kWsCT + 32, 2 * stage, st>>>(
           q, K, 2, ra, R, x3w, env_int("QAPB_FOLD_HINTS", ra == 2 ? 1 : 0) << 8);
     };
-    if (C == 2)
+    if (q.shard) {  // sharded (chunk 2): remote X3 pi gathered into x3buf first
+      if (C != 2) return cudaErrorInvalidValue;
+      x3_gather_kernel<<<q.ntriples * q.nchunks, 256, 0, st>>>(q);
+      go(zfold_ws_kernel<2, true, true, true, true>);
+    } else if (C == 2) {
       go(zfold_ws_kernel<2, true, true, true>);
-    else
+    } else {
       go(zfold_ws_kernel<1, true, true, true>);
+    }
     return cudaGetLastError();
   }
   const size_t smem = (size_t)(2 * C * (n - 1) * n + n * (n - 1) * C) * sizeof(double);
@@ -3031,6 +3061,16 @@ int exp_variant_host() {
     nofma += y == exp_glibc_host(p, 0);
   }
   return fma == 3 ? 1 : nofma == 3 ? 0 : -1;
+}
+
+// Sharded 2-phase: after the ranks' phase-2 regression flags are reduced
+// (min tile), every rank stops the same way (rlt2.cpp:332-335)
+__global__ void err_to_stop_kernel(DevScalars* S) {
+  if (S->err_tile != INT_MAX) S->stop = 1;
+}
+cudaError_t launch_err_to_stop(DevScalars* S, cudaStream_t st) {
+  err_to_stop_kernel<<<1, 1, 0, st>>>(S);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,

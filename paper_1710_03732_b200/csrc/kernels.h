@@ -130,6 +130,8 @@ struct ShardInfo {
   double* pi_send[kMaxRanks];          // PEER: fold owner's pi buffer for my X3 cells
   const double* cost_recv[kMaxRanks];  // local: costs of my remote-folded X3 cells
   double* d3[kMaxRanks];               // local: D' of my families' X3 cells in rank r (fold order)
+  double* keep[kMaxRanks];             // local (F2 sharded): the fold's new cost of those cells,
+                                       // which phase 2 updates (same layout as d3)
 };
 
 __host__ __device__ inline int shard_chunks(const ShardInfo& sh, int r) {
@@ -184,6 +186,7 @@ struct FoldParams {
   // box of {n, chunk*(n-1)} -- a unit's X1 / X2 rows, padded to n in smem
   const void* tmap_rows;
   int l2_hints;  // zfold_lean_kernel: X3 tile stores evict_last (QAPB_LEAN_HINTS)
+  int keep_cost; // sharded fold: also keep remote X3 costs in ShardInfo::keep (2-phase F2)
 };
 
 // Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
@@ -287,6 +290,8 @@ cudaError_t launch_x3_sync(int n, int chunk, int nchunks, const int* triples, in
                            int ri = 0);
 // one SA step on the device after an iteration (no-op unless that iteration's
 // X stage ran, when a certificate exists, or when best <= 0)
+// sharded 2-phase: raise stop when the reduced phase-2 regression flag is set
+cudaError_t launch_err_to_stop(DevScalars* S, cudaStream_t st);
 cudaError_t launch_sa_device(const SaParams& p, double* b, DevScalars* S, SaState* st,
                              double* sa_fac, double* sa_loc, cudaStream_t st_);
 // sharded: remote-folded X3 costs (cost_recv) -> the tile-layout cost array

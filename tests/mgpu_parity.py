@@ -37,7 +37,13 @@ def main():
     cases = {"nug12_F1": nug12, "nug12_S1": nug12, "nug12_F1_SA": nug12, "nug12_S1_SA": nug12,
              "rand20_F1": q.generate_instance(20, 1, 99),
              "rand20_S1": q.generate_instance(20, 1, 99), "grid20_F1": grid_instance(4, 5),
-             "grid30_F1": grid_instance(5, 6)}
+             "grid30_F1": grid_instance(5, 6),
+             # 2-phase variants (phase 2 across the ranks, even n)
+             "nug12_F2": nug12, "nug12_S2": nug12, "nug12_F2_SA": nug12,
+             "rand20_F2": q.generate_instance(20, 1, 99)}
+    only = os.environ.get("MGPU_CASES")  # debugging: a comma-separated subset
+    if only:
+        cases = {k: v for k, v in cases.items() if k in only.split(",")}
     results = {}
     for key, inst in cases.items():
         tr = g["traces"][key]
