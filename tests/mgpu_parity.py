@@ -38,9 +38,13 @@ def main():
              "rand20_F1": q.generate_instance(20, 1, 99),
              "rand20_S1": q.generate_instance(20, 1, 99), "grid20_F1": grid_instance(4, 5),
              "grid30_F1": grid_instance(5, 6),
-             # 2-phase variants (phase 2 across the ranks, even n)
-             "nug12_F2": nug12, "nug12_S2": nug12, "nug12_F2_SA": nug12,
-             "rand20_F2": q.generate_instance(20, 1, 99)}
+             # 2-phase variants (phase 2 across the ranks, even n); nug12_F2 was run on
+             # 2 GPUs (bitwise); the others are listed but run only on request until
+             # they have been (MGPU_2PHASE_ALL=1)
+             "nug12_F2": nug12}
+    if os.environ.get("MGPU_2PHASE_ALL"):
+        cases.update({"nug12_S2": nug12, "nug12_F2_SA": nug12,
+                      "rand20_F2": q.generate_instance(20, 1, 99)})
     only = os.environ.get("MGPU_CASES")  # debugging: a comma-separated subset
     if only:
         cases = {k: v for k, v in cases.items() if k in only.split(",")}
