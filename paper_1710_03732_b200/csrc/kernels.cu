@@ -1104,22 +1104,24 @@ __global__ void __launch_bounds__(512, 1) zfold_pipe_kernel(FoldParams P, int K)
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised z fold (single GPU, X3 split, n even; same arithmetic as
+// Warp-specialised z fold (X3 split, n even, chunk 1 or 2; same arithmetic as
 // zfold_kernel, rlt2.cpp:269-298).  Units are zfold_pipe_kernel's (triple T,
-// chunk of C locations pa), dealt the same way.  What changes is the
-// pipeline:
-//  * only the data other threads read is staged: pi(z) of the X1 / X2 rows
-//    (TMA bulk row copies into rows of pitch R = n (16-byte aligned rows;
-//    the transposed partner reads are then 2-way instead of 4-way bank
-//    conflicts), the unit's X3 pi (fold order) and the push rows.  That is
-//    ~50 KB per unit at n=30, so S = 4 stages fit and three units' loads are
-//    in flight while one is folded;
-//  * every D' value is read and written by the thread that owns the cell, so
-//    D' never goes through shared memory: each thread loads the D' of its
-//    cells of the NEXT unit into registers while it folds the current one;
-//  * one producer warp issues the copies; the 15 consumer warps wait on
-//    per-stage full barriers and release the stage with one arrive per warp
-//    on its empty barrier — no CTA-wide barrier in the loop.
+// chunk of C locations pa), dealt the same way: blocks of K triples of one
+// chunk, round-robin over the CTAs, so the chunks of a triple run at the same
+// time on neighbouring SMs.  One producer warp stages each unit into a ring of
+// S stages (full/empty mbarriers); 15 consumer warps fold it and release the
+// stage with one arrive per warp -- no CTA-wide barrier in the loop.  Per unit
+// (RI layout, the default; DESIGN.md section 4 has the measurements):
+//  * the X1 / X2 pi rows: one 2-D TMA box per array (rows padded to pitch
+//    R = n in shared memory, so the transposed partner reads see 2-way
+//    instead of 4-way bank conflicts), or 16-byte cp.async pieces;
+//  * the unit's X3 pi: its whole x3buf group in one bulk copy (x3w);
+//  * the push rows, and (DSM) the unit's D' blocks: X1 / X2 rows and d3;
+//  * consumers own their cells: X1 / X2 results leave as coalesced stores,
+//    the X3 tile pieces (16 bytes of each 224-byte row) with an evict_last L2
+//    policy so that the chunks' pieces merge into whole sectors in L2.
+// Without DSM, each thread instead loads the D' of its cells of the NEXT unit
+// into registers while it folds the current one.
 constexpr int kWsMaxStages = 8;
 // 15 consumer warps + 1 producer warp: 16 warps, so each SM sub-partition holds
 // 4 and a thread may use 128 registers (17 warps would cap it at 96).
