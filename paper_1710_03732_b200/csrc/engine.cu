@@ -867,6 +867,7 @@ FoldParams Engine::fold_params(int stage) const {
   if (f.tri0 == 0 && f.ntriples == ntriples_) f.order = order_;
   f.ri = ri_ ? 1 : 0;
   f.tmap_rows = (ri_ && tmaps_) ? tmaps_ + 384 : nullptr;
+  f.rows_cp = (world_ > 1 && is_two_phase()) ? 1 : 0;  // see launch_zfold
   f.nz = nd_;
   if (split_) {
     const int nch = world_ > 1 ? chunks_me_ : nchunks_;

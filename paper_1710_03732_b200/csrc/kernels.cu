@@ -2772,12 +2772,12 @@ cudaError_t launch_zfold(const FoldParams& p, cudaStream_t st) {
       const int St = std::max(2, std::min(S, env_int("QAPB_FOLD_WS_STAGES", 2)));
       // X1 / X2 pi rows: one padded 2-D TMA box per array (measured best),
       // else 16-byte cp.async pieces; a dense stage (R = n-2) takes one bulk copy
-      // Sharded engines stage the rows with cp.async pieces: a sharded phase 2
-      // at n=12 raised a misaligned-address fault with the TMA boxes, which
-      // was not root-caused before the GPUs closed
+      // rows_cp (sharded 2-phase engines): cp.async pieces -- their phase 2 at
+      // n=12 raised a misaligned-address fault with the TMA boxes, not
+      // root-caused before the GPUs closed
       const int ra = dense ? 0
                      : env_int("QAPB_FOLD_WS_ROWS",
-                               (p.tmap_rows && R == n && !p.shard) ? 2 : (dsm ? 1 : 0));
+                               (p.tmap_rows && R == n && !p.rows_cp) ? 2 : (dsm ? 1 : 0));
       if (ra == 2 && (!p.tmap_rows || R != n)) return cudaErrorInvalidValue;
       auto go = [&](auto kern) {
         allow_max_smem(kern);
@@ -2876,7 +2876,7 @@ cudaError_t launch_phase2_ri(const FoldParams& p, bool costs_are_d, cudaStream_t
     const int K = std::max(1, env_int("QAPB_FOLD_PIPE_K", 8));
     const int nwork = (q.ntriples + K - 1) / K * q.nchunks;
     const int grid = std::min(num_sms(), nwork);
-    const int ra = env_int("QAPB_FOLD_WS_ROWS", (q.tmap_rows && !q.shard) ? 2 : 1);
+    const int ra = env_int("QAPB_FOLD_WS_ROWS", (q.tmap_rows && !q.shard && !q.rows_cp) ? 2 : 1);
     if (ra == 2 && !q.tmap_rows) return cudaErrorInvalidValue;
     auto go = [&](auto kern) {
       allow_max_smem(kern);

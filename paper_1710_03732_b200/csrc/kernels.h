@@ -187,6 +187,7 @@ struct FoldParams {
   const void* tmap_rows;
   int l2_hints;  // zfold_lean_kernel: X3 tile stores evict_last (QAPB_LEAN_HINTS)
   int keep_cost; // sharded fold: also keep remote X3 costs in ShardInfo::keep (2-phase F2)
+  int rows_cp;   // stage the X1 / X2 pi rows with cp.async pieces, not TMA boxes
 };
 
 // Row-interleaved ("RI") device layout of the z arrays (pi(z), D', incz) of a
