@@ -194,9 +194,10 @@ ncclComm_t cached_comm(const ncclUniqueId& id, int world, int rank, int dev) {
 Engine::Engine(int m, const double* b, const double* c, const double* d, double offset,
                const qapb_config& cfg)
     : m_(m), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
-  const DeviceGuard dg(dev_);
+  // arguments first: a bad call fails the reference's way without touching the device
   if (m_ < 3) throw std::invalid_argument("AscentEngine: m >= 3 required");  // rlt2.cpp:209
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
+  const DeviceGuard dg(dev_);
   alloc();
   setup_shards(nullptr);
   init_state();
@@ -221,7 +222,7 @@ Engine::Engine(int m, const double* b, const double* c, const double* d, double 
 Engine::Engine(int n, const double* flow, const double* dist, const double* linear,
                const qapb_config& cfg, int rank, int world, const unsigned char* nccl_id)
     : rank_(rank), world_(world), m_(n), dev_(cfg.device), cfg_(cfg), rng_(cfg.seed) {
-  const DeviceGuard dg(dev_);
+  // arguments first: a bad call fails the reference's way without touching the device
   if (n < 3) throw std::invalid_argument("init_coefficients: n >= 3 required by RLT2");
   if (m_ > lap_max_m()) throw std::invalid_argument("AscentEngine: m too large for device LAP");
   if (world_ < 1 || world_ > kMaxRanks || rank_ < 0 || rank_ >= world_)
@@ -232,6 +233,7 @@ Engine::Engine(int n, const double* flow, const double* dist, const double* line
     throw std::invalid_argument("sharded engine: the 2-phase variants need even n "
                                 "(row-interleaved layout)");
   if (world_ > n) throw std::invalid_argument("sharded engine: more ranks than locations");
+  const DeviceGuard dg(dev_);
   alloc();
   setup_shards(nccl_id);
   init_state();
