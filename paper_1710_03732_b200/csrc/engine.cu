@@ -685,7 +685,6 @@ void Engine::enqueue_sharded_z(int it) {
     p.sh = shard_dev_;
     p.fpair_ij = fpair_ij_;
     p.patch = (patch && !cost_scatter_) ? 1 : 0;
-    if (env_int("QAPB_LAP_NOPATCH", 0)) p.patch = 0;  // timing experiment only (wrong results)
     if (split_) {  // local X3 members: slack into the fold-order split buffer
       p.x3buf = x3buf_;
       p.x3_group = x3_group_;
